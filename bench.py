@@ -1,0 +1,334 @@
+"""Benchmark of the lidarseg hot path on B200 (driver contract).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+                    [--config hdl64_batch] [--interval 1] [--frames F]
+
+A step = one pass of the whole hot path (bin -> mesh -> normals -> segment ->
+backfill -> prune) over one batch of F synthetic frames (BASELINE.json
+configs[3]: 512 HDL-64E-shape scans).  Each rank processes its own 512-frame
+batch (different poses), no data-path collective: "scaling": "weak".
+value = points processed by all ranks per second (device-resident inputs);
+e2e = the same through BatchPipeline with pinned host inputs, H2D of the
+points and D2H of the label grid inside the timed region.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+METRIC = "segmented points/sec (mesh+normals+labels), HDL-64E-shape scans"
+UNIT = "points/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="hdl64_batch")
+    ap.add_argument("--interval", type=int, default=1)
+    ap.add_argument("--frames", type=int, default=None)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--seed", type=int, default=2005)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+# Algorithmic bytes per stage of one pipeline launch over the batch (DESIGN.md
+# §Byte model): P points, C cells (F*R*S), Ck kept cells, N nodes.
+def stage_bytes(P, C, Ck, N):
+    return {
+        "bin_fill": 8 * C,
+        "bin": 16 * P + 8 * P,
+        "valid_bits": 8 * Ck + Ck / 8,
+        "frame_scan": Ck / 4,
+        "mesh": Ck / 4 + 4 * Ck + 24 * N,
+        "normals": 8 * Ck + 4 * Ck + 24 * N + 12 * N + 24 * N + N,
+        "uf_init": 4 * N,
+        "uf_union": 12 * N + 24 * N + N + 4 * N,
+        "uf_flatten": 8 * N,
+        "root_rank": 5 * N,
+        "label_dense": 4 * C + 4 * Ck + 9 * N,
+        "backfill": 4 * C + 8 * C + 4 * C,
+        "prune_plan": 0,
+        "prune_apply": 4 * C + 4 * C,
+    }
+
+
+def pipeline_bytes(P, C, N):
+    """B = 16 P + 8 C + 36 N + 4 C per batch."""
+    return 16 * P + 8 * C + 36 * N + 4 * C
+
+
+def cpu_baseline_port(shape, interval, seconds, seed):
+    """Oracle (NumPy port of the reference path) on 1 core, bounded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import lidarseg_oracle as oracle
+    from paper_2005_02704_b200 import synth
+    pts, nfr, t_used = 0, 0, 0.0
+    while t_used < seconds and nfr < 64:
+        xyz, ring, _ = synth.make_batch(shape, frames=1, seed=seed, first_frame=nfr)
+        xyz, ring = xyz.numpy(), ring.numpy()
+        t0 = time.perf_counter()
+        oracle.run_from_points(xyz, ring, shape.elevations, shape.steps, interval, shape.r_min, shape.r_max)
+        t_used += time.perf_counter() - t0
+        pts += xyz.shape[0]
+        nfr += 1
+    return {"value": pts / t_used, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{nfr} {shape.name} frames (k={interval}) through oracle/lidarseg_oracle.py "
+                      f"run_from_points, sequential, {t_used:.1f} s"}
+
+
+def _ref_worker(args):
+    xyz, ring, elev, steps, interval, rmin, rmax = args
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import lidarseg_oracle as oracle
+    oracle.run_from_points(xyz, ring, elev, steps, interval, rmin, rmax)
+    return xyz.shape[0]
+
+
+def run_reference(a, shape):
+    """--impl reference: the oracle port of the reference CPU path on all host cores."""
+    import multiprocessing as mp
+    from paper_2005_02704_b200 import synth
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    for var in ("OMP_NUM_THREADS", "MKL_NUM_THREADS", "OPENBLAS_NUM_THREADS"):
+        os.environ[var] = "1"
+    cores = os.cpu_count() or 1
+    per_step = max(cores, 2)
+    nuniq = min(per_step, 32)
+    frames = []
+    for f in range(nuniq):
+        xyz, ring, _ = synth.make_batch(shape, frames=1, seed=a.seed, first_frame=f)
+        frames.append((xyz.numpy(), ring.numpy(), shape.elevations, shape.steps, a.interval, shape.r_min,
+                       shape.r_max))
+    jobs = [frames[i % nuniq] for i in range(per_step)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        for _ in range(a.warmup):
+            pool.map(_ref_worker, jobs)
+        t0 = time.perf_counter()
+        pts = 0
+        for _ in range(a.steps):
+            pts += sum(pool.map(_ref_worker, jobs))
+        dt = time.perf_counter() - t0
+    v = pts / dt
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": dt / a.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded ray-cast scenes, BASELINE.json shapes)",
+            "impl": "reference",
+            "config": {"workload": f"{shape.name}: {per_step} frames per step (sample of the 512-frame batch)",
+                       "interval": a.interval},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{per_step} {shape.name} frames per step ({nuniq} distinct), "
+                                       f"multiprocessing pool of {cores} workers over frames"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    from paper_2005_02704_b200 import synth
+    shape = synth.CONFIGS[a.config]
+    if a.impl == "reference":
+        return run_reference(a, shape)
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2005_02704_b200 as L
+    from paper_2005_02704_b200 import _lib
+
+    F = a.frames or shape.frames
+    xyz, ring, off = synth.make_batch(shape, frames=F, seed=a.seed, device=dev, first_frame=rank * F)
+    P = int(xyz.shape[0])
+    cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
+                         r_max=shape.r_max)
+    bp = L.BatchPipeline(cfg, a.interval, frames=F, device=dev)
+    st = torch.cuda.current_stream()
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    for _ in range(max(a.warmup, 3)):
+        bp.run(xyz, ring, off)
+    torch.cuda.synchronize()
+    N = int(bp.n_nodes.sum().item())
+    C = F * cfg.rings * cfg.azimuth_steps
+    Ck = F * cfg.rings * bp.Sk
+
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    _lib.profile_begin()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(a.steps):
+        bp.run(xyz, ring, off)
+    e1.record(st)
+    torch.cuda.synchronize()
+    stages = _lib.profile_end()
+    clk = clocks.stop()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    tot_pts = torch.tensor([float(P)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(tot_pts)
+    ms = float(t.item())
+    ms_step = ms / a.steps
+    value = float(tot_pts.item()) * a.steps / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel + of the whole pipeline
+    peak, peak_kind = measured_peak_hbm()
+    sb = stage_bytes(P, C, Ck, N)
+    dom = max(stages, key=lambda k: stages[k][0]) if stages else None
+    roof = None
+    if dom:
+        dom_ms = stages[dom][0] / stages[dom][1]
+        ach = sb.get(dom, 0) / (dom_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "peak_kind": peak_kind,
+                "unit": "GB/s", "frac": ach / peak, "traffic": None, "ms_per_launch": dom_ms,
+                "share_of_step": stages[dom][0] / a.steps / ms_step,
+                "alg_bytes_per_launch": sb.get(dom, 0)}
+    pb = pipeline_bytes(P, C, N)
+    pipe_roof = {"alg_bytes_per_step": pb, "achieved_gbs": pb / (ms_step / 1e3) / 1e9,
+                 "frac": pb / (ms_step / 1e3) / 1e9 / peak, "frac_of_8tbs": pb / (ms_step / 1e3) / 1e9 / 8000.0}
+    stage_ms = {k: round(v[0] / v[1], 4) for k, v in stages.items()}
+
+    # ---- e2e through the public API with pinned host buffers
+    e2e = None
+    if not a.no_e2e:
+        hx = xyz.cpu().pin_memory()
+        hr = ring.cpu().pin_memory()
+        ho = off.cpu().pin_memory()
+        hl = torch.empty(bp.labels.shape, dtype=torch.int32).pin_memory()
+        dx, dr, do = torch.empty_like(xyz), torch.empty_like(ring), torch.empty_like(off)
+
+        def e2e_step():
+            dx.copy_(hx, non_blocking=True)
+            dr.copy_(hr, non_blocking=True)
+            do.copy_(ho, non_blocking=True)
+            bp.run(dx, dr, do)
+            hl.copy_(bp.labels, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e0.record(st)
+        for _ in range(a.steps):
+            e2e_step()
+        e1.record(st)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if ws > 1:
+            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+        h2d = hx.numel() * 4 + hr.numel() * 4 + ho.numel() * 8
+        e2e = {"value": float(tot_pts.item()) * a.steps / (float(te.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(hl.numel() * 4),
+               "ms_per_step": float(te.item()) / a.steps}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline_port(shape, a.interval, a.cpu_seconds, a.seed)
+
+    if rank == 0:
+        launches = sum(v[1] for v in stages.values())
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": a.steps,
+                "warmup": max(a.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded ray-cast scenes, BASELINE.json shapes)",
+                "config": {"workload": f"{shape.name}: {F} frames x {cfg.rings}x{cfg.azimuth_steps} per rank "
+                                       f"(BASELINE configs[3])", "interval": a.interval, "frames_per_rank": F,
+                           "points_per_rank": P, "nodes_per_rank": N, "parallelism": f"frame-shard x{ws}",
+                           "l2": "inputs (>1 GB per step) exceed the 126 MB L2; no flush needed"},
+                "frames_per_s": F * ws * a.steps / (ms / 1e3),
+                "roofline": roof, "pipeline_roofline": pipe_roof, "stage_ms": stage_ms,
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

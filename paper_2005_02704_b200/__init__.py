@@ -1,0 +1,18 @@
+"""lidarseg on B200: the per-scan hot path of arXiv 2005.02704 as sm_100a CUDA.
+
+Mirrors the reference package's public API for that path (reference
+pkg/src/lidarseg/__init__.py:21-35): data model, ``build_mesh``,
+``mesh_triangles``, ``estimate_normals``, ``segment``, ``backfill``,
+``prune_small``, ``run_pipeline``; adds ``bin_points`` and the batched
+``BatchPipeline``.  Every compute op runs through liblidarseg_b200.so (C ABI,
+include/lidarseg_b200.h); there is no CPU fallback.
+"""
+
+from .mesh import Mesh, build_mesh, mesh_triangles
+from .normals import NormalMap, estimate_normals, node_positions, normal_from_neighbors, normals_to_grid, point_normal
+from .pipeline import BatchPipeline, PipelineConfig, PipelineResult, bin_points, run_pipeline
+from .scan import (INVALID, GridIndex, Point3, ScanGrid, SensorConfig, polar_to_cartesian, subsample_steps,
+                   valid_point)
+from .segment import SegmenterConfig, backfill, prune_small, segment
+
+__version__ = "0.1.0"

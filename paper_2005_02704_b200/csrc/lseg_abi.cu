@@ -1,0 +1,320 @@
+// C ABI of lidarseg_b200 (declared in include/lidarseg_b200.h).
+//
+// Host-side validation mirrors the reference's ValueError contract
+// (scan.py:76-88, :223-224; segment.py:32-36); every entry point enqueues on
+// the caller's stream and returns without synchronising.
+
+#include <math.h>
+#include <stdio.h>
+
+#include <string>
+#include <vector>
+#include <cstring>
+
+#include "lseg_internal.cuh"
+#include "lseg_kernels.cuh"
+
+namespace lseg {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(int code, const std::string& msg) {
+  set_error(msg);
+  return code;
+}
+
+int check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(LSEG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return LSEG_OK;
+}
+
+// ---------------------------------------------------------------- profiler
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<const char*> names;  // names[i] = stage that ended at event i (nullptr = start mark)
+  size_t used = 0;
+};
+static thread_local Profiler g_prof;
+
+void prof_mark(const char* stage, cudaStream_t st) {
+  Profiler& p = g_prof;
+  if (!p.on) return;
+  if (p.used == p.pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    p.pool.push_back(e);
+  }
+  cudaEventRecord(p.pool[p.used], st);
+  if (p.names.size() <= p.used) p.names.resize(p.used + 1);
+  p.names[p.used] = stage;
+  ++p.used;
+}
+
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+Workspace carve(const Shape& s, int64_t label_bound, void* base) {
+  Workspace w{};
+  const int64_t K = label_bound > 0 ? label_bound : s.cap + 1;
+  w.K = K;
+  size_t off = 0;
+  char* b = static_cast<char*>(base);
+  auto take = [&](size_t bytes) -> char* {
+    char* p = b ? b + off : nullptr;
+    off += align_up(bytes);
+    return p;
+  };
+  const size_t words = (size_t)s.F * s.R * s.Wk;
+  w.vbits = reinterpret_cast<uint32_t*>(take(words * 4));
+  w.wpre = reinterpret_cast<int32_t*>(take(words * 4));
+  w.parent = reinterpret_cast<int32_t*>(take((size_t)s.F * s.cap * 4));
+  w.rank = reinterpret_cast<int32_t*>(take((size_t)s.F * s.cap * 4));
+  w.normals64 = reinterpret_cast<double*>(take((size_t)s.F * s.cap * 3 * 8));
+  w.hist = reinterpret_cast<int32_t*>(take((size_t)s.F * K * 4));
+  w.remap = reinterpret_cast<int32_t*>(take((size_t)s.F * K * 4));
+  w.fscal = reinterpret_cast<int32_t*>(take((size_t)s.F * 4 * 4));
+  w.lab_tmp = reinterpret_cast<int32_t*>(take((size_t)s.F * s.R * s.S * 4));
+  w.bytes = off;
+  return w;
+}
+
+static int check_sensor(const lseg_sensor* sn) {
+  if (!sn) return fail(LSEG_EINVAL, "sensor is NULL");
+  if (sn->rings < 2) return fail(LSEG_EINVAL, "ring_elevations needs at least 2 entries");
+  if (sn->steps < 3) return fail(LSEG_EINVAL, "azimuth_steps must be >= 3");
+  if (sn->steps > 16384) return fail(LSEG_EINVAL, "azimuth_steps > 16384 not supported");
+  if (!(0.0 < sn->r_min && sn->r_min < sn->r_max)) return fail(LSEG_EINVAL, "require 0 < r_min < r_max");
+  if (!sn->cos_el || !sn->sin_el || !sn->cos_az || !sn->sin_az)
+    return fail(LSEG_EINVAL, "sensor angle tables must be device pointers");
+  return LSEG_OK;
+}
+
+static int check_shape(int F, int R, int S, int k, Shape* out) {
+  if (F < 0) return fail(LSEG_EINVAL, "frames must be >= 0");
+  if (kept_count(S, k) < 0)
+    return fail(LSEG_EINVAL, "interval " + std::to_string(k) + " not in [1, " + std::to_string(S - 1) + "]");
+  *out = make_shape(F, R, S, k);
+  if (out->cap >= (int64_t)1 << 30) return fail(LSEG_EINVAL, "grid too large for int32 node ids");
+  return LSEG_OK;
+}
+
+static int check_ws(const Shape& s, int64_t label_bound, void* ws, size_t ws_bytes, Workspace* out) {
+  *out = carve(s, label_bound, ws);
+  if (!ws || ws_bytes < out->bytes)
+    return fail(LSEG_EWORKSPACE, "workspace too small: need " + std::to_string(out->bytes) + " bytes");
+  return LSEG_OK;
+}
+
+}  // namespace lseg
+
+using namespace lseg;
+
+extern "C" {
+
+const char* lseg_last_error(void) { return g_last_error.c_str(); }
+
+const char* lseg_version(void) { return "lidarseg_b200 0.1.0 sm_100a"; }
+
+int lseg_profile_begin(void) {
+  g_prof.on = true;
+  g_prof.used = 0;
+  return LSEG_OK;
+}
+
+int lseg_profile_end(char* names_csv, size_t names_cap, double* ms, int32_t* counts, int32_t max_stages,
+                     int32_t* n_stages) {
+  Profiler& p = g_prof;
+  p.on = false;
+  std::vector<std::string> order;
+  std::vector<double> tot;
+  std::vector<int> cnt;
+  if (p.used > 0 && cudaEventSynchronize(p.pool[p.used - 1]) != cudaSuccess)
+    return fail(LSEG_ECUDA, "profile_end: event sync failed");
+  for (size_t i = 1; i < p.used; ++i) {
+    if (!p.names[i]) continue;  // a start mark closes nothing
+    float t = 0.f;
+    cudaEventElapsedTime(&t, p.pool[i - 1], p.pool[i]);
+    size_t j = 0;
+    while (j < order.size() && order[j] != p.names[i]) ++j;
+    if (j == order.size()) { order.push_back(p.names[i]); tot.push_back(0.0); cnt.push_back(0); }
+    tot[j] += t;
+    cnt[j] += 1;
+  }
+  std::string csv;
+  const int n = (int)order.size() < max_stages ? (int)order.size() : max_stages;
+  for (int j = 0; j < n; ++j) {
+    if (j) csv += ",";
+    csv += order[j];
+    if (ms) ms[j] = tot[j];
+    if (counts) counts[j] = cnt[j];
+  }
+  if (names_csv && names_cap) {
+    strncpy(names_csv, csv.c_str(), names_cap - 1);
+    names_csv[names_cap - 1] = 0;
+  }
+  if (n_stages) *n_stages = n;
+  p.used = 0;
+  return LSEG_OK;
+}
+
+int32_t lseg_kept_count(int32_t steps, int32_t interval) { return kept_count(steps, interval); }
+
+size_t lseg_workspace_bytes(int32_t frames, int32_t rings, int32_t steps, int32_t interval,
+                            int64_t label_bound) {
+  if (kept_count(steps, interval) < 0 || frames < 0 || rings < 1) return 0;
+  return carve(make_shape(frames, rings, steps, interval), label_bound, nullptr).bytes;
+}
+
+int lseg_bin_points(const lseg_sensor* sensor, int32_t frames, const float* xyz, const int32_t* ring,
+                    const int64_t* frame_offsets, int64_t total_points, double* ranges, int32_t* cell,
+                    void* stream) {
+  if (int e = check_sensor(sensor)) return e;
+  if (frames < 0 || total_points < 0) return fail(LSEG_EINVAL, "negative sizes");
+  if (frames == 0) return LSEG_OK;
+  if (!ranges || !frame_offsets || (total_points > 0 && (!xyz || !ring)))
+    return fail(LSEG_EINVAL, "NULL buffer");
+  launch_bin(*sensor, frames, xyz, ring, frame_offsets, total_points, ranges, cell, (cudaStream_t)stream);
+  return check_launch("bin_points");
+}
+
+int lseg_build_mesh(const lseg_sensor* sensor, int32_t frames, int32_t interval, double max_edge_length,
+                    const double* ranges, int32_t* node_ids, int32_t* neighbors, int32_t* node_rings,
+                    int32_t* node_steps, int32_t* n_nodes, void* workspace, size_t workspace_bytes,
+                    void* stream) {
+  if (int e = check_sensor(sensor)) return e;
+  Shape sh;
+  if (int e = check_shape(frames, sensor->rings, sensor->steps, interval, &sh)) return e;
+  if (frames == 0) return LSEG_OK;
+  Workspace ws;
+  if (int e = check_ws(sh, 0, workspace, workspace_bytes, &ws)) return e;
+  if (!ranges || !node_ids || !neighbors || !n_nodes) return fail(LSEG_EINVAL, "NULL buffer");
+  launch_mesh(*sensor, sh, max_edge_length, ranges, ws, node_ids, neighbors, node_rings, node_steps, n_nodes,
+              (cudaStream_t)stream);
+  return check_launch("build_mesh");
+}
+
+int lseg_mesh_triangles(int32_t frames, int32_t rings, int32_t kept, const int32_t* node_ids, int32_t* tris,
+                        int32_t* n_tris, void* stream) {
+  if (frames < 0 || rings < 1 || kept < 1) return fail(LSEG_EINVAL, "bad shape");
+  if (frames == 0) return LSEG_OK;
+  if (!node_ids || !tris || !n_tris) return fail(LSEG_EINVAL, "NULL buffer");
+  launch_triangles(frames, rings, kept, node_ids, tris, n_tris, (cudaStream_t)stream);
+  return check_launch("mesh_triangles");
+}
+
+int lseg_estimate_normals(const lseg_sensor* sensor, int32_t frames, int32_t interval, const double* ranges,
+                          const int32_t* node_ids, const int32_t* neighbors, const int32_t* n_nodes,
+                          double* normals64, float* normals32, uint8_t* nmask, void* stream) {
+  (void)n_nodes;
+  if (int e = check_sensor(sensor)) return e;
+  Shape sh;
+  if (int e = check_shape(frames, sensor->rings, sensor->steps, interval, &sh)) return e;
+  if (frames == 0) return LSEG_OK;
+  if (!ranges || !node_ids || !neighbors || !nmask) return fail(LSEG_EINVAL, "NULL buffer");
+  launch_normals(*sensor, sh, ranges, node_ids, neighbors, normals64, normals32, nmask, (cudaStream_t)stream);
+  return check_launch("estimate_normals");
+}
+
+int lseg_segment(int32_t frames, int32_t rings, int32_t steps, int32_t interval, const int32_t* node_ids,
+                 const int32_t* neighbors, const int32_t* n_nodes, const double* normals64,
+                 const uint8_t* nmask, const double* thresholds, int32_t* labels, int32_t* n_labels,
+                 void* workspace, size_t workspace_bytes, void* stream) {
+  Shape sh;
+  if (int e = check_shape(frames, rings, steps, interval, &sh)) return e;
+  if (!thresholds) return fail(LSEG_EINVAL, "thresholds is NULL");
+  for (int c = 0; c < 3; ++c)
+    if (!(thresholds[c] > 0.0 && thresholds[c] <= 2.0)) return fail(LSEG_EINVAL, "thresholds must be in (0, 2]");
+  if (frames == 0) return LSEG_OK;
+  Workspace ws;
+  if (int e = check_ws(sh, 0, workspace, workspace_bytes, &ws)) return e;
+  if (!node_ids || !neighbors || !n_nodes || !normals64 || !nmask || !labels || !n_labels)
+    return fail(LSEG_EINVAL, "NULL buffer");
+  // all 6 slots: correct for any symmetric-or-not neighbour table a caller passes
+  launch_segment(sh, 6, node_ids, neighbors, n_nodes, normals64, nmask, thresholds, labels, n_labels, ws,
+                 nullptr, (cudaStream_t)stream);
+  return check_launch("segment");
+}
+
+int lseg_backfill(const lseg_sensor* sensor, int32_t frames, const double* ranges, const int32_t* labels_in,
+                  int32_t* labels_out, void* stream) {
+  if (int e = check_sensor(sensor)) return e;
+  if (frames < 0) return fail(LSEG_EINVAL, "frames must be >= 0");
+  if (frames == 0) return LSEG_OK;
+  if (!ranges || !labels_in || !labels_out) return fail(LSEG_EINVAL, "NULL buffer");
+  if (labels_in == labels_out) return fail(LSEG_EINVAL, "labels_in and labels_out must not alias");
+  const Shape sh = make_shape(frames, sensor->rings, sensor->steps, 1);
+  launch_ring_fill(0, *sensor, sh, ranges, labels_in, labels_out, nullptr, nullptr, nullptr, 0, 0,
+                   (cudaStream_t)stream);
+  return check_launch("backfill");
+}
+
+int lseg_prune_small(int32_t frames, int32_t rings, int32_t steps, const int32_t* labels_in,
+                     int32_t min_segment_size, int64_t label_bound, int32_t* labels_out, void* workspace,
+                     size_t workspace_bytes, void* stream) {
+  if (frames < 0 || rings < 1 || steps < 1) return fail(LSEG_EINVAL, "bad shape");
+  if (min_segment_size < 0) return fail(LSEG_EINVAL, "min_segment_size must be >= 0");
+  if (label_bound < 1) return fail(LSEG_EINVAL, "label_bound must be >= 1");
+  if (steps > 16384) return fail(LSEG_EINVAL, "steps > 16384 not supported");
+  if (frames == 0) return LSEG_OK;
+  if (!labels_in || !labels_out) return fail(LSEG_EINVAL, "NULL buffer");
+  if (labels_in == labels_out) return fail(LSEG_EINVAL, "labels_in and labels_out must not alias");
+  Shape shr = make_shape(frames, rings, steps < 2 ? 2 : steps, 1);
+  Workspace ws;
+  if (int e = check_ws(shr, label_bound, workspace, workspace_bytes, &ws)) return e;
+  shr.S = steps;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemsetAsync(ws.hist, 0, sizeof(int32_t) * (size_t)frames * label_bound, st);
+  launch_hist(shr, label_bound, labels_in, ws.hist, st);
+  launch_prune_plan(shr, nullptr, label_bound, min_segment_size, ws.hist, ws.remap, ws.fscal, st);
+  lseg_sensor dummy{};
+  dummy.rings = rings;
+  dummy.steps = steps;
+  launch_ring_fill(1, dummy, shr, nullptr, labels_in, labels_out, ws.hist, ws.remap, ws.fscal, label_bound,
+                   min_segment_size, st);
+  return check_launch("prune_small");
+}
+
+int lseg_run_pipeline(const lseg_sensor* sensor, int32_t frames, int32_t interval, const double* thresholds,
+                      int32_t min_segment_size, const float* xyz, const int32_t* ring,
+                      const int64_t* frame_offsets, int64_t total_points, double* ranges, int32_t* node_ids,
+                      int32_t* neighbors, float* normals32, uint8_t* nmask, int32_t* node_labels,
+                      int32_t* labels, int32_t* n_nodes, int32_t* n_labels, void* workspace,
+                      size_t workspace_bytes, void* stream) {
+  if (int e = check_sensor(sensor)) return e;
+  Shape sh;
+  if (int e = check_shape(frames, sensor->rings, sensor->steps, interval, &sh)) return e;
+  if (!thresholds) return fail(LSEG_EINVAL, "thresholds is NULL");
+  for (int c = 0; c < 3; ++c)
+    if (!(thresholds[c] > 0.0 && thresholds[c] <= 2.0)) return fail(LSEG_EINVAL, "thresholds must be in (0, 2]");
+  if (min_segment_size < 0) return fail(LSEG_EINVAL, "min_segment_size must be >= 0");
+  if (frames == 0) return LSEG_OK;
+  Workspace ws;
+  if (int e = check_ws(sh, 0, workspace, workspace_bytes, &ws)) return e;
+  if (!ranges || !node_ids || !neighbors || !nmask || !labels || !n_nodes || !n_labels || !frame_offsets)
+    return fail(LSEG_EINVAL, "NULL buffer");
+  cudaStream_t st = (cudaStream_t)stream;
+  prof_mark(nullptr, st);
+  launch_bin(*sensor, frames, xyz, ring, frame_offsets, total_points, ranges, nullptr, st);
+  launch_mesh(*sensor, sh, __builtin_nan(""), ranges, ws, node_ids, neighbors, nullptr, nullptr, n_nodes, st);
+  launch_normals(*sensor, sh, ranges, node_ids, neighbors, ws.normals64, normals32, nmask, st);
+  prof_mark("normals", st);
+  // node labels land in `labels` first when the caller does not want them kept
+  int32_t* nl = node_labels ? node_labels : labels;
+  launch_segment(sh, 3, node_ids, neighbors, n_nodes, ws.normals64, nmask, thresholds, nl, n_labels, ws,
+                 ws.hist, st);
+  // backfill nl -> lab_tmp (+ histogram of the filled grid), then prune lab_tmp -> labels
+  int32_t* filled = ws.lab_tmp;
+  launch_ring_fill(0, *sensor, sh, ranges, nl, filled, ws.hist, nullptr, nullptr, ws.K, 0, st);
+  prof_mark("backfill", st);
+  launch_prune_plan(sh, n_labels, ws.K, min_segment_size, ws.hist, ws.remap, ws.fscal, st);
+  prof_mark("prune_plan", st);
+  launch_ring_fill(1, *sensor, sh, nullptr, filled, labels, ws.hist, ws.remap, ws.fscal, ws.K, min_segment_size,
+                   st);
+  prof_mark("prune_apply", st);
+  return check_launch("run_pipeline");
+}
+
+}  // extern "C"

@@ -1,0 +1,24 @@
+// Kernel launchers (lseg_kernels.cu) used by the C ABI (lseg_abi.cu).
+#pragma once
+#include "lseg_internal.cuh"
+
+namespace lseg {
+void launch_bin(const lseg_sensor& sn, int F, const float* xyz, const int32_t* ring, const int64_t* off,
+                int64_t P, double* ranges, int32_t* cell, cudaStream_t st);
+void launch_mesh(const lseg_sensor& sn, const Shape& sh, double max_edge, const double* ranges,
+                 const Workspace& ws, int32_t* node_ids, int32_t* neighbors, int32_t* node_rings,
+                 int32_t* node_steps, int32_t* n_nodes, cudaStream_t st);
+void launch_normals(const lseg_sensor& sn, const Shape& sh, const double* ranges, const int32_t* node_ids,
+                    const int32_t* neighbors, double* n64, float* n32, uint8_t* nmask, cudaStream_t st);
+void launch_segment(const Shape& sh, int nslots, const int32_t* node_ids, const int32_t* neighbors,
+                    const int32_t* n_nodes, const double* n64, const uint8_t* nmask, const double* thr,
+                    int32_t* labels, int32_t* n_labels, const Workspace& ws, int32_t* hist, cudaStream_t st);
+void launch_ring_fill(int mode, const lseg_sensor& sn, const Shape& sh, const double* ranges,
+                      const int32_t* in, int32_t* out, int32_t* hist, const int32_t* remap,
+                      const int32_t* fscal, int64_t K, int32_t m, cudaStream_t st);
+void launch_prune_plan(const Shape& sh, const int32_t* n_labels, int64_t K, int32_t m, const int32_t* hist,
+                       int32_t* remap, int32_t* fscal, cudaStream_t st);
+void launch_hist(const Shape& sh, int64_t K, const int32_t* labels, int32_t* hist, cudaStream_t st);
+void launch_triangles(int F, int R, int Sk, const int32_t* node_ids, int32_t* tris, int32_t* n_tris,
+                      cudaStream_t st);
+}  // namespace lseg

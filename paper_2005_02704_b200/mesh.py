@@ -1,0 +1,120 @@
+"""Cylindrical 6-neighbour mesh, mirroring reference pkg/src/lidarseg/mesh.py.
+
+``build_mesh`` / ``mesh_triangles`` run on the GPU (C ABI lseg_build_mesh /
+lseg_mesh_triangles); the Mesh dataclass and its helpers are the reference's
+host-side view (mesh.py:30-80) so callers see identical objects.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from functools import cached_property
+
+import numpy as np
+import torch
+
+from . import _lib
+from .scan import ScanGrid, device_tables, subsample_steps
+
+SLOTS = ((1, 0), (1, 1), (0, 1), (-1, 0), (-1, -1), (0, -1))  # reference mesh.py:27
+
+
+@dataclass(frozen=True)
+class Mesh:
+    """Neighbour topology of the sub-sampled grid (node ids row-major over
+    (ring, kept position); ``neighbors`` slots N0..N5, -1 absent)."""
+
+    rings: int
+    full_steps: int
+    interval: int
+    kept_steps: np.ndarray
+    node_rings: np.ndarray
+    node_steps: np.ndarray
+    node_ids: np.ndarray
+    neighbors: np.ndarray
+    _dev: dict | None = field(default=None, repr=False, compare=False)
+
+    @property
+    def n_nodes(self) -> int:
+        return int(self.node_rings.size)
+
+    @cached_property
+    def degrees(self) -> np.ndarray:
+        return (self.neighbors >= 0).sum(axis=1)
+
+    def node_at(self, ring: int, step: int) -> int:
+        pos = np.searchsorted(self.kept_steps, step)
+        if pos >= self.kept_steps.size or self.kept_steps[pos] != step:
+            return -1
+        return int(self.node_ids[ring, pos])
+
+    def neighbor_cells(self, ring: int, step: int) -> list[tuple[int, int]]:
+        nid = self.node_at(ring, step)
+        if nid < 0:
+            raise ValueError(f"({ring}, {step}) is not a mesh node")
+        return [(int(self.node_rings[q]), int(self.node_steps[q])) for q in self.neighbors[nid] if q >= 0]
+
+    def edges(self) -> np.ndarray:
+        src = np.repeat(np.arange(self.n_nodes), 6)
+        dst = self.neighbors.reshape(-1)
+        ok = dst >= 0
+        pairs = np.stack([src[ok], dst[ok]], axis=1)
+        pairs.sort(axis=1)
+        return np.unique(pairs, axis=0)
+
+    # ---- device views (frame axis of 1) used to chain ops without re-upload
+    def device(self, device=None) -> dict:
+        if self._dev is not None:
+            return self._dev
+        dev = torch.device(device or "cuda")
+        Sk = self.kept_steps.size
+        cap = self.rings * Sk
+        nb = torch.full((1, cap, 6), -1, dtype=torch.int32)
+        nb[0, : self.n_nodes] = torch.from_numpy(np.ascontiguousarray(self.neighbors, dtype=np.int32))
+        d = {"node_ids": torch.from_numpy(np.ascontiguousarray(self.node_ids, np.int32)).to(dev).view(1, self.rings, Sk),
+             "neighbors": nb.to(dev),
+             "n_nodes": torch.tensor([self.n_nodes], dtype=torch.int32, device=dev)}
+        object.__setattr__(self, "_dev", d)
+        return d
+
+
+def build_mesh(grid: ScanGrid, interval: int, max_edge_length: float | None = None) -> Mesh:
+    """GPU build_mesh (reference mesh.py:105-136)."""
+    kept = subsample_steps(grid.config, interval)  # ValueError contract
+    L = _lib.lib()
+    cfg = grid.config
+    R, S, Sk = cfg.rings, cfg.azimuth_steps, kept.size
+    cap = R * Sk
+    dev = torch.device("cuda")
+    _, sn = device_tables(cfg, dev)
+    ranges = grid.device_ranges(dev)
+    node_ids = torch.empty((1, R, Sk), dtype=torch.int32, device=dev)
+    nbrs = torch.empty((1, cap, 6), dtype=torch.int32, device=dev)
+    node_rings = torch.empty((1, cap), dtype=torch.int32, device=dev)
+    node_steps = torch.empty((1, cap), dtype=torch.int32, device=dev)
+    n_nodes = torch.empty(1, dtype=torch.int32, device=dev)
+    wsb = _lib.workspace_bytes(1, R, S, interval)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    me = float("nan") if max_edge_length is None else float(max_edge_length)
+    _lib.check(L.lseg_build_mesh(sn, 1, int(interval), me, _lib.ptr(ranges), _lib.ptr(node_ids), _lib.ptr(nbrs),
+                                 _lib.ptr(node_rings), _lib.ptr(node_steps), _lib.ptr(n_nodes), _lib.ptr(ws), wsb,
+                                 _lib.stream_ptr()))
+    n = int(n_nodes.item())
+    return Mesh(rings=R, full_steps=S, interval=int(interval), kept_steps=kept,
+                node_rings=node_rings[0, :n].cpu().numpy(),
+                node_steps=node_steps[0, :n].cpu().numpy().astype(np.int64),
+                node_ids=node_ids[0].cpu().numpy(), neighbors=nbrs[0, :n].cpu().numpy(),
+                _dev={"node_ids": node_ids, "neighbors": nbrs, "n_nodes": n_nodes})
+
+
+def mesh_triangles(mesh: Mesh) -> np.ndarray:
+    """GPU mesh_triangles (reference mesh.py:173-189): (F, 3) node ids."""
+    L = _lib.lib()
+    d = mesh.device()
+    R, Sk = mesh.rings, mesh.kept_steps.size
+    dev = d["node_ids"].device
+    tris = torch.empty((1, 2 * R * Sk, 3), dtype=torch.int32, device=dev)
+    nt = torch.empty(1, dtype=torch.int32, device=dev)
+    _lib.check(L.lseg_mesh_triangles(1, R, Sk, _lib.ptr(d["node_ids"]), _lib.ptr(tris), _lib.ptr(nt),
+                                     _lib.stream_ptr()))
+    return tris[0, : int(nt.item())].cpu().numpy()

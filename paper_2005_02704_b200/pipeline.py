@@ -1,0 +1,150 @@
+"""End-to-end hot path, mirroring reference pkg/src/lidarseg/pipeline.py.
+
+* ``run_pipeline(scan, cfg, interval=None)`` — the reference's single-scan
+  entry point (pipeline.py:47-70): mesh -> normals -> segment -> backfill ->
+  prune on the GPU, stage timings from CUDA events.
+* ``bin_points(xyz, ring, config)`` — the new binning op.
+* ``BatchPipeline`` — the batched, device-resident form of the whole path
+  (points -> labels for F frames in one C-ABI call, lseg_run_pipeline); this
+  is what the benchmark measures.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .mesh import Mesh, build_mesh
+from .normals import NormalMap, estimate_normals_device
+from .scan import ScanGrid, SensorConfig, device_tables, subsample_steps
+from .segment import SegmenterConfig, backfill_device, prune_small_device, segment_device
+
+
+@dataclass(frozen=True)
+class PipelineConfig:
+    sensor: SensorConfig = field(default_factory=SensorConfig.default)
+    interval: int = 5
+    intervals: tuple = (5, 10, 15)
+    segmenter: SegmenterConfig = field(default_factory=SegmenterConfig)
+    eval: object = None       # reference EvalConfig (out of scope here)
+    baseline: object = None   # reference BaselineConfig (out of scope here)
+
+    def __post_init__(self):
+        if self.interval < 1:
+            raise ValueError("interval must be >= 1")
+        if not self.intervals or any(i < 1 for i in self.intervals):
+            raise ValueError("intervals must be positive")
+        object.__setattr__(self, "intervals", tuple(int(i) for i in self.intervals))
+
+
+@dataclass(frozen=True)
+class PipelineResult:
+    labels: np.ndarray
+    normals: NormalMap
+    mesh: Mesh
+    timings_ms: dict
+
+
+def bin_points(xyz, ring, config: SensorConfig) -> ScanGrid:
+    """Scatter f32 points (P,3) + ring ids (P,) into a ScanGrid (GPU, lseg_bin_points)."""
+    L = _lib.lib()
+    dev = torch.device("cuda")
+    x = torch.as_tensor(np.ascontiguousarray(xyz, dtype=np.float32)).reshape(-1, 3).to(dev)
+    r = torch.as_tensor(np.ascontiguousarray(ring, dtype=np.int32)).reshape(-1).to(dev)
+    if x.shape[0] != r.shape[0]:
+        raise ValueError("xyz and ring lengths differ")
+    _, sn = device_tables(config, dev)
+    off = torch.tensor([0, x.shape[0]], dtype=torch.int64, device=dev)
+    ranges = torch.empty((1, config.rings, config.azimuth_steps), dtype=torch.float64, device=dev)
+    _lib.check(L.lseg_bin_points(sn, 1, _lib.ptr(x), _lib.ptr(r), _lib.ptr(off), x.shape[0], _lib.ptr(ranges),
+                                 None, _lib.stream_ptr()))
+    out = ranges[0].cpu().numpy()
+    out[np.isnan(out)] = np.nan  # canonical NaN
+    return ScanGrid(config=config, ranges=out)
+
+
+def run_pipeline(scan: ScanGrid, cfg: PipelineConfig, interval: int | None = None) -> PipelineResult:
+    """GPU run_pipeline (reference pipeline.py:47-70)."""
+    interval = cfg.interval if interval is None else int(interval)
+    _lib.lib()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    ev[0].record()
+    mesh = build_mesh(scan, interval)
+    ev[1].record()
+    n64, _, mask = estimate_normals_device(scan, mesh)
+    ev[2].record()
+    node_labels, _ = segment_device(mesh, n64, mask, cfg.segmenter)
+    ev[3].record()
+    ranges = scan.device_ranges()
+    filled = backfill_device(scan.config, ranges.unsqueeze(0), node_labels)
+    labels = prune_small_device(filled, cfg.segmenter.min_segment_size, mesh.rings * mesh.kept_steps.size + 1)
+    ev[4].record()
+    torch.cuda.synchronize()
+    n = mesh.n_nodes
+    m = mask[0, :n].bool().cpu().numpy()
+    vals = n64[0, :n].cpu().numpy()
+    vals[~m] = np.nan
+    t = [ev[0].elapsed_time(ev[i]) for i in range(1, 5)]
+    timings = {"mesh": t[0], "normals": t[1] - t[0], "segment": t[2] - t[1], "backfill": t[3] - t[2], "total": t[3]}
+    return PipelineResult(labels=labels[0].cpu().numpy(), normals=NormalMap(values=vals, mask=m), mesh=mesh,
+                          timings_ms=timings)
+
+
+class BatchPipeline:
+    """Device-resident batched hot path: F frames of points -> labels.
+
+    Buffers are allocated once for (frames, points capacity); ``run`` takes
+    device tensors xyz (P,3) f32, ring (P,) i32, offsets (F+1,) i64 and
+    enqueues ONE C-ABI call (lseg_run_pipeline) on the current stream.
+    """
+
+    def __init__(self, config: SensorConfig, interval: int, segmenter: SegmenterConfig | None = None,
+                 frames: int = 1, device=None, keep_node_labels: bool = False):
+        self.L = _lib.lib()
+        self.config = config
+        self.interval = int(interval)
+        subsample_steps(config, interval)
+        self.seg = segmenter or SegmenterConfig()
+        self.frames = int(frames)
+        self.device = torch.device(device or "cuda")
+        R, S = config.rings, config.azimuth_steps
+        self.Sk = _lib.kept_count(S, interval)
+        self.cap = R * self.Sk
+        F, dev = self.frames, self.device
+        _, self.sn = device_tables(config, dev)
+        self.thr = _lib.thresholds_arg(self.seg.thresholds)
+        self.ranges = torch.empty((F, R, S), dtype=torch.float64, device=dev)
+        self.node_ids = torch.empty((F, R, self.Sk), dtype=torch.int32, device=dev)
+        self.neighbors = torch.empty((F, self.cap, 6), dtype=torch.int32, device=dev)
+        self.normals = torch.empty((F, self.cap, 3), dtype=torch.float32, device=dev)
+        self.nmask = torch.empty((F, self.cap), dtype=torch.uint8, device=dev)
+        self.node_labels = torch.empty((F, R, S), dtype=torch.int32, device=dev) if keep_node_labels else None
+        self.labels = torch.empty((F, R, S), dtype=torch.int32, device=dev)
+        self.n_nodes = torch.empty(F, dtype=torch.int32, device=dev)
+        self.n_labels = torch.empty(F, dtype=torch.int32, device=dev)
+        self.ws_bytes = _lib.workspace_bytes(F, R, S, interval)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+
+    def run(self, xyz, ring, offsets):
+        P = int(xyz.shape[0])
+        _lib.check(self.L.lseg_run_pipeline(
+            self.sn, self.frames, self.interval, self.thr, int(self.seg.min_segment_size), _lib.ptr(xyz),
+            _lib.ptr(ring), _lib.ptr(offsets), P, _lib.ptr(self.ranges), _lib.ptr(self.node_ids),
+            _lib.ptr(self.neighbors), _lib.ptr(self.normals), _lib.ptr(self.nmask), _lib.ptr(self.node_labels),
+            _lib.ptr(self.labels), _lib.ptr(self.n_nodes), _lib.ptr(self.n_labels), _lib.ptr(self.ws),
+            self.ws_bytes, _lib.stream_ptr()))
+        return self.labels
+
+    def frame(self, f: int) -> dict:
+        """Host copies of frame f's outputs (reference-shaped)."""
+        n = int(self.n_nodes[f].item())
+        m = self.nmask[f, :n].bool().cpu().numpy()
+        out = {"ranges": self.ranges[f].cpu().numpy(), "node_ids": self.node_ids[f].cpu().numpy(),
+               "neighbors": self.neighbors[f, :n].cpu().numpy(), "normals": self.normals[f, :n].cpu().numpy(),
+               "mask": m, "labels": self.labels[f].cpu().numpy(), "n_labels": int(self.n_labels[f].item())}
+        if self.node_labels is not None:
+            out["node_labels"] = self.node_labels[f].cpu().numpy()
+        return out

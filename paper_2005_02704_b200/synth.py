@@ -167,7 +167,9 @@ def cast_frame(shape: ScanShape, scene: dict, frame: int, seed: int, device="cpu
     ds = torch.stack([(ct * torch.cos(phi)[None]).expand(R, S),
                       (ct * torch.sin(phi)[None]).expand(R, S),
                       st.expand(R, S)], dim=-1).reshape(-1, 3)
-    tx, yaw_deg = shape.pose_step[0] * frame, shape.pose_step[1] * frame
+    # the object field repeats every 60 m along the sensor path so that every
+    # frame of a long batch still sees the scene (consecutive frames overlap)
+    tx, yaw_deg = (shape.pose_step[0] * frame) % 60.0, shape.pose_step[1] * frame
     yaw = math.radians(yaw_deg)
     rz = torch.tensor([[math.cos(yaw), -math.sin(yaw), 0.0],
                        [math.sin(yaw), math.cos(yaw), 0.0], [0.0, 0.0, 1.0]], **f64)
@@ -199,14 +201,15 @@ def cast_frame(shape: ScanShape, scene: dict, frame: int, seed: int, device="cpu
 
 
 def make_batch(shape: ScanShape | str, frames: int | None = None, seed: int = 0, device="cpu",
-               scene_seed: int | None = None):
-    """Frames of one config: returns xyz (P,3) f32, ring (P,) i32, offsets (F+1,) i64."""
+               scene_seed: int | None = None, first_frame: int = 0):
+    """Frames [first_frame, first_frame + frames) of one config: returns
+    xyz (P,3) f32, ring (P,) i32, offsets (F+1,) i64."""
     if isinstance(shape, str):
         shape = CONFIGS[shape]
     frames = shape.frames if frames is None else int(frames)
     scene = make_scene(shape, seed if scene_seed is None else scene_seed)
     xs, rs, offs = [], [], [0]
-    for f in range(frames):
+    for f in range(first_frame, first_frame + frames):
         x, r = cast_frame(shape, scene, f, seed, device)
         xs.append(x)
         rs.append(r)

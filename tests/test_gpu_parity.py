@@ -1,0 +1,158 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+reference's golden vectors.  Bit-exact for indices / labels; normals compared
+in fp64 (expected bit-exact, asserted to 1e-12) and in fp32 to 1e-5."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_names, load_golden
+
+pytestmark = pytest.mark.gpu
+
+PIPE = golden_names("vlp16") + golden_names("small") + golden_names("maxedge")
+
+
+@pytest.fixture(scope="module")
+def L():
+    import paper_2005_02704_b200 as L
+    return L
+
+
+def sensor(L, g):
+    return L.SensorConfig(ring_elevations=g["elev"], azimuth_steps=int(g["steps"]), r_min=float(g["r_min"]),
+                          r_max=float(g["r_max"]))
+
+
+@pytest.mark.parametrize("name", PIPE)
+def test_ops_match_golden(L, name):
+    g = load_golden(name)
+    cfg = sensor(L, g)
+    grid = L.ScanGrid(config=cfg, ranges=g["ranges"])
+    me = None if float(g["max_edge"]) < 0 else float(g["max_edge"])
+    mesh = L.build_mesh(grid, int(g["interval"]), max_edge_length=me)
+    np.testing.assert_array_equal(mesh.kept_steps, g["kept"])
+    np.testing.assert_array_equal(mesh.node_ids, g["node_ids"])
+    np.testing.assert_array_equal(mesh.neighbors, g["neighbors"])
+    np.testing.assert_array_equal(mesh.node_rings, g["node_rings"])
+    np.testing.assert_array_equal(mesh.node_steps, g["node_steps"])
+    np.testing.assert_array_equal(L.mesh_triangles(mesh), g["triangles"])
+    nm = L.estimate_normals(grid, mesh)
+    np.testing.assert_array_equal(nm.mask, g["nmask"])
+    m = nm.mask
+    np.testing.assert_allclose(nm.values[m], g["normals"][m], rtol=0, atol=1e-12)
+    exact = np.mean(nm.values[m] == g["normals"][m]) if m.any() else 1.0
+    assert exact == 1.0, f"fp64 normals not bit-exact: {exact:.6f}"
+    scfg = L.SegmenterConfig(*[float(t) for t in g["thr"]], min_segment_size=int(g["mseg"]))
+    dense = L.segment(mesh, nm, scfg)
+    np.testing.assert_array_equal(dense, g["node_dense"])
+    filled = L.backfill(grid, dense)
+    np.testing.assert_array_equal(filled, g["filled"])
+    np.testing.assert_array_equal(L.prune_small(filled, int(g["mseg"])), g["labels"])
+    if me is None:
+        res = L.run_pipeline(grid, L.PipelineConfig(sensor=cfg, interval=int(g["interval"]), segmenter=scfg))
+        np.testing.assert_array_equal(res.labels, g["labels"])
+        assert set(res.timings_ms) == {"mesh", "normals", "segment", "backfill", "total"}
+
+
+@pytest.mark.parametrize("name", golden_names("seg"))
+def test_segment_prescribed_normals(L, name):
+    g = load_golden(name)
+    cfg = L.SensorConfig(ring_elevations=g["elev"], azimuth_steps=int(g["steps"]))
+    grid = L.ScanGrid(config=cfg, ranges=g["ranges"])
+    mesh = L.build_mesh(grid, 1)
+    np.testing.assert_array_equal(mesh.neighbors, g["neighbors"])
+    nm = L.NormalMap(values=g["values"], mask=g["mask"])
+    dense = L.segment(mesh, nm, L.SegmenterConfig(*[float(t) for t in g["thr"]]))
+    np.testing.assert_array_equal(dense, g["node_dense"])
+
+
+@pytest.mark.parametrize("name", golden_names("fill"))
+def test_backfill_prune_golden(L, name):
+    g = load_golden(name)
+    cfg = L.SensorConfig(ring_elevations=g["elev"], azimuth_steps=int(g["steps"]))
+    grid = L.ScanGrid(config=cfg, ranges=g["ranges"])
+    filled = L.backfill(grid, g["labels_in"])
+    np.testing.assert_array_equal(filled, g["filled"])
+    np.testing.assert_array_equal(L.prune_small(filled, int(g["mseg"])), g["pruned"])
+
+
+@pytest.mark.parametrize("name", golden_names("vlp16"))
+def test_bin_points_golden(L, name):
+    g = load_golden(name)
+    grid = L.bin_points(g["xyz"], g["ring"], sensor(L, g))
+    np.testing.assert_array_equal(grid.ranges, g["ranges"])
+
+
+def _run_batch(L, shape_name, frames, k, seed=5):
+    from paper_2005_02704_b200 import synth
+    shape = synth.CONFIGS[shape_name]
+    xyz, ring, off = synth.make_batch(shape, frames=frames, seed=seed, device="cuda")
+    cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
+                         r_max=shape.r_max)
+    bp = L.BatchPipeline(cfg, k, frames=frames, keep_node_labels=True)
+    bp.run(xyz, ring, off)
+    torch.cuda.synchronize()
+    return shape, cfg, bp, xyz.cpu().numpy(), ring.cpu().numpy(), off.cpu().numpy()
+
+
+@pytest.mark.parametrize("shape_name,frames,k", [("vlp16", 3, 1), ("vlp16", 2, 5), ("hdl64", 2, 1),
+                                                  ("hdl64", 2, 5), ("os128", 1, 1), ("os128", 1, 5)])
+def test_batch_pipeline_vs_oracle(L, oracle, shape_name, frames, k):
+    shape, cfg, bp, xyz, ring, off = _run_batch(L, shape_name, frames, k)
+    for f in range(frames):
+        sl = slice(off[f], off[f + 1])
+        want = oracle.run_from_points(xyz[sl], ring[sl], shape.elevations, shape.steps, k, shape.r_min,
+                                      shape.r_max)
+        got = bp.frame(f)
+        np.testing.assert_array_equal(got["ranges"], want["ranges"])
+        np.testing.assert_array_equal(got["node_ids"], want["mesh"]["node_ids"])
+        np.testing.assert_array_equal(got["neighbors"], want["mesh"]["neighbors"])
+        np.testing.assert_array_equal(got["mask"], want["mask"])
+        m = want["mask"]
+        np.testing.assert_allclose(got["normals"][m], want["normals"][m], rtol=0, atol=1e-5)
+        np.testing.assert_array_equal(got["normals"][m], want["normals"][m].astype(np.float32))
+        np.testing.assert_array_equal(got["node_labels"], want["node_labels"])
+        np.testing.assert_array_equal(got["labels"], want["labels"])
+
+
+def test_stress_frame_vs_oracle(L, oracle):
+    shape, cfg, bp, xyz, ring, off = _run_batch(L, "stress", 1, 1, seed=9)
+    want = oracle.run_from_points(xyz, ring, shape.elevations, shape.steps, 1, shape.r_min, shape.r_max)
+    got = bp.frame(0)
+    np.testing.assert_array_equal(got["neighbors"], want["mesh"]["neighbors"])
+    np.testing.assert_array_equal(got["node_labels"], want["node_labels"])
+    np.testing.assert_array_equal(got["labels"], want["labels"])
+
+
+def test_determinism_and_empty_frames(L):
+    from paper_2005_02704_b200 import synth
+    shape = synth.CONFIGS["hdl64"]
+    xyz, ring, off = synth.make_batch(shape, frames=2, seed=1, device="cuda")
+    # frame 1 empty, frame 2 = frame 1 of the batch, frame 0 = frame 0
+    n0 = int(off[1])
+    off3 = torch.tensor([0, n0, n0, int(off[2])], dtype=torch.int64, device="cuda")
+    cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
+                         r_max=shape.r_max)
+    bp = L.BatchPipeline(cfg, 1, frames=3)
+    a = bp.run(xyz, ring, off3).clone()
+    b = bp.run(xyz, ring, off3).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    assert int(bp.n_nodes[1]) == 0 and int(bp.n_labels[1]) == 0
+    assert int(a[1].abs().sum()) == 0
+    bp1 = L.BatchPipeline(cfg, 1, frames=1)
+    bp1.run(xyz[n0:], ring[n0:], torch.tensor([0, int(off[2]) - n0], dtype=torch.int64, device="cuda"))
+    torch.cuda.synchronize()
+    assert torch.equal(bp1.labels[0], a[2])
+
+
+def test_value_errors(L):
+    cfg = L.SensorConfig.uniform(rings=4, azimuth_steps=8)
+    grid = L.ScanGrid(config=cfg, ranges=np.full((4, 8), 5.0))
+    with pytest.raises(ValueError):
+        L.build_mesh(grid, 0)
+    with pytest.raises(ValueError):
+        L.build_mesh(grid, 8)
+    with pytest.raises(ValueError):
+        L.SegmenterConfig(threshold_i=0.0)
