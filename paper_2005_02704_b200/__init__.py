@@ -10,7 +10,7 @@ include/lidarseg_b200.h); there is no CPU fallback.
 
 from .mesh import Mesh, build_mesh, mesh_triangles
 from .normals import NormalMap, estimate_normals, node_positions, normal_from_neighbors, normals_to_grid, point_normal
-from .pipeline import BatchPipeline, PipelineConfig, PipelineResult, bin_points, run_pipeline
+from .pipeline import BatchPipeline, PipelineConfig, PipelineResult, StreamingPipeline, bin_points, run_pipeline
 from .scan import (INVALID, GridIndex, Point3, ScanGrid, SensorConfig, polar_to_cartesian, subsample_steps,
                    valid_point)
 from .segment import SegmenterConfig, backfill, prune_small, segment

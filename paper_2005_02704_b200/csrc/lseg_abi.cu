@@ -77,6 +77,10 @@ Workspace carve(const Shape& s, int64_t label_bound, void* base) {
   w.remap = reinterpret_cast<int32_t*>(take((size_t)s.F * K * 4));
   w.fscal = reinterpret_cast<int32_t*>(take((size_t)s.F * 4 * 4));
   w.lab_tmp = reinterpret_cast<int32_t*>(take((size_t)s.F * s.R * s.S * 4));
+  w.bflags = reinterpret_cast<uint8_t*>(take((size_t)s.F * s.R * s.Sk));
+  w.fallback = reinterpret_cast<int32_t*>(take((size_t)s.F * 4));
+  w.rbits = reinterpret_cast<uint32_t*>(take(words * 4));
+  w.rpre = reinterpret_cast<int32_t*>(take(words * 4));
   w.bytes = off;
   return w;
 }
@@ -297,18 +301,15 @@ int lseg_run_pipeline(const lseg_sensor* sensor, int32_t frames, int32_t interva
     return fail(LSEG_EINVAL, "NULL buffer");
   cudaStream_t st = (cudaStream_t)stream;
   prof_mark(nullptr, st);
-  launch_bin(*sensor, frames, xyz, ring, frame_offsets, total_points, ranges, nullptr, st);
-  launch_mesh(*sensor, sh, __builtin_nan(""), ranges, ws, node_ids, neighbors, nullptr, nullptr, n_nodes, st);
-  launch_normals(*sensor, sh, ranges, node_ids, neighbors, ws.normals64, normals32, nmask, st);
-  prof_mark("normals", st);
-  // node labels land in `labels` first when the caller does not want them kept
-  int32_t* nl = node_labels ? node_labels : labels;
-  launch_segment(sh, 3, node_ids, neighbors, n_nodes, ws.normals64, nmask, thresholds, nl, n_labels, ws,
-                 ws.hist, st);
-  // backfill nl -> lab_tmp (+ histogram of the filled grid), then prune lab_tmp -> labels
+  if (sensor->steps <= 8192) {
+    launch_bin_fused(*sensor, sh, xyz, ring, frame_offsets, ws, ranges, n_nodes, st);
+  } else {
+    launch_bin(*sensor, frames, xyz, ring, frame_offsets, total_points, ranges, nullptr, st);
+    launch_valid_scan(*sensor, sh, ranges, ws, n_nodes, st);
+  }
+  launch_fused_graph(*sensor, sh, ws, ranges, thresholds, node_ids, neighbors, normals32, nmask, n_nodes, n_labels,
+                     node_labels, st);
   int32_t* filled = ws.lab_tmp;
-  launch_ring_fill(0, *sensor, sh, ranges, nl, filled, ws.hist, nullptr, nullptr, ws.K, 0, st);
-  prof_mark("backfill", st);
   launch_prune_plan(sh, n_labels, ws.K, min_segment_size, ws.hist, ws.remap, ws.fscal, st);
   prof_mark("prune_plan", st);
   launch_ring_fill(1, *sensor, sh, nullptr, filled, labels, ws.hist, ws.remap, ws.fscal, ws.K, min_segment_size,

@@ -81,7 +81,8 @@ __global__ void k_valid_bits(lseg_sensor sn, Shape sh, const double* __restrict_
 // --------------------------------------------------------------------------
 template <int T, int ITEMS>
 __global__ void __launch_bounds__(T) k_frame_scan(Shape sh, const uint32_t* __restrict__ vbits,
-                                                  int32_t* __restrict__ wpre, int32_t* __restrict__ n_nodes) {
+                                                  int32_t* __restrict__ wpre, int32_t* __restrict__ n_nodes,
+                                                  int32_t* __restrict__ hist, int64_t K) {
   using Scan = cub::BlockScan<int, T>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int carry;
@@ -111,6 +112,10 @@ __global__ void __launch_bounds__(T) k_frame_scan(Shape sh, const uint32_t* __re
     __syncthreads();
   }
   if (threadIdx.x == 0) n_nodes[f] = carry;
+  if (hist) {  // zero the histogram slots 0..count this frame's labels will use
+    int32_t* h = hist + (int64_t)f * K;
+    for (int64_t l = threadIdx.x; l <= carry; l += T) h[l] = 0;
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -190,8 +195,7 @@ __global__ void k_normals(lseg_sensor sn, Shape sh, const double* __restrict__ r
     const double* rf = ranges + (int64_t)f * sh.R * sh.S;
     const Vec3 p = cell_pos(sn, i, c * sh.k, __ldg(rf + (int64_t)i * sh.S + (int64_t)c * sh.k));
     const int64_t node = (int64_t)f * sh.cap + id;
-    double vx[6], vy[6], vz[6];
-    int cnt = 0;
+    Fan fan;
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       if (__ldg(neighbors + node * 6 + s) < 0) continue;
@@ -199,13 +203,10 @@ __global__ void k_normals(lseg_sensor sn, Shape sh, const double* __restrict__ r
       int c2 = c + slot_dc(s);
       c2 = c2 < 0 ? c2 + sh.Sk : (c2 >= sh.Sk ? c2 - sh.Sk : c2);
       const Vec3 q = cell_pos(sn, i2, c2 * sh.k, __ldg(rf + (int64_t)i2 * sh.S + (int64_t)c2 * sh.k));
-      vx[cnt] = __dsub_rn(q.x, p.x);
-      vy[cnt] = __dsub_rn(q.y, p.y);
-      vz[cnt] = __dsub_rn(q.z, p.z);
-      ++cnt;
+      fan.add(__dsub_rn(q.x, p.x), __dsub_rn(q.y, p.y), __dsub_rn(q.z, p.z));
     }
     double n[3];
-    const bool ok = fan_normal(vx, vy, vz, cnt, p, n);
+    const bool ok = fan.finish(p, n);
     if (!ok) n[0] = n[1] = n[2] = __longlong_as_double(0x7ff8000000000000LL);
     if (n64) { n64[node * 3] = n[0]; n64[node * 3 + 1] = n[1]; n64[node * 3 + 2] = n[2]; }
     if (n32) { n32[node * 3] = (float)n[0]; n32[node * 3 + 1] = (float)n[1]; n32[node * 3 + 2] = (float)n[2]; }
@@ -568,12 +569,36 @@ void launch_mesh(const lseg_sensor& sn, const Shape& sh, double max_edge, const 
   const int64_t nwords = (int64_t)sh.F * sh.R * sh.Wk;
   k_valid_bits<<<grid_for(nwords * 32, 256), 256, 0, st>>>(sn, sh, ranges, ws.vbits);
   prof_mark("valid_bits", st);
-  k_frame_scan<1024, 4><<<sh.F, 1024, 0, st>>>(sh, ws.vbits, ws.wpre, n_nodes);
+  k_frame_scan<1024, 4><<<sh.F, 1024, 0, st>>>(sh, ws.vbits, ws.wpre, n_nodes, nullptr, 0);
   prof_mark("frame_scan", st);
   const int64_t ncell = (int64_t)sh.F * sh.R * sh.Sk;
   k_mesh<<<grid_for(ncell, 256), 256, 0, st>>>(sn, sh, max_edge, ranges, ws.vbits, ws.wpre, node_ids,
                                                neighbors, node_rings, node_steps);
   prof_mark("mesh", st);
+}
+
+void launch_valid_scan(const lseg_sensor& sn, const Shape& sh, const double* ranges, const Workspace& ws,
+                       int32_t* n_nodes, cudaStream_t st) {
+  const int64_t nwords = (int64_t)sh.F * sh.R * sh.Wk;
+  k_valid_bits<<<grid_for(nwords * 32, 256), 256, 0, st>>>(sn, sh, ranges, ws.vbits);
+  prof_mark("valid_bits", st);
+  k_frame_scan<1024, 4><<<sh.F, 1024, 0, st>>>(sh, ws.vbits, ws.wpre, n_nodes, nullptr, 0);
+  prof_mark("frame_scan", st);
+}
+
+void launch_frame_scan(const Shape& sh, const Workspace& ws, int32_t* n_nodes, cudaStream_t st) {
+  k_frame_scan<1024, 4><<<sh.F, 1024, 0, st>>>(sh, ws.vbits, ws.wpre, n_nodes, nullptr, 0);
+  prof_mark("frame_scan", st);
+}
+
+void launch_scan_bits(const Shape& sh, const uint32_t* bits, int32_t* pre, int32_t* counts, int32_t* hist, int64_t K,
+                      cudaStream_t st) {
+  k_frame_scan<1024, 4><<<sh.F, 1024, 0, st>>>(sh, bits, pre, counts, hist, K);
+}
+
+void launch_root_rank(const Shape& sh, const int32_t* n_nodes, const int32_t* parent, const uint8_t* nmask,
+                      int32_t* rank, int32_t* n_labels, int32_t* hist, int64_t K, cudaStream_t st) {
+  k_root_rank<1024, 4><<<sh.F, 1024, 0, st>>>(sh, n_nodes, parent, nmask, rank, n_labels, hist, K);
 }
 
 void launch_normals(const lseg_sensor& sn, const Shape& sh, const double* ranges, const int32_t* node_ids,

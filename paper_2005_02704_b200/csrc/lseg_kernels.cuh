@@ -21,4 +21,16 @@ void launch_prune_plan(const Shape& sh, const int32_t* n_labels, int64_t K, int3
 void launch_hist(const Shape& sh, int64_t K, const int32_t* labels, int32_t* hist, cudaStream_t st);
 void launch_triangles(int F, int R, int Sk, const int32_t* node_ids, int32_t* tris, int32_t* n_tris,
                       cudaStream_t st);
+void launch_valid_scan(const lseg_sensor& sn, const Shape& sh, const double* ranges, const Workspace& ws,
+                       int32_t* n_nodes, cudaStream_t st);
+void launch_root_rank(const Shape& sh, const int32_t* n_nodes, const int32_t* parent, const uint8_t* nmask,
+                      int32_t* rank, int32_t* n_labels, int32_t* hist, int64_t K, cudaStream_t st);
+void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace& ws, const double* ranges,
+                        const double* thr, int32_t* node_ids, int32_t* neighbors, float* n32, uint8_t* nmask,
+                        int32_t* n_nodes, int32_t* n_labels, int32_t* node_labels, cudaStream_t st);
+void launch_bin_fused(const lseg_sensor& sn, const Shape& sh, const float* xyz, const int32_t* ring,
+                      const int64_t* off, const Workspace& ws, double* ranges, int32_t* n_nodes, cudaStream_t st);
+void launch_frame_scan(const Shape& sh, const Workspace& ws, int32_t* n_nodes, cudaStream_t st);
+void launch_scan_bits(const Shape& sh, const uint32_t* bits, int32_t* pre, int32_t* counts, int32_t* hist, int64_t K,
+                      cudaStream_t st);
 }  // namespace lseg

@@ -148,3 +148,71 @@ class BatchPipeline:
         if self.node_labels is not None:
             out["node_labels"] = self.node_labels[f].cpu().numpy()
         return out
+
+
+class StreamingPipeline:
+    """Host-to-host batched hot path with copy/compute overlap.
+
+    The batch is cut into chunks of ``chunk_frames``; for each chunk the
+    points are copied host->device on one stream, the pipeline runs on a
+    second, and the label grid is copied device->host on a third, double
+    buffered, so PCIe traffic in both directions overlaps the kernels.
+    Host buffers should be pinned (``torch.Tensor.pin_memory()``).
+    """
+
+    def __init__(self, config: SensorConfig, interval: int, segmenter: SegmenterConfig | None = None,
+                 chunk_frames: int = 64, max_chunk_points: int | None = None, device=None):
+        self.device = torch.device(device or "cuda")
+        self.cf = int(chunk_frames)
+        R, S = config.rings, config.azimuth_steps
+        self.maxp = int(max_chunk_points or self.cf * R * S)
+        self.bps = [BatchPipeline(config, interval, segmenter, frames=self.cf, device=self.device) for _ in range(2)]
+        self.xyz = [torch.empty((self.maxp, 3), dtype=torch.float32, device=self.device) for _ in range(2)]
+        self.ring = [torch.empty(self.maxp, dtype=torch.int32, device=self.device) for _ in range(2)]
+        self.off = [torch.empty(self.cf + 1, dtype=torch.int64, device=self.device) for _ in range(2)]
+        self.s_in, self.s_run, self.s_out = (torch.cuda.Stream(self.device) for _ in range(3))
+        self.freed = [torch.cuda.Event() for _ in range(2)]     # d2h of the chunk that used buffer b done
+        self.loaded = [torch.cuda.Event() for _ in range(2)]
+        self.computed = [torch.cuda.Event() for _ in range(2)]
+
+    def run_host(self, xyz_h, ring_h, offsets_h, labels_h):
+        """xyz_h (P,3) f32, ring_h (P,) i32, offsets_h (F+1,) i64 host tensors
+        (pinned); labels_h (F,R,S) i32 pinned output.  Enqueues everything and
+        returns; synchronise on the current stream to wait."""
+        F = offsets_h.numel() - 1
+        offs = offsets_h.tolist()
+        cur = torch.cuda.current_stream(self.device)
+        start = torch.cuda.Event()
+        start.record(cur)
+        for s in (self.s_in, self.s_run, self.s_out):
+            s.wait_event(start)
+        for ci, f0 in enumerate(range(0, F, self.cf)):
+            b = ci % 2
+            f1 = min(F, f0 + self.cf)
+            nf = f1 - f0
+            p0, p1 = offs[f0], offs[f1]
+            if p1 - p0 > self.maxp:
+                raise ValueError("chunk has more points than max_chunk_points")
+            bp = self.bps[b]
+            with torch.cuda.stream(self.s_in):
+                if ci >= 2:
+                    self.s_in.wait_event(self.freed[b])
+                self.xyz[b][: p1 - p0].copy_(xyz_h[p0:p1], non_blocking=True)
+                self.ring[b][: p1 - p0].copy_(ring_h[p0:p1], non_blocking=True)
+                loc = offsets_h[f0:f1 + 1] - p0
+                if nf < self.cf:  # pad the last chunk with empty frames
+                    loc = torch.cat([loc, loc[-1:].expand(self.cf - nf)])
+                self.off[b].copy_(loc, non_blocking=True)
+                self.loaded[b].record(self.s_in)
+            with torch.cuda.stream(self.s_run):
+                self.s_run.wait_event(self.loaded[b])
+                bp.run(self.xyz[b], self.ring[b], self.off[b])
+                self.computed[b].record(self.s_run)
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(self.computed[b])
+                labels_h[f0:f1].copy_(bp.labels[:nf], non_blocking=True)
+                self.freed[b].record(self.s_out)
+        cur.wait_stream(self.s_out)
+        cur.wait_stream(self.s_run)
+        cur.wait_stream(self.s_in)
+        return labels_h

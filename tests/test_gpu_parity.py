@@ -156,3 +156,30 @@ def test_value_errors(L):
         L.build_mesh(grid, 8)
     with pytest.raises(ValueError):
         L.SegmenterConfig(threshold_i=0.0)
+
+
+def test_unsorted_points_take_generic_binning(L):
+    """Shuffled (non ring-major) input and out-of-range ring ids give the same
+    result as ring-major input (k_bin_rows flags the frame, k_bin_atomic bins it)."""
+    from paper_2005_02704_b200 import synth
+    shape = synth.CONFIGS["vlp16"]
+    xyz, ring, off = synth.make_batch(shape, frames=2, seed=4, device="cuda")
+    cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
+                         r_max=shape.r_max)
+    bp = L.BatchPipeline(cfg, 1, frames=2)
+    want = bp.run(xyz, ring, off).clone()
+    want_r = bp.ranges.clone()
+    n0 = int(off[1])
+    g = torch.Generator(device="cuda")
+    g.manual_seed(0)
+    perm = torch.randperm(int(off[2]) - n0, device="cuda", generator=g) + n0
+    idx = torch.cat([torch.arange(n0, device="cuda"), perm])
+    xs, rs = xyz[idx].contiguous(), ring[idx].contiguous()
+    # extra points with invalid ring ids in frame 1 must be ignored
+    xs = torch.cat([xs, torch.ones((3, 3), device="cuda")])
+    rs = torch.cat([rs, torch.tensor([-1, shape.rings, 99], dtype=torch.int32, device="cuda")])
+    off2 = torch.tensor([0, n0, xs.shape[0]], dtype=torch.int64, device="cuda")
+    got = bp.run(xs, rs, off2)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+    assert torch.equal(torch.nan_to_num(bp.ranges, nan=-1.0), torch.nan_to_num(want_r, nan=-1.0))
