@@ -109,18 +109,20 @@ def measured_peak_hbm():
 # §5): P points, C cells (F*R*S), Ck kept cells (F*R*S'), N mesh nodes.  Each
 # entry is the compulsory HBM traffic of that kernel's inputs and outputs.
 def stage_bytes(P, C, Ck, N):
-    bnd = Ck * (1.0 / 8 + 1.0 / 64)  # tile-boundary cells (8 x 64 tiles)
+    bnd = Ck * (2.0 / 16 + 2.0 / 64)  # tile-border cells (16 x 64 tiles)
     return {
         "bin_rows": 16 * P + 8 * C + Ck / 8,           # points in, f64 grid + valid bits out
         "bin_fallback": 0,                             # no-op unless the input is not ring-major
         "frame_scan": Ck / 4,                          # valid bits in, word prefix out
-        "tile": 8 * Ck + Ck / 4 + 4 * Ck + 24 * N + 12 * N + N + 4 * Ck + bnd,
-        "merge": 2 * bnd,
-        "root_bits": 4 * Ck + Ck / 8,
+        # ranges + valid bits in; node ids, neighbours, normals, mask, parent,
+        # fp64 border normals (first/last row and column of 16 x 64 tiles) out
+        "tile": 8 * Ck + Ck / 4 + 4 * Ck + 24 * N + 12 * N + N + 4 * Ck + 24 * bnd,
+        "merge": 4 * bnd + 24 * bnd,
+        "root_flatten": 4 * Ck + Ck / 8,
         "root_scan": Ck / 4,
-        "labels_backfill": 4 * Ck + Ck / 2 + 8 * (C - Ck) + 4 * C,
-        "prune_plan": 0,
-        "prune_apply": 8 * C,
+        "labels_backfill": 4 * Ck + Ck / 8 + 8 * (C - Ck) + 4 * C,
+        "prune_plan": Ck / 8 + Ck / 4,
+        "prune_apply": 8 * C + Ck / 4,
         # single-op (unfused) path stages
         "bin_fill": 8 * C, "bin": 24 * P, "valid_bits": 8 * Ck, "mesh": 4 * Ck + 24 * N,
         "normals": 12 * Ck + 24 * N + 37 * N,

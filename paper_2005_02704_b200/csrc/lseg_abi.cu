@@ -77,10 +77,13 @@ Workspace carve(const Shape& s, int64_t label_bound, void* base) {
   w.remap = reinterpret_cast<int32_t*>(take((size_t)s.F * K * 4));
   w.fscal = reinterpret_cast<int32_t*>(take((size_t)s.F * 4 * 4));
   w.lab_tmp = reinterpret_cast<int32_t*>(take((size_t)s.F * s.R * s.S * 4));
-  w.bflags = reinterpret_cast<uint8_t*>(take((size_t)s.F * s.R * s.Sk));
+  w.bnorm = reinterpret_cast<double*>(take((size_t)s.F * s.cap * 3 * 8));
   w.fallback = reinterpret_cast<int32_t*>(take((size_t)s.F * 4));
   w.rbits = reinterpret_cast<uint32_t*>(take(words * 4));
   w.rpre = reinterpret_cast<int32_t*>(take(words * 4));
+  w.sbits = reinterpret_cast<uint32_t*>(take(words * 4));
+  w.spre = reinterpret_cast<int32_t*>(take(words * 4));
+  w.fscal_cnt = reinterpret_cast<int32_t*>(take((size_t)s.F * 4));
   w.bytes = off;
   return w;
 }
@@ -309,12 +312,7 @@ int lseg_run_pipeline(const lseg_sensor* sensor, int32_t frames, int32_t interva
   }
   launch_fused_graph(*sensor, sh, ws, ranges, thresholds, node_ids, neighbors, normals32, nmask, n_nodes, n_labels,
                      node_labels, st);
-  int32_t* filled = ws.lab_tmp;
-  launch_prune_plan(sh, n_labels, ws.K, min_segment_size, ws.hist, ws.remap, ws.fscal, st);
-  prof_mark("prune_plan", st);
-  launch_ring_fill(1, *sensor, sh, nullptr, filled, labels, ws.hist, ws.remap, ws.fscal, ws.K, min_segment_size,
-                   st);
-  prof_mark("prune_apply", st);
+  launch_prune_fused(sh, ws, min_segment_size, labels, st);
   return check_launch("run_pipeline");
 }
 

@@ -11,15 +11,17 @@
 //              root chase), then the nearest-donor backfill and the label
 //              histogram, in one pass (replaces label_dense + backfill).
 #include <cub/block/block_scan.cuh>
+#include <stdlib.h>
 
 #include "lseg_internal.cuh"
 #include "lseg_kernels.cuh"
 
 namespace lseg {
 
-static constexpr int TILE_R = 8;
+static constexpr int TILE_R = 16;
 static constexpr int TILE_C = 64;
 static constexpr int TILE_T = 256;
+static const int g_tile_dbg = getenv("LSEG_DEBUG_TILE") ? atoi(getenv("LSEG_DEBUG_TILE")) : 0;
 
 __device__ __forceinline__ int wrapc(int c, int Sk) { return c < 0 ? c + Sk : (c >= Sk ? c - Sk : c); }
 
@@ -51,20 +53,67 @@ __device__ __forceinline__ void lunion(int* par, int a, int b) {
   }
 }
 
+// Is the forward edge (r, c) -> slot s internal to the (TR x TC) tile that
+// owns (r, c)?  Shared by k_tile (local unions) and k_merge (the rest).
+template <int TR, int TC>
+__device__ __forceinline__ bool edge_internal(int r, int c, int s, int Sk) {
+  const int tr = r + slot_dr(s);
+  int tc = c + slot_dc(s);
+  if (tc >= Sk) tc -= Sk;
+  return (tr / TR == r / TR) && (tc / TC == c / TC);
+}
+
+// Normal of a node whose 6 slots are all present: the same operation sequence
+// as Fan (pairs (0,1)..(4,5),(5,0) accumulated in order) but straight-line, so
+// the six square roots / reciprocals are independent and can overlap.
+__device__ __forceinline__ bool fan6(const double* vx, const double* vy, const double* vz, const Vec3& p,
+                                     double out[3]) {
+  double l[6];
+#pragma unroll
+  for (int a = 0; a < 6; ++a) l[a] = norm3(vx[a], vy[a], vz[a]);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, ws = 0.0;
+#pragma unroll
+  for (int a = 0; a < 6; ++a) {
+    const int b = (a + 1) % 6;
+    const double L = __dadd_rn(l[a], l[b]);
+    const double w = (L > 0.0) ? __drcp_rn(L) : 0.0;
+    a0 = __dadd_rn(a0, __dmul_rn(w, __dsub_rn(__dmul_rn(vy[a], vz[b]), __dmul_rn(vz[a], vy[b]))));
+    a1 = __dadd_rn(a1, __dmul_rn(w, __dsub_rn(__dmul_rn(vz[a], vx[b]), __dmul_rn(vx[a], vz[b]))));
+    a2 = __dadd_rn(a2, __dmul_rn(w, __dsub_rn(__dmul_rn(vx[a], vy[b]), __dmul_rn(vy[a], vx[b]))));
+    ws = __dadd_rn(ws, w);
+  }
+  if (!(ws > 0.0)) return false;
+  const double m0 = __ddiv_rn(a0, ws), m1 = __ddiv_rn(a1, ws), m2 = __ddiv_rn(a2, ws);
+  const double mag = norm3(m0, m1, m2);
+  if (!(mag >= 1e-12)) return false;
+  double u0 = __ddiv_rn(m0, mag), u1 = __ddiv_rn(m1, mag), u2 = __ddiv_rn(m2, mag);
+  const double dot = __dadd_rn(__dadd_rn(__dmul_rn(u0, p.x), __dmul_rn(u2, p.z)), __dmul_rn(u1, p.y));
+  if (dot > 0.0) { u0 = -u0; u1 = -u1; u2 = -u2; }
+  out[0] = u0; out[1] = u1; out[2] = u2;
+  return true;
+}
+
+// One CTA per (frame, TR x TC tile of kept cells).
+//   A  ranges + node ids of the tile and a 1-cell halo into shared memory
+//   B  fp64 normals of the tile's nodes (shared memory)
+//   C  neighbours / normals / mask out; fp64 normals of the tile's border
+//      cells to `bnorm` for k_merge
+//   D  homogeneity test + shared-memory union-find on internal forward edges
+//   E  parent[cell] = tile-local root cell (-1 for cells without a normal)
 template <int TR, int TC, int T>
-__global__ void __launch_bounds__(T) k_tile(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
-                                             const uint32_t* __restrict__ vbits, const int32_t* __restrict__ wpre,
-                                             double t0, double t1, double t2, int32_t* __restrict__ node_ids,
-                                             int32_t* __restrict__ neighbors, float* __restrict__ n32,
-                                             uint8_t* __restrict__ nmask, int32_t* __restrict__ parent,
-                                             uint8_t* __restrict__ bflags) {
-  constexpr int GR = TR + 3, GC = TC + 3;  // ranges halo: rows r0-1..r0+TR+1, cols c0-1..c0+TC+1
-  constexpr int NR = TR + 1, NC = TC + 1;  // normals: rows r0..r0+TR, cols c0..c0+TC
-  __shared__ double s_r[GR][GC];
-  __shared__ double s_n[NR][NC][3];
-  __shared__ uint8_t s_has[NR][NC];
-  __shared__ int s_gid[TR * TC];
-  __shared__ int s_par[TR * TC];
+__global__ void __launch_bounds__(T, 3) k_tile(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
+                                                const uint32_t* __restrict__ vbits, const int32_t* __restrict__ wpre,
+                                                double t0, double t1, double t2, int32_t* __restrict__ node_ids,
+                                                int32_t* __restrict__ neighbors, float* __restrict__ n32,
+                                                uint8_t* __restrict__ nmask, int32_t* __restrict__ parent,
+                                                double* __restrict__ bnorm, int dbg) {
+  constexpr int GR = TR + 2, GC = TC + 2;  // halo rows r0-1..r0+TR, cols c0-1..c0+TC
+  constexpr int NT = TR * TC;
+  __shared__ double s_r[GR * GC];
+  __shared__ int s_id[GR * GC];
+  __shared__ double s_nx[NT], s_ny[NT], s_nz[NT];
+  __shared__ uint8_t s_has[NT];
+  __shared__ int s_par[NT];
 
   const int tilesC = (sh.Sk + TC - 1) / TC;
   const int tilesR = (sh.R + TR - 1) / TR;
@@ -73,152 +122,212 @@ __global__ void __launch_bounds__(T) k_tile(lseg_sensor sn, Shape sh, const doub
   const int rem = (int)(b - (int64_t)f * tilesR * tilesC);
   const int r0 = (rem / tilesC) * TR, c0 = (rem % tilesC) * TC;
   const int TRe = min(TR, sh.R - r0), TCe = min(TC, sh.Sk - c0);
-  const bool full_width = (c0 == 0 && TCe == sh.Sk);
   const double* rf = ranges + (int64_t)f * sh.R * sh.S;
   const uint32_t* vbf = vbits + (int64_t)f * sh.R * sh.Wk;
   const int32_t* wpf = wpre + (int64_t)f * sh.R * sh.Wk;
   const int64_t nbase = (int64_t)f * sh.cap;
   const int tid = threadIdx.x;
 
-  // A. ranges halo (NaN outside the ring range)
+  // A. halo ranges (NaN outside the ring range) and node ids (-1 absent)
   for (int e = tid; e < GR * GC; e += T) {
     const int y = e / GC, x = e - y * GC;
     const int rr = r0 - 1 + y;
     double v = __longlong_as_double(0x7ff8000000000000LL);
-    if (rr >= 0 && rr < sh.R) v = __ldg(rf + (int64_t)rr * sh.S + (int64_t)wrapc(c0 - 1 + x, sh.Sk) * sh.k);
-    s_r[y][x] = v;
+    int id = -1;
+    if (rr >= 0 && rr < sh.R) {
+      const int cc = wrapc(c0 - 1 + x, sh.Sk);
+      v = __ldg(rf + (int64_t)rr * sh.S + (int64_t)cc * sh.k);
+      id = id_at(vbf, wpf, sh.Wk, rr, cc);
+    }
+    s_r[e] = v;
+    s_id[e] = id;
   }
   __syncthreads();
 
-  // B. fp64 normals for tile + forward halo (reference normals.py:94-145 order)
-  for (int e = tid; e < NR * NC; e += T) {
-    const int y = e / NC, x = e - y * NC;
-    const int rr = r0 + y;
+  // B. fp64 normals (reference normals.py:94-145 operation order)
+  for (int e = tid; e < NT; e += T) {
+    const int y = e / TC, x = e - y * TC;
     bool ok = false;
     double nv[3] = {0.0, 0.0, 0.0};
-    const double rp = s_r[y + 1][x + 1];
-    if (rr < sh.R && in_window(rp, sn.r_min, sn.r_max)) {
-      const int cc = wrapc(c0 + x, sh.Sk);
-      const Vec3 p = cell_pos(sn, rr, cc * sh.k, rp);
-      Fan fan;
-#pragma unroll
-      for (int s = 0; s < 6; ++s) {
-        const int dy = slot_dr(s), dx = slot_dc(s);
-        const double rq = s_r[y + 1 + dy][x + 1 + dx];
-        bool present = in_window(rq, sn.r_min, sn.r_max);
-        if (s == 5 && sh.Sk == 2) present = false;  // duplicate of slot 2 (mesh.py:96-101)
-        if (present) {
-          const Vec3 q = cell_pos(sn, rr + dy, wrapc(cc + dx, sh.Sk) * sh.k, rq);
-          fan.add(__dsub_rn(q.x, p.x), __dsub_rn(q.y, p.y), __dsub_rn(q.z, p.z));
-        }
-      }
-      ok = fan.finish(p, nv);
-    }
-    s_n[y][x][0] = nv[0];
-    s_n[y][x][1] = nv[1];
-    s_n[y][x][2] = nv[2];
-    s_has[y][x] = ok ? 1 : 0;
-  }
-
-  // C. tile nodes: ids, slots, outputs
-  for (int e = tid; e < TR * TC; e += T) {
-    const int y = e / TC, x = e - y * TC;
-    int id = -1;
-    if (y < TRe && x < TCe) {
+    const int g = (y + 1) * GC + (x + 1);
+    if (y < TRe && x < TCe && s_id[g] >= 0 && (dbg & 1)) {
+      ok = true;
+      nv[2] = 1.0;
+    } else if (y < TRe && x < TCe && s_id[g] >= 0) {
       const int rr = r0 + y, cc = c0 + x;
-      id = id_at(vbf, wpf, sh.Wk, rr, cc);
-      if (node_ids) node_ids[((int64_t)f * sh.R + rr) * sh.Sk + cc] = id;
-      if (id >= 0) {
-        int nb[6];
+      const Vec3 p = cell_pos(sn, rr, cc * sh.k, s_r[g]);
+      int pres = 0;
+#pragma unroll
+      for (int s = 0; s < 6; ++s)
+        if (s_id[g + slot_dr(s) * GC + slot_dc(s)] >= 0 && !(s == 5 && sh.Sk == 2)) pres |= 1 << s;  // mesh.py:96-101
+      if (pres == 0x3f) {
+        double vx[6], vy[6], vz[6];
 #pragma unroll
         for (int s = 0; s < 6; ++s) {
-          const int r2 = rr + slot_dr(s);
-          nb[s] = (r2 >= 0 && r2 < sh.R) ? id_at(vbf, wpf, sh.Wk, r2, wrapc(cc + slot_dc(s), sh.Sk)) : -1;
+          const int dy = slot_dr(s), dx = slot_dc(s);
+          const Vec3 q = cell_pos(sn, rr + dy, wrapc(cc + dx, sh.Sk) * sh.k, s_r[g + dy * GC + dx]);
+          vx[s] = __dsub_rn(q.x, p.x);
+          vy[s] = __dsub_rn(q.y, p.y);
+          vz[s] = __dsub_rn(q.z, p.z);
         }
-        if (sh.Sk == 2 && nb[5] == nb[2]) nb[5] = -1;
-        int4* o4 = reinterpret_cast<int4*>(neighbors + (nbase + id) * 6);  // 24 B, 8-B aligned
-        int2* o2 = reinterpret_cast<int2*>(o4);
-        o2[0] = make_int2(nb[0], nb[1]);
-        o2[1] = make_int2(nb[2], nb[3]);
-        o2[2] = make_int2(nb[4], nb[5]);
+        ok = fan6(vx, vy, vz, p, nv);
+      } else {
+        Fan fan;
+#pragma unroll
+        for (int s = 0; s < 6; ++s) {
+          if (!(pres & (1 << s))) continue;
+          const int dy = slot_dr(s), dx = slot_dc(s);
+          const Vec3 q = cell_pos(sn, rr + dy, wrapc(cc + dx, sh.Sk) * sh.k, s_r[g + dy * GC + dx]);
+          fan.add(__dsub_rn(q.x, p.x), __dsub_rn(q.y, p.y), __dsub_rn(q.z, p.z));
+        }
+        ok = fan.finish(p, nv);
       }
     }
-    s_gid[e] = id;
+    s_nx[e] = nv[0];
+    s_ny[e] = nv[1];
+    s_nz[e] = nv[2];
+    s_has[e] = ok ? 1 : 0;
     s_par[e] = e;
   }
-  __syncthreads();  // s_n / s_has / s_gid / s_par complete
+  __syncthreads();
 
-  // D. outputs that need the normals + local union over passing forward edges
-  for (int e = tid; e < TR * TC; e += T) {
+  // C. per-node outputs
+  for (int e = tid; e < NT; e += T) {
     const int y = e / TC, x = e - y * TC;
-    const int id = s_gid[e];
+    if (y >= TRe || x >= TCe) continue;
+    const int rr = r0 + y, cc = c0 + x;
+    const int g = (y + 1) * GC + (x + 1);
+    const int id = s_id[g];
+    const int64_t cell = (int64_t)rr * sh.Sk + cc;
+    if (node_ids) node_ids[nbase + cell] = id;
     if (id < 0) continue;
-    const bool has = s_has[y][x];
+    int nb[6];
+#pragma unroll
+    for (int s = 0; s < 6; ++s) nb[s] = s_id[g + slot_dr(s) * GC + slot_dc(s)];
+    if (sh.Sk == 2 && nb[5] == nb[2]) nb[5] = -1;
+    int2* o2 = reinterpret_cast<int2*>(neighbors + (nbase + id) * 6);  // 24 B rows, 8-B aligned
+    o2[0] = make_int2(nb[0], nb[1]);
+    o2[1] = make_int2(nb[2], nb[3]);
+    o2[2] = make_int2(nb[4], nb[5]);
+    const bool has = s_has[e];
     if (n32) {
       float* o = n32 + (nbase + id) * 3;
-      const float nanf_ = __int_as_float(0x7fc00000);
-      o[0] = has ? (float)s_n[y][x][0] : nanf_;
-      o[1] = has ? (float)s_n[y][x][1] : nanf_;
-      o[2] = has ? (float)s_n[y][x][2] : nanf_;
+      const float qn = __int_as_float(0x7fc00000);
+      o[0] = has ? (float)s_nx[e] : qn;
+      o[1] = has ? (float)s_ny[e] : qn;
+      o[2] = has ? (float)s_nz[e] : qn;
     }
     nmask[nbase + id] = has ? 1 : 0;
+    if (has && (y == 0 || y == TRe - 1 || x == 0 || x == TCe - 1)) {
+      double* o = bnorm + (nbase + cell) * 3;
+      o[0] = s_nx[e];
+      o[1] = s_ny[e];
+      o[2] = s_nz[e];
+    }
   }
-  uint8_t myflags[(TR * TC + T - 1) / T];
+
+  // D. local components.  D1: one warp per tile row turns the passing
+  // horizontal edges into 64-bit masks; every node's parent becomes the start
+  // of its horizontal run (bit arithmetic, no atomics).  D2: vertical /
+  // diagonal edges join runs with shared-memory union-find, skipping an edge
+  // when the parallel edge one column to the left already joins the same two
+  // runs.  D3: column-wrap edges of a full-width tile (S' <= TC).
+  static_assert(TC == 64, "row masks assume 64-column tiles");
+  __shared__ unsigned long long s_H[TR], s_V0[TR], s_V1[TR];
+  const int lane = tid & 31;
+  for (int y = tid >> 5; y < TR && !(dbg & 2); y += T / 32) {
+    unsigned long long H = 0, V0 = 0, V1 = 0;
 #pragma unroll
-  for (int j = 0; j < (TR * TC + T - 1) / T; ++j) myflags[j] = 0;
-#pragma unroll
-  for (int j = 0; j < (TR * TC + T - 1) / T; ++j) {
-    const int e = tid + j * T;
-    if (e >= TR * TC) break;
-    const int y = e / TC, x = e - y * TC;
-    if (s_gid[e] < 0 || !s_has[y][x]) continue;
-    const double* a = s_n[y][x];
-#pragma unroll
-    for (int s = 0; s < 3; ++s) {  // forward slots N0 (+1,0), N1 (+1,+1), N2 (0,+1)
-      const int ty = y + slot_dr(s), tx = x + slot_dc(s);
-      if (r0 + ty >= sh.R) continue;        // no ring below the bottom ring
-      if (!s_has[ty][tx]) continue;         // target absent or without a normal
-      if (!normals_pass(a, s_n[ty][tx], t0, t1, t2)) continue;
-      int lx = tx;
-      bool local = (ty < TRe);
-      if (local) {
-        if (tx >= TCe) {
-          if (full_width) lx = tx - TCe; else local = false;
+    for (int half = 0; half < 2; ++half) {
+      const int x = lane + 32 * half;
+      const int e = y * TC + x;
+      bool h = false, v0 = false, v1 = false;
+      if (y < TRe && s_has[e]) {
+        const double a[3] = {s_nx[e], s_ny[e], s_nz[e]};
+        if (x + 1 < TCe && s_has[e + 1]) {
+          const double q[3] = {s_nx[e + 1], s_ny[e + 1], s_nz[e + 1]};
+          h = normals_pass(a, q, t0, t1, t2);
+        }
+        if (y + 1 < TRe) {
+          if (s_has[e + TC]) {
+            const double q[3] = {s_nx[e + TC], s_ny[e + TC], s_nz[e + TC]};
+            v0 = normals_pass(a, q, t0, t1, t2);
+          }
+          if (x + 1 < TCe && s_has[e + TC + 1]) {
+            const double q[3] = {s_nx[e + TC + 1], s_ny[e + TC + 1], s_nz[e + TC + 1]};
+            v1 = normals_pass(a, q, t0, t1, t2);
+          }
         }
       }
-      if (local) lunion(s_par, e, ty * TC + lx);
-      else myflags[j] |= (uint8_t)(1u << s);
+      const unsigned long long sh_ = half ? 32 : 0;
+      H |= (unsigned long long)__ballot_sync(0xffffffffu, h) << sh_;
+      V0 |= (unsigned long long)__ballot_sync(0xffffffffu, v0) << sh_;
+      V1 |= (unsigned long long)__ballot_sync(0xffffffffu, v1) << sh_;
+    }
+    if (lane == 0) { s_H[y] = H; s_V0[y] = V0; s_V1[y] = V1; }
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int x = lane + 32 * half;
+      const unsigned long long Z = ~H & ((1ull << x) - 1ull);
+      const int start = Z ? 64 - __clzll((long long)Z) : 0;
+      s_par[y * TC + x] = y * TC + start;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < NT && !(dbg & 2); e += T) {
+    const int y = e / TC, x = e - y * TC;
+    if (y + 1 >= TRe || !s_has[e]) continue;
+    const unsigned long long Hy = s_H[y], Hn = s_H[y + 1], V0 = s_V0[y], V1 = s_V1[y];
+    const unsigned long long bx = 1ull << x, bl = bx >> 1;
+    if (V0 & bx) {
+      const bool dup = x > 0 && (Hy & bl) && (Hn & bl) && (V0 & bl);
+      if (!dup) lunion(s_par, e, e + TC);
+    }
+    if (V1 & bx) {
+      const bool dup = ((V0 & bx) && (Hn & bx)) || (x > 0 && (Hy & bl) && (Hn & bx) && (V1 & bl));
+      if (!dup) lunion(s_par, e, e + TC + 1);
+    }
+  }
+  if (c0 == 0 && TCe == sh.Sk && !(dbg & 2)) {  // full-width tile: wrap edges (x = S'-1 -> 0)
+    for (int y = tid; y < TRe; y += T) {
+      const int e = y * TC + TCe - 1;
+      if (!s_has[e]) continue;
+      const double a[3] = {s_nx[e], s_ny[e], s_nz[e]};
+      const int t2e = y * TC;  // (y, 0)
+      if (TCe > 1 && s_has[t2e]) {
+        const double q[3] = {s_nx[t2e], s_ny[t2e], s_nz[t2e]};
+        if (normals_pass(a, q, t0, t1, t2)) lunion(s_par, e, t2e);
+      }
+      const int t1e = (y + 1) * TC;  // (y+1, 0)
+      if (y + 1 < TRe && s_has[t1e]) {
+        const double q[3] = {s_nx[t1e], s_ny[t1e], s_nz[t1e]};
+        if (normals_pass(a, q, t0, t1, t2)) lunion(s_par, e, t1e);
+      }
     }
   }
   __syncthreads();
 
-  // E. local roots -> global parent; boundary flags for k_merge
-#pragma unroll
-  for (int j = 0; j < (TR * TC + T - 1) / T; ++j) {
-    const int e = tid + j * T;
-    if (e >= TR * TC) break;
+  // E. tile-local roots (min cell of each local component) -> parent
+  for (int e = tid; e < NT; e += T) {
     const int y = e / TC, x = e - y * TC;
     if (y >= TRe || x >= TCe) continue;
-    const int id = s_gid[e];
-    // union-find runs on frame-local kept-cell indices (row-major, so the
-    // minimum cell of a component is also its minimum node id)
     int pc = -1;
-    if (id >= 0 && s_has[y][x]) {
+    if (s_has[e]) {
       const int lr = lfind(s_par, e);
       pc = (r0 + lr / TC) * sh.Sk + c0 + lr % TC;
     }
     parent[nbase + (int64_t)(r0 + y) * sh.Sk + c0 + x] = pc;
-    if (y == TR - 1 || y == TRe - 1 || x == TC - 1 || x == TCe - 1)
-      bflags[((int64_t)f * sh.R + r0 + y) * sh.Sk + c0 + x] = (id >= 0) ? myflags[j] : 0;
   }
 }
 
-// Global union over tile-boundary edges.  Threads enumerate the cells of the
-// tiles' last rows and last columns (duplicates at corners are harmless).
+// Global union over the forward edges that leave a tile.  Threads enumerate
+// the cells of each tile's last row and last column (corner duplicates are
+// harmless); both endpoints' fp64 normals come from `bnorm`.
 template <int TR, int TC>
-__global__ void k_merge(Shape sh, const uint8_t* __restrict__ bflags, int32_t* __restrict__ parent) {
-  const int nbr = (sh.R + TR - 1) / TR;                // boundary rows per frame (last row of each tile row)
-  const int nbc = (sh.Sk + TC - 1) / TC;               // boundary cols per frame
+__global__ void k_merge(Shape sh, const double* __restrict__ bnorm, double t0, double t1, double t2,
+                        int32_t* __restrict__ parent) {
+  const int nbr = (sh.R + TR - 1) / TR;
+  const int nbc = (sh.Sk + TC - 1) / TC;
   const int64_t per = (int64_t)nbr * sh.Sk + (int64_t)nbc * sh.R;
   const int64_t n = per * sh.F;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
@@ -235,36 +344,20 @@ __global__ void k_merge(Shape sh, const uint8_t* __restrict__ bflags, int32_t* _
       c = min(bc * TC + TC - 1, sh.Sk - 1);
       r = (int)(u - (int64_t)bc * sh.R);
     }
-    const uint8_t fl = bflags[((int64_t)f * sh.R + r) * sh.Sk + c];
-    if (!fl) continue;
     int32_t* par = parent + (int64_t)f * sh.cap;
     const int p = r * sh.Sk + c;
+    if (__ldcg(par + p) < 0) continue;  // no normal
+    const double* bn = bnorm + (int64_t)f * sh.cap * 3;
+    const double a[3] = {__ldcg(bn + 3 * p), __ldcg(bn + 3 * p + 1), __ldcg(bn + 3 * p + 2)};
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
-      if (!(fl & (1u << s))) continue;
+      if (r + slot_dr(s) >= sh.R) continue;
+      if (edge_internal<TR, TC>(r, c, s, sh.Sk)) continue;
       const int q = (r + slot_dr(s)) * sh.Sk + wrapc(c + slot_dc(s), sh.Sk);
-      uf_union(par, p, q);
+      if (__ldcg(par + q) < 0) continue;
+      const double b[3] = {__ldcg(bn + 3 * q), __ldcg(bn + 3 * q + 1), __ldcg(bn + 3 * q + 2)};
+      if (normals_pass(a, b, t0, t1, t2)) uf_union(par, p, q);
     }
-  }
-}
-
-// Final roots as a bit per kept cell (a labelled cell whose parent is itself);
-// k_frame_scan over these bits gives every root its rank = label - 1.
-__global__ void k_root_bits(Shape sh, const int32_t* __restrict__ parent, uint32_t* __restrict__ rbits) {
-  const int64_t nwords = (int64_t)sh.F * sh.R * sh.Wk;
-  const int lane = threadIdx.x & 31;
-  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nwords;
-       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t row = w / sh.Wk;
-    const int c = (int)(w - row * sh.Wk) * 32 + lane;
-    bool root = false;
-    if (c < sh.Sk) {
-      const int f = (int)(row / sh.R);
-      const int64_t cell = row * sh.Sk + c;  // == f*cap + frame-local cell
-      root = (__ldg(parent + cell) == (int)(cell - (int64_t)f * sh.cap));
-    }
-    const uint32_t b = __ballot_sync(0xffffffffu, root);
-    if (lane == 0) rbits[w] = b;
   }
 }
 
@@ -273,6 +366,41 @@ __device__ __forceinline__ int root_of(const int32_t* __restrict__ par, int x) {
   int p = __ldcg(par + x);
   while (p != x) { x = p; p = __ldcg(par + x); }
   return x;
+}
+
+// After k_merge: point every labelled cell straight at its final root, mark
+// roots with a bit per kept cell (k_frame_scan over these gives label ranks)
+// and zero each root's histogram slot (labels are root cell + 1 until pruning).
+__global__ void k_root_flatten(Shape sh, int32_t* __restrict__ parent, uint32_t* __restrict__ rbits,
+                               int32_t* __restrict__ hist, int64_t K) {
+  const int64_t nwords = (int64_t)sh.F * sh.R * sh.Wk;
+  const int lane = threadIdx.x & 31;
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nwords;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t row = w / sh.Wk;
+    const int c = (int)(w - row * sh.Wk) * 32 + lane;
+    const int f = (int)(row / sh.R);
+    bool root = false;
+    if (c < sh.Sk) {
+      int32_t* par = parent + (int64_t)f * sh.cap;
+      const int cell = (int)(row - (int64_t)f * sh.R) * sh.Sk + c;
+      const int p = __ldcg(par + cell);
+      if (p >= 0) {
+        const int r = root_of(par, p);
+        if (r != p) par[cell] = r;
+        root = (r == cell);
+        if (root) hist[(int64_t)f * K + cell + 1] = 0;
+      }
+    }
+    const uint32_t b = __ballot_sync(0xffffffffu, root);
+    if (lane == 0) rbits[w] = b;
+  }
+}
+
+// 1 + rank of root cell rc among the set bits of (bits, pre) = its label.
+__device__ __forceinline__ int rank_label(const uint32_t* bf, const int32_t* pf, int Wk, int Sk, int rc) {
+  const int rr = rc / Sk, cc = rc - rr * Sk;
+  return 1 + node_id_at(bf + (int64_t)rr * Wk, pf + (int64_t)rr * Wk, cc);
 }
 
 // Node labels + backfill + histogram for one ring row per CTA.
@@ -296,28 +424,28 @@ __global__ void __launch_bounds__(T) k_labels_backfill(lseg_sensor sn, Shape sh,
   const uint32_t* vbr = vbits + row * sh.Wk;
   const int32_t* par = parent + (int64_t)f * sh.cap;
 
-  // node labels of this row (reference segment.py:86-88); -1 marks an invalid
-  // kept cell (so k = 1 needs no ranges read for validity)
+  // node labels of this row, provisional ids = root cell + 1 (ascending root
+  // cell == ascending reference label, so the final compaction in
+  // k_prune_rows reproduces the reference ids); -1 marks an invalid kept cell
+  // (so k = 1 needs no ranges read for validity)
   const uint32_t* rbf = rbits + (int64_t)f * sh.R * sh.Wk;
   const int32_t* rpf = rpre + (int64_t)f * sh.R * sh.Wk;
   for (int s = threadIdx.x; s < S; s += T) {
     int lab = 0;
     if (s % sh.k == 0) {
       const int c = s / sh.k;
-      const int p = __ldcg(par + i * sh.Sk + c);
-      if (p >= 0) {
-        const int rc = root_of(par, p);
-        const int rr = rc / sh.Sk, cc = rc - rr * sh.Sk;
-        lab = 1 + node_id_at(rbf + (int64_t)rr * sh.Wk, rpf + (int64_t)rr * sh.Wk, cc);
-      } else if (!((__ldg(vbr + (c >> 5)) >> (c & 31)) & 1u)) {
-        lab = -1;
-      }
+      const int p = __ldcg(par + i * sh.Sk + c);  // flattened: p is the root cell
+      if (p >= 0) lab = p + 1;
+      else if (!((__ldg(vbr + (c >> 5)) >> (c & 31)) & 1u)) lab = -1;
     }
     s_row[s] = lab;
   }
   __syncthreads();
-  if (node_labels)
-    for (int s = threadIdx.x; s < S; s += T) node_labels[row * S + s] = max(s_row[s], 0);
+  if (node_labels)  // reference segment() output: 1 + rank of the root
+    for (int s = threadIdx.x; s < S; s += T) {
+      const int v = s_row[s];
+      node_labels[row * S + s] = v > 0 ? rank_label(rbf, rpf, sh.Wk, sh.Sk, v - 1) : 0;
+    }
 
   const int s0 = threadIdx.x * ITEMS;
   int lab[ITEMS];
@@ -393,20 +521,50 @@ __global__ void __launch_bounds__(T) k_labels_backfill(lseg_sensor sn, Shape sh,
 // ---------------------------------------------------------------- binning
 static constexpr double kTwoPiF = 6.283185307179586;  // == 2.0 * np.pi
 
-__device__ __forceinline__ int64_t lower_bound_ring(const int32_t* __restrict__ ring, int64_t lo, int64_t hi, int v) {
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (__ldg(ring + mid) < v) lo = mid + 1; else hi = mid;
+// First index in [lo, hi) whose ring id is >= v, found by one warp with a
+// 32-ary search (4 dependent probes for a 124 k-point frame instead of 17).
+// Exact for ring-major input; for other orders the result is arbitrary but in
+// range, and k_bin_rows' segment check sends the frame to the generic path.
+__device__ __forceinline__ int64_t warp_lower_bound(const int32_t* __restrict__ ring, int64_t lo, int64_t hi, int v,
+                                                    int lane) {
+  while (hi - lo > 32) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t q = lo + (int64_t)lane * step;
+    const bool less = (q < hi) && (__ldg(ring + q) < v);
+    const unsigned m = __ballot_sync(0xffffffffu, less);
+    const int c = (~m == 0u) ? 32 : __ffs(~m) - 1;  // leading lanes with ring < v
+    const int64_t nlo = (c == 0) ? lo : lo + (int64_t)(c - 1) * step + 1;
+    const int64_t nhi = (c == 32) ? hi : min(hi, lo + (int64_t)c * step);
+    lo = nlo;
+    hi = nhi;
   }
-  return lo;
+  const int64_t q = lo + lane;
+  const unsigned m = __ballot_sync(0xffffffffu, (q < hi) && (__ldg(ring + q) < v));
+  const int c = (~m == 0u) ? 32 : __ffs(~m) - 1;
+  return min(hi, lo + c);
 }
 
 // Same definition as k_bin_points: r and step of one point.
+// The step is rint(phi*S/2pi) of the fp64 phi; a float atan2 of the (exact,
+// float) inputs decides it whenever phi*S/2pi is clearly away from a
+// half-integer (its error is < 1e-5 rad, far inside the guard), otherwise the
+// fp64 formula runs -- the result is the fp64 formula's either way.
 __device__ __forceinline__ bool bin_one(const lseg_sensor& sn, const float* __restrict__ xyz, int64_t p, double& r,
                                         int& step) {
-  const double x = (double)__ldg(xyz + 3 * p), y = (double)__ldg(xyz + 3 * p + 1), z = (double)__ldg(xyz + 3 * p + 2);
+  const float xf = __ldg(xyz + 3 * p), yf = __ldg(xyz + 3 * p + 1), zf = __ldg(xyz + 3 * p + 2);
+  const double x = (double)xf, y = (double)yf, z = (double)zf;
   r = __dsqrt_rn(__dadd_rn(__dadd_rn(x * x, y * y), z * z));
   if (!in_window(r, sn.r_min, sn.r_max)) return false;
+  const float scale = (float)sn.steps * 0.15915494309189535f;  // S / (2 pi)
+  float ph = atan2f(yf, xf);
+  if (ph < 0.0f) ph += 6.283185307179586f;
+  const float t = ph * scale;
+  const float fr = t - floorf(t);
+  if (fabsf(fr - 0.5f) > 1e-3f + 2e-5f * scale) {
+    int st = (int)rintf(t);
+    step = st >= sn.steps ? st - sn.steps : st;
+    return true;
+  }
   double phi = atan2(y, x);
   if (phi < 0.0) phi = __dadd_rn(phi, kTwoPiF);
   step = (int)rint(__ddiv_rn(__dmul_rn(phi, (double)sn.steps), kTwoPiF)) % sn.steps;
@@ -429,10 +587,16 @@ __global__ void __launch_bounds__(T) k_bin_rows(lseg_sensor sn, Shape sh, const 
   const int64_t row = blockIdx.x;
   const int f = (int)(row / sh.R), i = (int)(row - (int64_t)f * sh.R);
   const int S = sh.S;
+  __shared__ int64_t s_lohi[2];
   const int64_t p0 = __ldg(off + f), p1 = __ldg(off + f + 1);
-  const int64_t lo = lower_bound_ring(ring, p0, p1, i);
-  const int64_t hi = lower_bound_ring(ring, p0, p1, i + 1);
+  const int warp = threadIdx.x >> 5;
+  if (warp < 2) {
+    const int64_t b = warp_lower_bound(ring, p0, p1, i + warp, threadIdx.x & 31);
+    if ((threadIdx.x & 31) == 0) s_lohi[warp] = b;
+  }
   for (int s = threadIdx.x; s < S; s += T) s_cell[s] = ~0ull;
+  __syncthreads();
+  const int64_t lo = s_lohi[0], hi = s_lohi[1];
   if (threadIdx.x == 0) s_bad = (hi < lo) ? 1 : 0;
   __syncthreads();
   int bad = 0;
@@ -510,6 +674,145 @@ void launch_bin_fused(const lseg_sensor& sn, const Shape& sh, const float* xyz, 
   launch_frame_scan(sh, ws, n_nodes, st);
 }
 
+// Pruning plan over roots: a root survives unless its (post-backfill) count is
+// below min_size; survivor bits -> k_frame_scan gives the compaction ranks.
+// fscal[f*4] = 1 when some label of frame f is small (reference
+// segment.py:136-140: otherwise labels stay as they are).
+__global__ void k_survivors(Shape sh, const uint32_t* __restrict__ rbits, const int32_t* __restrict__ hist, int64_t K,
+                            int32_t min_size, uint32_t* __restrict__ sbits, int32_t* __restrict__ fscal) {
+  const int64_t nwords = (int64_t)sh.F * sh.R * sh.Wk;
+  const int lane = threadIdx.x & 31;
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nwords;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t row = w / sh.Wk;
+    const int f = (int)(row / sh.R);
+    const uint32_t rb = __ldg(rbits + w);
+    bool surv = false, small = false;
+    if ((rb >> lane) & 1u) {
+      const int cell = (int)(row - (int64_t)f * sh.R) * sh.Sk + (int)(w - row * sh.Wk) * 32 + lane;
+      const int cnt = __ldg(hist + (int64_t)f * K + cell + 1);
+      small = (min_size > 0) && (cnt < min_size);
+      surv = !small;
+    }
+    const uint32_t b = __ballot_sync(0xffffffffu, surv);
+    const uint32_t sm = __ballot_sync(0xffffffffu, small);
+    if (lane == 0) {
+      sbits[w] = b;
+      if (sm) atomicOr(fscal + f * 4, 1);
+    }
+  }
+}
+
+// Dissolve small segments into the nearest surviving ring donor (reference
+// segment.py:141-154) and write the final compacted ids, one CTA per ring row.
+template <int T, int ITEMS>
+__global__ void __launch_bounds__(T) k_prune_rows(Shape sh, const int32_t* __restrict__ lab_in,
+                                                  int32_t* __restrict__ out, const int32_t* __restrict__ hist,
+                                                  int64_t K, int32_t min_size, const int32_t* __restrict__ fscal,
+                                                  const uint32_t* __restrict__ rbits, const int32_t* __restrict__ rpre,
+                                                  const uint32_t* __restrict__ sbits,
+                                                  const int32_t* __restrict__ spre) {
+  using Scan = cub::BlockScan<int, T>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int s_first[T];
+  __shared__ int s_next[T];
+  __shared__ int s_gfirst, s_glast;
+  extern __shared__ int s_row[];
+  const int64_t row = blockIdx.x;
+  const int f = (int)(row / sh.R);
+  const int S = sh.S;
+  const bool any_small = fscal[f * 4] != 0;
+  const int32_t* hf = hist + (int64_t)f * K;
+  const uint32_t* bb = (any_small ? sbits : rbits) + (int64_t)f * sh.R * sh.Wk;
+  const int32_t* bp = (any_small ? spre : rpre) + (int64_t)f * sh.R * sh.Wk;
+  const int s0 = threadIdx.x * ITEMS;
+  int lab[ITEMS];
+  bool gone[ITEMS];
+  int last = INT_MIN, first = INT_MAX;
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const int s = s0 + j;
+    lab[j] = 0;
+    gone[j] = false;
+    if (s < S) {
+      lab[j] = __ldcg(lab_in + row * S + s);
+      gone[j] = any_small && lab[j] > 0 && __ldg(hf + lab[j]) < min_size;
+      if (lab[j] > 0 && !gone[j]) { if (first == INT_MAX) first = s; last = s; }
+      s_row[s] = gone[j] ? 0 : lab[j];  // donor labels only
+    }
+  }
+  __syncthreads();
+  int prev;
+  Scan(tmp).ExclusiveScan(last, prev, INT_MIN, cub::Max());
+  __syncthreads();
+  s_first[threadIdx.x] = first;
+  __syncthreads();
+  int rout;
+  Scan(tmp).ExclusiveScan(s_first[T - 1 - threadIdx.x], rout, INT_MAX, cub::Min());
+  s_next[T - 1 - threadIdx.x] = rout;
+  if (threadIdx.x == T - 1) s_glast = (last != INT_MIN) ? last : prev;
+  __syncthreads();
+  const int next = s_next[threadIdx.x];
+  if (threadIdx.x == 0) s_gfirst = (first != INT_MAX) ? first : next;
+  __syncthreads();
+  const int gfirst = s_gfirst, glast = s_glast;
+  const bool has_donor = (gfirst != INT_MAX);
+  int nxt[ITEMS];
+  {
+    int nd = next;
+#pragma unroll
+    for (int j = ITEMS - 1; j >= 0; --j) {
+      nxt[j] = nd;
+      if (lab[j] > 0 && !gone[j]) nd = s0 + j;
+    }
+  }
+  int pd = prev;
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const int s = s0 + j;
+    if (s >= S) break;
+    int res = lab[j];
+    if (gone[j]) {
+      res = 0;
+      if (has_donor) {
+        const int left = (pd != INT_MIN) ? pd : glast - S;
+        const int right = (nxt[j] != INT_MAX) ? nxt[j] : gfirst + S;
+        const int dl = s - left, dr = right - s;
+        const int ls = left < 0 ? left + S : left;
+        const int rs = right >= S ? right - S : right;
+        res = s_row[dl < dr ? ls : (dr < dl ? rs : min(ls, rs))];
+      }
+    } else if (res > 0) {
+      pd = s;
+    }
+    out[row * S + s] = res > 0 ? rank_label(bb, bp, sh.Wk, sh.Sk, res - 1) : 0;
+  }
+}
+
+void launch_prune_fused(const Shape& sh, const Workspace& ws, int32_t min_size, int32_t* labels, cudaStream_t st) {
+  cudaMemsetAsync(ws.fscal, 0, sizeof(int32_t) * 4 * sh.F, st);
+  const int64_t nwords = (int64_t)sh.F * sh.R * sh.Wk;
+  const int64_t blocks = (nwords * 32 + 255) / 256;
+  k_survivors<<<(unsigned)(blocks < 148 * 64 ? blocks : 148 * 64), 256, 0, st>>>(sh, ws.rbits, ws.hist, ws.K, min_size,
+                                                                                ws.sbits, ws.fscal);
+  launch_scan_bits(sh, ws.sbits, ws.spre, ws.fscal_cnt, nullptr, 0, st);
+  prof_mark("prune_plan", st);
+  const size_t smem = sizeof(int) * sh.S;
+#define PR(T_, I_)                                                                                            \
+  do {                                                                                                        \
+    if (smem > 48 * 1024)                                                                                     \
+      cudaFuncSetAttribute(k_prune_rows<T_, I_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+    k_prune_rows<T_, I_><<<sh.F * sh.R, T_, smem, st>>>(sh, ws.lab_tmp, labels, ws.hist, ws.K, min_size,      \
+                                                        ws.fscal, ws.rbits, ws.rpre, ws.sbits, ws.spre);      \
+  } while (0)
+  if (sh.S <= 1024) PR(256, 4);
+  else if (sh.S <= 2048) PR(256, 8);
+  else if (sh.S <= 4096) PR(256, 16);
+  else PR(512, 32);
+#undef PR
+  prof_mark("prune_apply", st);
+}
+
 // ---------------------------------------------------------------- launchers
 void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace& ws, const double* ranges,
                         const double* thr, int32_t* node_ids, int32_t* neighbors, float* n32, uint8_t* nmask,
@@ -518,18 +821,19 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   const int64_t nt = (int64_t)sh.F * tilesR * tilesC;
   k_tile<TILE_R, TILE_C, TILE_T><<<(unsigned)nt, TILE_T, 0, st>>>(sn, sh, ranges, ws.vbits, ws.wpre, thr[0], thr[1],
                                                                   thr[2], node_ids, neighbors, n32, nmask, ws.parent,
-                                                                  ws.bflags);
+                                                                  ws.bnorm, g_tile_dbg);
   prof_mark("tile", st);
   const int64_t nb = ((int64_t)tilesR * sh.Sk + (int64_t)tilesC * sh.R) * sh.F;
   k_merge<TILE_R, TILE_C><<<(unsigned)((nb + 255) / 256 < 148 * 32 ? (nb + 255) / 256 : 148 * 32), 256, 0, st>>>(
-      sh, ws.bflags, ws.parent);
+      sh, ws.bnorm, thr[0], thr[1], thr[2], ws.parent);
   prof_mark("merge", st);
   {
     const int64_t nwords = (int64_t)sh.F * sh.R * sh.Wk;
     const int64_t blocks = (nwords * 32 + 255) / 256;
-    k_root_bits<<<(unsigned)(blocks < 148 * 64 ? blocks : 148 * 64), 256, 0, st>>>(sh, ws.parent, ws.rbits);
-    prof_mark("root_bits", st);
-    launch_scan_bits(sh, ws.rbits, ws.rpre, n_labels, ws.hist, ws.K, st);
+    k_root_flatten<<<(unsigned)(blocks < 148 * 64 ? blocks : 148 * 64), 256, 0, st>>>(sh, ws.parent, ws.rbits,
+                                                                                     ws.hist, ws.K);
+    prof_mark("root_flatten", st);
+    launch_scan_bits(sh, ws.rbits, ws.rpre, n_labels, nullptr, 0, st);
     prof_mark("root_scan", st);
   }
   // labels + backfill -> lab_tmp (+ histogram)
@@ -542,6 +846,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
                                                              ws.rpre, node_labels, ws.lab_tmp, ws.hist, ws.K);  \
   } while (0)
   if (sh.S <= 1024) LB(256, 4);
+  else if (sh.S <= 2048) LB(256, 8);
   else if (sh.S <= 4096) LB(256, 16);
   else LB(512, 32);
 #undef LB

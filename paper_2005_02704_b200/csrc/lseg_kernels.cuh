@@ -33,4 +33,5 @@ void launch_bin_fused(const lseg_sensor& sn, const Shape& sh, const float* xyz, 
 void launch_frame_scan(const Shape& sh, const Workspace& ws, int32_t* n_nodes, cudaStream_t st);
 void launch_scan_bits(const Shape& sh, const uint32_t* bits, int32_t* pre, int32_t* counts, int32_t* hist, int64_t K,
                       cudaStream_t st);
+void launch_prune_fused(const Shape& sh, const Workspace& ws, int32_t min_size, int32_t* labels, cudaStream_t st);
 }  // namespace lseg
