@@ -13,7 +13,7 @@ import os
 import torch
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "liblidarseg_b200.so")
+LIB_PATH = os.environ.get("LSEG_LIB_PATH") or os.path.join(PKG, "liblidarseg_b200.so")
 
 
 class LidarSegError(RuntimeError):

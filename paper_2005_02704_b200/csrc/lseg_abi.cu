@@ -78,6 +78,10 @@ Workspace carve(const Shape& s, int64_t label_bound, void* base) {
   w.fscal = reinterpret_cast<int32_t*>(take((size_t)s.F * 4 * 4));
   w.lab_tmp = reinterpret_cast<int32_t*>(take((size_t)s.F * s.R * s.S * 4));
   w.bnorm = reinterpret_cast<double*>(take((size_t)s.F * s.cap * 3 * 8));
+  {
+    const size_t tiles = (size_t)s.F * ((s.R + 15) / 16) * ((s.Sk + 63) / 64);
+    w.masks = reinterpret_cast<unsigned long long*>(take(tiles * 16 * 5 * 8));
+  }
   w.fallback = reinterpret_cast<int32_t*>(take((size_t)s.F * 4));
   w.rbits = reinterpret_cast<uint32_t*>(take(words * 4));
   w.rpre = reinterpret_cast<int32_t*>(take(words * 4));

@@ -101,19 +101,27 @@ __device__ __forceinline__ bool fan6(const double* vx, const double* vy, const d
 //   D  homogeneity test + shared-memory union-find on internal forward edges
 //   E  parent[cell] = tile-local root cell (-1 for cells without a normal)
 template <int TR, int TC, int T>
-__global__ void __launch_bounds__(T, 3) k_tile(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
+#ifndef LSEG_TILE_MINB
+#define LSEG_TILE_MINB 3
+#endif
+__global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
                                                 const uint32_t* __restrict__ vbits, const int32_t* __restrict__ wpre,
                                                 double t0, double t1, double t2, int32_t* __restrict__ node_ids,
                                                 int32_t* __restrict__ neighbors, float* __restrict__ n32,
-                                                uint8_t* __restrict__ nmask, int32_t* __restrict__ parent,
+                                                uint8_t* __restrict__ nmask, unsigned long long* __restrict__ masks,
                                                 double* __restrict__ bnorm, int dbg) {
   constexpr int GR = TR + 2, GC = TC + 2;  // halo rows r0-1..r0+TR, cols c0-1..c0+TC
   constexpr int NT = TR * TC;
-  __shared__ double s_r[GR * GC];
-  __shared__ int s_id[GR * GC];
-  __shared__ double s_nx[NT], s_ny[NT], s_nz[NT];
-  __shared__ uint8_t s_has[NT];
-  __shared__ int s_par[NT];
+  // dynamic shared memory (58 KB > the 48 KB static limit), see tile_smem_bytes()
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  double* s_px = reinterpret_cast<double*>(s_dyn);
+  double* s_py = s_px + GR * GC;
+  double* s_pz = s_py + GR * GC;
+  double* s_nx = s_pz + GR * GC;
+  double* s_ny = s_nx + NT;
+  double* s_nz = s_ny + NT;
+  int* s_id = reinterpret_cast<int*>(s_nz + NT);
+  uint8_t* s_has = reinterpret_cast<uint8_t*>(s_id + GR * GC);
 
   const int tilesC = (sh.Sk + TC - 1) / TC;
   const int tilesR = (sh.R + TR - 1) / TR;
@@ -128,23 +136,28 @@ __global__ void __launch_bounds__(T, 3) k_tile(lseg_sensor sn, Shape sh, const d
   const int64_t nbase = (int64_t)f * sh.cap;
   const int tid = threadIdx.x;
 
-  // A. halo ranges (NaN outside the ring range) and node ids (-1 absent)
+  // A. halo positions dir*r (reference product order) and node ids (-1 absent)
   for (int e = tid; e < GR * GC; e += T) {
     const int y = e / GC, x = e - y * GC;
     const int rr = r0 - 1 + y;
-    double v = __longlong_as_double(0x7ff8000000000000LL);
+    Vec3 q = {0.0, 0.0, 0.0};
     int id = -1;
     if (rr >= 0 && rr < sh.R) {
       const int cc = wrapc(c0 - 1 + x, sh.Sk);
-      v = __ldg(rf + (int64_t)rr * sh.S + (int64_t)cc * sh.k);
       id = id_at(vbf, wpf, sh.Wk, rr, cc);
+      if (id >= 0) q = cell_pos(sn, rr, cc * sh.k, __ldg(rf + (int64_t)rr * sh.S + (int64_t)cc * sh.k));
     }
-    s_r[e] = v;
+    s_px[e] = q.x;
+    s_py[e] = q.y;
+    s_pz[e] = q.z;
     s_id[e] = id;
   }
   __syncthreads();
 
-  // B. fp64 normals (reference normals.py:94-145 operation order)
+  // B. fp64 normals (reference normals.py:94-145 operation order), branch-free
+  // over the presence pattern so a warp never runs two code paths: every slot
+  // forms the pair (a, next present slot after a); pairs the reference does
+  // not form get weight 0, which adds exact zeros to the sums.
   for (int e = tid; e < NT; e += T) {
     const int y = e / TC, x = e - y * TC;
     bool ok = false;
@@ -154,40 +167,61 @@ __global__ void __launch_bounds__(T, 3) k_tile(lseg_sensor sn, Shape sh, const d
       ok = true;
       nv[2] = 1.0;
     } else if (y < TRe && x < TCe && s_id[g] >= 0) {
-      const int rr = r0 + y, cc = c0 + x;
-      const Vec3 p = cell_pos(sn, rr, cc * sh.k, s_r[g]);
-      int pres = 0;
+      const Vec3 p = {s_px[g], s_py[g], s_pz[g]};
+      unsigned m = 0;
+      double vx[6], vy[6], vz[6], l[6];
 #pragma unroll
-      for (int s = 0; s < 6; ++s)
-        if (s_id[g + slot_dr(s) * GC + slot_dc(s)] >= 0 && !(s == 5 && sh.Sk == 2)) pres |= 1 << s;  // mesh.py:96-101
-      if (pres == 0x3f) {
-        double vx[6], vy[6], vz[6];
+      for (int s = 0; s < 6; ++s) {
+        const int gq = g + slot_dr(s) * GC + slot_dc(s);
+        const bool pr = s_id[gq] >= 0 && !(s == 5 && sh.Sk == 2);  // mesh.py:96-101 dedupe
+        m |= pr ? (1u << s) : 0u;
+        vx[s] = pr ? __dsub_rn(s_px[gq], p.x) : 0.0;
+        vy[s] = pr ? __dsub_rn(s_py[gq], p.y) : 0.0;
+        vz[s] = pr ? __dsub_rn(s_pz[gq], p.z) : 0.0;
+        l[s] = norm3(vx[s], vy[s], vz[s]);
+      }
+      const int cnt = __popc(m);
+      const int last = 31 - __clz(m | 1u);
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, ws = 0.0;
 #pragma unroll
-        for (int s = 0; s < 6; ++s) {
-          const int dy = slot_dr(s), dx = slot_dc(s);
-          const Vec3 q = cell_pos(sn, rr + dy, wrapc(cc + dx, sh.Sk) * sh.k, s_r[g + dy * GC + dx]);
-          vx[s] = __dsub_rn(q.x, p.x);
-          vy[s] = __dsub_rn(q.y, p.y);
-          vz[s] = __dsub_rn(q.z, p.z);
+      for (int a = 0; a < 6; ++a) {
+        const unsigned rot = ((m >> (a + 1)) | (m << (5 - a))) & 0x1fu;  // slots a+1 .. a+5 (mod 6)
+        const int j = __ffs(rot) - 1;                                     // partner = a+1+j (mod 6)
+        const bool valid = ((m >> a) & 1u) && cnt >= 2 && !(cnt == 2 && a == last);
+        double bx = vx[(a + 1) % 6], by = vy[(a + 1) % 6], bz = vz[(a + 1) % 6], lb = l[(a + 1) % 6];
+#pragma unroll
+        for (int k = 1; k < 5; ++k) {
+          const int c = (a + 1 + k) % 6;
+          const bool pick = (j == k);
+          bx = pick ? vx[c] : bx;
+          by = pick ? vy[c] : by;
+          bz = pick ? vz[c] : bz;
+          lb = pick ? l[c] : lb;
         }
-        ok = fan6(vx, vy, vz, p, nv);
-      } else {
-        Fan fan;
-#pragma unroll
-        for (int s = 0; s < 6; ++s) {
-          if (!(pres & (1 << s))) continue;
-          const int dy = slot_dr(s), dx = slot_dc(s);
-          const Vec3 q = cell_pos(sn, rr + dy, wrapc(cc + dx, sh.Sk) * sh.k, s_r[g + dy * GC + dx]);
-          fan.add(__dsub_rn(q.x, p.x), __dsub_rn(q.y, p.y), __dsub_rn(q.z, p.z));
+        const double L = __dadd_rn(l[a], lb);
+        double w = (L > 0.0) ? __drcp_rn(L) : 0.0;
+        w = valid ? w : 0.0;
+        a0 = __dadd_rn(a0, __dmul_rn(w, __dsub_rn(__dmul_rn(vy[a], bz), __dmul_rn(vz[a], by))));
+        a1 = __dadd_rn(a1, __dmul_rn(w, __dsub_rn(__dmul_rn(vz[a], bx), __dmul_rn(vx[a], bz))));
+        a2 = __dadd_rn(a2, __dmul_rn(w, __dsub_rn(__dmul_rn(vx[a], by), __dmul_rn(vy[a], bx))));
+        ws = __dadd_rn(ws, w);
+      }
+      if (cnt >= 2 && ws > 0.0) {
+        const double m0 = __ddiv_rn(a0, ws), m1 = __ddiv_rn(a1, ws), m2 = __ddiv_rn(a2, ws);
+        const double mag = norm3(m0, m1, m2);
+        if (mag >= 1e-12) {
+          double u0 = __ddiv_rn(m0, mag), u1 = __ddiv_rn(m1, mag), u2 = __ddiv_rn(m2, mag);
+          const double dot = __dadd_rn(__dadd_rn(__dmul_rn(u0, p.x), __dmul_rn(u2, p.z)), __dmul_rn(u1, p.y));
+          if (dot > 0.0) { u0 = -u0; u1 = -u1; u2 = -u2; }
+          nv[0] = u0; nv[1] = u1; nv[2] = u2;
+          ok = true;
         }
-        ok = fan.finish(p, nv);
       }
     }
     s_nx[e] = nv[0];
     s_ny[e] = nv[1];
     s_nz[e] = nv[2];
     s_has[e] = ok ? 1 : 0;
-    s_par[e] = e;
   }
   __syncthreads();
 
@@ -226,23 +260,26 @@ __global__ void __launch_bounds__(T, 3) k_tile(lseg_sensor sn, Shape sh, const d
     }
   }
 
-  // D. local components.  D1: one warp per tile row turns the passing
-  // horizontal edges into 64-bit masks; every node's parent becomes the start
-  // of its horizontal run (bit arithmetic, no atomics).  D2: vertical /
-  // diagonal edges join runs with shared-memory union-find, skipping an edge
-  // when the parallel edge one column to the left already joins the same two
-  // runs.  D3: column-wrap edges of a full-width tile (S' <= TC).
+  // D. homogeneity test on the tile's internal forward edges, one warp per
+  // tile row, as 64-bit masks per row (bit x = column x):
+  //   H  (y,x)->(y,x+1)   V0 (y,x)->(y+1,x)   V1 (y,x)->(y+1,x+1)
+  //   HAS  node with a normal;  W bit0/bit1 = column-wrap right / diagonal edge
+  //   of x = S'-1 in a full-width tile (S' <= TC).
+  // k_tile_cc turns them into tile-local components.
   static_assert(TC == 64, "row masks assume 64-column tiles");
-  __shared__ unsigned long long s_H[TR], s_V0[TR], s_V1[TR];
   const int lane = tid & 31;
-  for (int y = tid >> 5; y < TR && !(dbg & 2); y += T / 32) {
-    unsigned long long H = 0, V0 = 0, V1 = 0;
+  const bool full_width = (c0 == 0 && TCe == sh.Sk);
+  unsigned long long* mrow = masks + (((int64_t)f * tilesR + r0 / TR) * tilesC + c0 / TC) * (TR * 5);
+  for (int y = tid >> 5; y < TR; y += T / 32) {
+    unsigned long long H = 0, V0 = 0, V1 = 0, HS = 0;
+    bool w0 = false, w1 = false;
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
       const int x = lane + 32 * half;
       const int e = y * TC + x;
       bool h = false, v0 = false, v1 = false;
-      if (y < TRe && s_has[e]) {
+      const bool has = (y < TRe) && s_has[e];
+      if (has) {
         const double a[3] = {s_nx[e], s_ny[e], s_nz[e]};
         if (x + 1 < TCe && s_has[e + 1]) {
           const double q[3] = {s_nx[e + 1], s_ny[e + 1], s_nz[e + 1]};
@@ -258,26 +295,68 @@ __global__ void __launch_bounds__(T, 3) k_tile(lseg_sensor sn, Shape sh, const d
             v1 = normals_pass(a, q, t0, t1, t2);
           }
         }
+        if (full_width && x == TCe - 1) {
+          const int e0 = y * TC;  // (y, 0)
+          if (TCe > 1 && s_has[e0]) {
+            const double q[3] = {s_nx[e0], s_ny[e0], s_nz[e0]};
+            w0 = normals_pass(a, q, t0, t1, t2);
+          }
+          if (y + 1 < TRe && s_has[e0 + TC]) {
+            const double q[3] = {s_nx[e0 + TC], s_ny[e0 + TC], s_nz[e0 + TC]};
+            w1 = normals_pass(a, q, t0, t1, t2);
+          }
+        }
       }
       const unsigned long long sh_ = half ? 32 : 0;
       H |= (unsigned long long)__ballot_sync(0xffffffffu, h) << sh_;
       V0 |= (unsigned long long)__ballot_sync(0xffffffffu, v0) << sh_;
       V1 |= (unsigned long long)__ballot_sync(0xffffffffu, v1) << sh_;
+      HS |= (unsigned long long)__ballot_sync(0xffffffffu, has) << sh_;
     }
-    if (lane == 0) { s_H[y] = H; s_V0[y] = V0; s_V1[y] = V1; }
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const int x = lane + 32 * half;
-      const unsigned long long Z = ~H & ((1ull << x) - 1ull);
-      const int start = Z ? 64 - __clzll((long long)Z) : 0;
-      s_par[y * TC + x] = y * TC + start;
+    const unsigned W = (__ballot_sync(0xffffffffu, w0) ? 1u : 0u) | (__ballot_sync(0xffffffffu, w1) ? 2u : 0u);
+    if (lane == 0) {
+      mrow[y * 5 + 0] = H;
+      mrow[y * 5 + 1] = V0;
+      mrow[y * 5 + 2] = V1;
+      mrow[y * 5 + 3] = HS;
+      mrow[y * 5 + 4] = W;
     }
   }
+}
+
+// Tile-local connected components from k_tile's masks (one small CTA per
+// tile): each node's parent starts as the first cell of its horizontal run
+// (bit arithmetic), vertical / diagonal edges join runs with shared-memory
+// union-find -- skipping an edge when the parallel edge one column to the left
+// already joins the same two runs -- and each labelled cell gets
+// parent[cell] = minimum cell of its tile-local component (-1 without normal).
+template <int TR, int TC, int T>
+__global__ void __launch_bounds__(T) k_tile_cc(Shape sh, const unsigned long long* __restrict__ masks,
+                                               int32_t* __restrict__ parent) {
+  constexpr int NT = TR * TC;
+  __shared__ int s_par[NT];
+  __shared__ unsigned long long s_m[TR * 5];
+  const int tilesC = (sh.Sk + TC - 1) / TC;
+  const int tilesR = (sh.R + TR - 1) / TR;
+  const int64_t b = blockIdx.x;
+  const int f = (int)(b / ((int64_t)tilesR * tilesC));
+  const int rem = (int)(b - (int64_t)f * tilesR * tilesC);
+  const int r0 = (rem / tilesC) * TR, c0 = (rem % tilesC) * TC;
+  const int TRe = min(TR, sh.R - r0), TCe = min(TC, sh.Sk - c0);
+  const unsigned long long* mrow = masks + b * (TR * 5);
+  for (int j = threadIdx.x; j < TR * 5; j += T) s_m[j] = __ldg(mrow + j);
   __syncthreads();
-  for (int e = tid; e < NT && !(dbg & 2); e += T) {
+  for (int e = threadIdx.x; e < NT; e += T) {
     const int y = e / TC, x = e - y * TC;
-    if (y + 1 >= TRe || !s_has[e]) continue;
-    const unsigned long long Hy = s_H[y], Hn = s_H[y + 1], V0 = s_V0[y], V1 = s_V1[y];
+    const unsigned long long Z = ~s_m[y * 5] & ((1ull << x) - 1ull);
+    s_par[e] = y * TC + (Z ? 64 - __clzll((long long)Z) : 0);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < NT; e += T) {
+    const int y = e / TC, x = e - y * TC;
+    if (y + 1 >= TRe) continue;
+    const unsigned long long Hy = s_m[y * 5], V0 = s_m[y * 5 + 1], V1 = s_m[y * 5 + 2];
+    const unsigned long long Hn = s_m[(y + 1) * 5];
     const unsigned long long bx = 1ull << x, bl = bx >> 1;
     if (V0 & bx) {
       const bool dup = x > 0 && (Hy & bl) && (Hn & bl) && (V0 & bl);
@@ -288,31 +367,18 @@ __global__ void __launch_bounds__(T, 3) k_tile(lseg_sensor sn, Shape sh, const d
       if (!dup) lunion(s_par, e, e + TC + 1);
     }
   }
-  if (c0 == 0 && TCe == sh.Sk && !(dbg & 2)) {  // full-width tile: wrap edges (x = S'-1 -> 0)
-    for (int y = tid; y < TRe; y += T) {
-      const int e = y * TC + TCe - 1;
-      if (!s_has[e]) continue;
-      const double a[3] = {s_nx[e], s_ny[e], s_nz[e]};
-      const int t2e = y * TC;  // (y, 0)
-      if (TCe > 1 && s_has[t2e]) {
-        const double q[3] = {s_nx[t2e], s_ny[t2e], s_nz[t2e]};
-        if (normals_pass(a, q, t0, t1, t2)) lunion(s_par, e, t2e);
-      }
-      const int t1e = (y + 1) * TC;  // (y+1, 0)
-      if (y + 1 < TRe && s_has[t1e]) {
-        const double q[3] = {s_nx[t1e], s_ny[t1e], s_nz[t1e]};
-        if (normals_pass(a, q, t0, t1, t2)) lunion(s_par, e, t1e);
-      }
-    }
+  for (int y = threadIdx.x; y < TRe; y += T) {  // full-width column wrap (x = S'-1 -> 0)
+    const unsigned W = (unsigned)s_m[y * 5 + 4];
+    if (W & 1u) lunion(s_par, y * TC + TCe - 1, y * TC);
+    if (W & 2u) lunion(s_par, y * TC + TCe - 1, (y + 1) * TC);
   }
   __syncthreads();
-
-  // E. tile-local roots (min cell of each local component) -> parent
-  for (int e = tid; e < NT; e += T) {
+  const int64_t nbase = (int64_t)f * sh.cap;
+  for (int e = threadIdx.x; e < NT; e += T) {
     const int y = e / TC, x = e - y * TC;
     if (y >= TRe || x >= TCe) continue;
     int pc = -1;
-    if (s_has[e]) {
+    if ((s_m[y * 5 + 3] >> x) & 1ull) {
       const int lr = lfind(s_par, e);
       pc = (r0 + lr / TC) * sh.Sk + c0 + lr % TC;
     }
@@ -819,10 +885,19 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
                         int32_t* n_nodes, int32_t* n_labels, int32_t* node_labels, cudaStream_t st) {
   const int tilesC = (sh.Sk + TILE_C - 1) / TILE_C, tilesR = (sh.R + TILE_R - 1) / TILE_R;
   const int64_t nt = (int64_t)sh.F * tilesR * tilesC;
-  k_tile<TILE_R, TILE_C, TILE_T><<<(unsigned)nt, TILE_T, 0, st>>>(sn, sh, ranges, ws.vbits, ws.wpre, thr[0], thr[1],
-                                                                  thr[2], node_ids, neighbors, n32, nmask, ws.parent,
+  const size_t tsmem = (size_t)(3 * (TILE_R + 2) * (TILE_C + 2) + 3 * TILE_R * TILE_C) * 8 +
+                       (size_t)(TILE_R + 2) * (TILE_C + 2) * 4 + (size_t)TILE_R * TILE_C;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_tile<TILE_R, TILE_C, TILE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+    attr_set = true;
+  }
+  k_tile<TILE_R, TILE_C, TILE_T><<<(unsigned)nt, TILE_T, tsmem, st>>>(sn, sh, ranges, ws.vbits, ws.wpre, thr[0], thr[1],
+                                                                  thr[2], node_ids, neighbors, n32, nmask, ws.masks,
                                                                   ws.bnorm, g_tile_dbg);
   prof_mark("tile", st);
+  k_tile_cc<TILE_R, TILE_C, 128><<<(unsigned)nt, 128, 0, st>>>(sh, ws.masks, ws.parent);
+  prof_mark("tile_cc", st);
   const int64_t nb = ((int64_t)tilesR * sh.Sk + (int64_t)tilesC * sh.R) * sh.F;
   k_merge<TILE_R, TILE_C><<<(unsigned)((nb + 255) / 256 < 148 * 32 ? (nb + 255) / 256 : 148 * 32), 256, 0, st>>>(
       sh, ws.bnorm, thr[0], thr[1], thr[2], ws.parent);
