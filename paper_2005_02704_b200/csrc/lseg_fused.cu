@@ -21,7 +21,6 @@ namespace lseg {
 static constexpr int TILE_R = 16;
 static constexpr int TILE_C = 64;
 static constexpr int TILE_T = 256;
-static const int g_tile_dbg = getenv("LSEG_DEBUG_TILE") ? atoi(getenv("LSEG_DEBUG_TILE")) : 0;
 
 __device__ __forceinline__ int wrapc(int c, int Sk) { return c < 0 ? c + Sk : (c >= Sk ? c - Sk : c); }
 
@@ -109,7 +108,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
                                                 double t0, double t1, double t2, int32_t* __restrict__ node_ids,
                                                 int32_t* __restrict__ neighbors, float* __restrict__ n32,
                                                 uint8_t* __restrict__ nmask, unsigned long long* __restrict__ masks,
-                                                double* __restrict__ bnorm, int dbg) {
+                                                double* __restrict__ bnorm) {
   constexpr int GR = TR + 2, GC = TC + 2;  // halo rows r0-1..r0+TR, cols c0-1..c0+TC
   constexpr int NT = TR * TC;
   // dynamic shared memory (58 KB > the 48 KB static limit), see tile_smem_bytes()
@@ -121,7 +120,9 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   double* s_ny = s_nx + NT;
   double* s_nz = s_ny + NT;
   int* s_id = reinterpret_cast<int*>(s_nz + NT);
-  uint8_t* s_has = reinterpret_cast<uint8_t*>(s_id + GR * GC);
+  unsigned short* s_list = reinterpret_cast<unsigned short*>(s_id + GR * GC);  // fan6 list from the front, rest from the back
+  uint8_t* s_has = reinterpret_cast<uint8_t*>(s_list + NT);
+  uint8_t* s_m = s_has + NT;  // presence mask of general-path nodes
 
   const int tilesC = (sh.Sk + TC - 1) / TC;
   const int tilesR = (sh.R + TR - 1) / TR;
@@ -154,74 +155,101 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   }
   __syncthreads();
 
-  // B. fp64 normals (reference normals.py:94-145 operation order), branch-free
-  // over the presence pattern so a warp never runs two code paths: every slot
-  // forms the pair (a, next present slot after a); pairs the reference does
-  // not form get weight 0, which adds exact zeros to the sums.
-  for (int e = tid; e < NT; e += T) {
-    const int y = e / TC, x = e - y * TC;
-    bool ok = false;
-    double nv[3] = {0.0, 0.0, 0.0};
-    const int g = (y + 1) * GC + (x + 1);
-    if (y < TRe && x < TCe && s_id[g] >= 0 && (dbg & 1)) {
-      ok = true;
-      nv[2] = 1.0;
-    } else if (y < TRe && x < TCe && s_id[g] >= 0) {
-      const Vec3 p = {s_px[g], s_py[g], s_pz[g]};
+  // B. fp64 normals (reference normals.py:94-145 operation order).  Nodes are
+  // first sorted into two work lists so that no warp runs both code paths:
+  // nodes with all 6 slots (the common case) take the straight-line fan6,
+  // the rest the streaming Fan over their present slots.
+  __shared__ int s_cnt[2 * (T / 32) + 2];
+  {
+    const int lane = tid & 31, warp = tid >> 5;
+    unsigned char ml[(NT + T - 1) / T];
+    int kind[(NT + T - 1) / T];  // 0 none, 1 fan6, 2 general
+    int na = 0, nb = 0;
+#pragma unroll
+    for (int j = 0; j < (NT + T - 1) / T; ++j) {
+      const int e = tid + j * T;
+      const int y = e / TC, x = e - y * TC;
+      const int g = (y + 1) * GC + (x + 1);
       unsigned m = 0;
-      double vx[6], vy[6], vz[6], l[6];
+      kind[j] = 0;
+      if (e < NT && y < TRe && x < TCe && s_id[g] >= 0) {
 #pragma unroll
-      for (int s = 0; s < 6; ++s) {
-        const int gq = g + slot_dr(s) * GC + slot_dc(s);
-        const bool pr = s_id[gq] >= 0 && !(s == 5 && sh.Sk == 2);  // mesh.py:96-101 dedupe
-        m |= pr ? (1u << s) : 0u;
-        vx[s] = pr ? __dsub_rn(s_px[gq], p.x) : 0.0;
-        vy[s] = pr ? __dsub_rn(s_py[gq], p.y) : 0.0;
-        vz[s] = pr ? __dsub_rn(s_pz[gq], p.z) : 0.0;
-        l[s] = norm3(vx[s], vy[s], vz[s]);
+        for (int s = 0; s < 6; ++s)
+          if (s_id[g + slot_dr(s) * GC + slot_dc(s)] >= 0 && !(s == 5 && sh.Sk == 2)) m |= 1u << s;  // mesh.py:96-101
+        kind[j] = (m == 0x3fu) ? 1 : 2;
       }
-      const int cnt = __popc(m);
-      const int last = 31 - __clz(m | 1u);
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, ws = 0.0;
-#pragma unroll
-      for (int a = 0; a < 6; ++a) {
-        const unsigned rot = ((m >> (a + 1)) | (m << (5 - a))) & 0x1fu;  // slots a+1 .. a+5 (mod 6)
-        const int j = __ffs(rot) - 1;                                     // partner = a+1+j (mod 6)
-        const bool valid = ((m >> a) & 1u) && cnt >= 2 && !(cnt == 2 && a == last);
-        double bx = vx[(a + 1) % 6], by = vy[(a + 1) % 6], bz = vz[(a + 1) % 6], lb = l[(a + 1) % 6];
-#pragma unroll
-        for (int k = 1; k < 5; ++k) {
-          const int c = (a + 1 + k) % 6;
-          const bool pick = (j == k);
-          bx = pick ? vx[c] : bx;
-          by = pick ? vy[c] : by;
-          bz = pick ? vz[c] : bz;
-          lb = pick ? l[c] : lb;
-        }
-        const double L = __dadd_rn(l[a], lb);
-        double w = (L > 0.0) ? __drcp_rn(L) : 0.0;
-        w = valid ? w : 0.0;
-        a0 = __dadd_rn(a0, __dmul_rn(w, __dsub_rn(__dmul_rn(vy[a], bz), __dmul_rn(vz[a], by))));
-        a1 = __dadd_rn(a1, __dmul_rn(w, __dsub_rn(__dmul_rn(vz[a], bx), __dmul_rn(vx[a], bz))));
-        a2 = __dadd_rn(a2, __dmul_rn(w, __dsub_rn(__dmul_rn(vx[a], by), __dmul_rn(vy[a], bx))));
-        ws = __dadd_rn(ws, w);
-      }
-      if (cnt >= 2 && ws > 0.0) {
-        const double m0 = __ddiv_rn(a0, ws), m1 = __ddiv_rn(a1, ws), m2 = __ddiv_rn(a2, ws);
-        const double mag = norm3(m0, m1, m2);
-        if (mag >= 1e-12) {
-          double u0 = __ddiv_rn(m0, mag), u1 = __ddiv_rn(m1, mag), u2 = __ddiv_rn(m2, mag);
-          const double dot = __dadd_rn(__dadd_rn(__dmul_rn(u0, p.x), __dmul_rn(u2, p.z)), __dmul_rn(u1, p.y));
-          if (dot > 0.0) { u0 = -u0; u1 = -u1; u2 = -u2; }
-          nv[0] = u0; nv[1] = u1; nv[2] = u2;
-          ok = true;
-        }
-      }
+      ml[j] = (unsigned char)m;
+      na += kind[j] == 1;
+      nb += kind[j] == 2;
+      if (e < NT) { s_has[e] = 0; s_nx[e] = s_ny[e] = s_nz[e] = 0.0; }
     }
-    s_nx[e] = nv[0];
-    s_ny[e] = nv[1];
-    s_nz[e] = nv[2];
-    s_has[e] = ok ? 1 : 0;
+    // block-wide exclusive offsets of (na, nb): warp scan + per-warp totals
+    int ia = na, ib = nb;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ta = __shfl_up_sync(0xffffffffu, ia, o), tb = __shfl_up_sync(0xffffffffu, ib, o);
+      if (lane >= o) { ia += ta; ib += tb; }
+    }
+    if (lane == 31) { s_cnt[warp] = ia; s_cnt[T / 32 + warp] = ib; }
+    __syncthreads();
+    int oa = 0, ob = 0, ta = 0, tb = 0;
+    for (int w = 0; w < T / 32; ++w) {
+      if (w < warp) { oa += s_cnt[w]; ob += s_cnt[T / 32 + w]; }
+      ta += s_cnt[w];
+      tb += s_cnt[T / 32 + w];
+    }
+    oa += ia - na;
+    ob += ib - nb;
+#pragma unroll
+    for (int j = 0; j < (NT + T - 1) / T; ++j) {
+      const int e = tid + j * T;
+      if (kind[j] == 1) s_list[oa++] = (unsigned short)e;
+      else if (kind[j] == 2) { s_list[NT - 1 - ob] = (unsigned short)e; s_m[e] = ml[j]; ++ob; }
+    }
+    if (tid == 0) { s_cnt[2 * (T / 32)] = ta; s_cnt[2 * (T / 32) + 1] = tb; }
+  }
+  __syncthreads();
+  const int nfan6 = s_cnt[2 * (T / 32)], ngen = s_cnt[2 * (T / 32) + 1];
+  for (int i = tid; i < nfan6; i += T) {
+    const int e = s_list[i];
+    const int y = e / TC, x = e - y * TC;
+    const int g = (y + 1) * GC + (x + 1);
+    const Vec3 p = {s_px[g], s_py[g], s_pz[g]};
+    double vx[6], vy[6], vz[6], nv[3];
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const int gq = g + slot_dr(s) * GC + slot_dc(s);
+      vx[s] = __dsub_rn(s_px[gq], p.x);
+      vy[s] = __dsub_rn(s_py[gq], p.y);
+      vz[s] = __dsub_rn(s_pz[gq], p.z);
+    }
+    if (fan6(vx, vy, vz, p, nv)) {
+      s_nx[e] = nv[0];
+      s_ny[e] = nv[1];
+      s_nz[e] = nv[2];
+      s_has[e] = 1;
+    }
+  }
+  for (int i = tid; i < ngen; i += T) {
+    const int e = s_list[NT - 1 - i];
+    const int y = e / TC, x = e - y * TC;
+    const int g = (y + 1) * GC + (x + 1);
+    const unsigned m = s_m[e];
+    const Vec3 p = {s_px[g], s_py[g], s_pz[g]};
+    Fan fan;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      if (!((m >> s) & 1u)) continue;
+      const int gq = g + slot_dr(s) * GC + slot_dc(s);
+      fan.add(__dsub_rn(s_px[gq], p.x), __dsub_rn(s_py[gq], p.y), __dsub_rn(s_pz[gq], p.z));
+    }
+    double nv[3];
+    if (fan.finish(p, nv)) {
+      s_nx[e] = nv[0];
+      s_ny[e] = nv[1];
+      s_nz[e] = nv[2];
+      s_has[e] = 1;
+    }
   }
   __syncthreads();
 
@@ -886,7 +914,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   const int tilesC = (sh.Sk + TILE_C - 1) / TILE_C, tilesR = (sh.R + TILE_R - 1) / TILE_R;
   const int64_t nt = (int64_t)sh.F * tilesR * tilesC;
   const size_t tsmem = (size_t)(3 * (TILE_R + 2) * (TILE_C + 2) + 3 * TILE_R * TILE_C) * 8 +
-                       (size_t)(TILE_R + 2) * (TILE_C + 2) * 4 + (size_t)TILE_R * TILE_C;
+                       (size_t)(TILE_R + 2) * (TILE_C + 2) * 4 + (size_t)TILE_R * TILE_C * 4;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k_tile<TILE_R, TILE_C, TILE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
@@ -894,7 +922,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   }
   k_tile<TILE_R, TILE_C, TILE_T><<<(unsigned)nt, TILE_T, tsmem, st>>>(sn, sh, ranges, ws.vbits, ws.wpre, thr[0], thr[1],
                                                                   thr[2], node_ids, neighbors, n32, nmask, ws.masks,
-                                                                  ws.bnorm, g_tile_dbg);
+                                                                  ws.bnorm);
   prof_mark("tile", st);
   k_tile_cc<TILE_R, TILE_C, 128><<<(unsigned)nt, 128, 0, st>>>(sh, ws.masks, ws.parent);
   prof_mark("tile_cc", st);
