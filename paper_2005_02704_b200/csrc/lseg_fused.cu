@@ -374,25 +374,28 @@ __global__ void __launch_bounds__(T) k_tile_cc(Shape sh, const unsigned long lon
   const unsigned long long* mrow = masks + b * (TR * 5);
   for (int j = threadIdx.x; j < TR * 5; j += T) s_m[j] = __ldg(mrow + j);
   __syncthreads();
+  // run starts: parent of every cell = first cell of its horizontal run
   for (int e = threadIdx.x; e < NT; e += T) {
     const int y = e / TC, x = e - y * TC;
     const unsigned long long Z = ~s_m[y * 5] & ((1ull << x) - 1ull);
     s_par[e] = y * TC + (Z ? 64 - __clzll((long long)Z) : 0);
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < NT; e += T) {
-    const int y = e / TC, x = e - y * TC;
-    if (y + 1 >= TRe) continue;
+  // vertical / diagonal unions, one warp per row pair: edges whose parallel
+  // edge one column to the left already joins the same two runs are dropped
+  // with 64-bit mask arithmetic before any union-find work
+  const int lane = threadIdx.x & 31;
+  for (int y = threadIdx.x >> 5; y + 1 < TRe; y += T / 32) {
     const unsigned long long Hy = s_m[y * 5], V0 = s_m[y * 5 + 1], V1 = s_m[y * 5 + 2];
     const unsigned long long Hn = s_m[(y + 1) * 5];
-    const unsigned long long bx = 1ull << x, bl = bx >> 1;
-    if (V0 & bx) {
-      const bool dup = x > 0 && (Hy & bl) && (Hn & bl) && (V0 & bl);
-      if (!dup) lunion(s_par, e, e + TC);
-    }
-    if (V1 & bx) {
-      const bool dup = ((V0 & bx) && (Hn & bx)) || (x > 0 && (Hy & bl) && (Hn & bx) && (V1 & bl));
-      if (!dup) lunion(s_par, e, e + TC + 1);
+    const unsigned long long U0 = V0 & ~((Hy << 1) & (Hn << 1) & (V0 << 1));
+    const unsigned long long U1 = V1 & ~((V0 & Hn) | ((Hy << 1) & Hn & (V1 << 1)));
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int x = lane + 32 * half;
+      const int e = y * TC + x;
+      if ((U0 >> x) & 1ull) lunion(s_par, e, e + TC);
+      if ((U1 >> x) & 1ull) lunion(s_par, e, e + TC + 1);
     }
   }
   for (int y = threadIdx.x; y < TRe; y += T) {  // full-width column wrap (x = S'-1 -> 0)
@@ -401,13 +404,22 @@ __global__ void __launch_bounds__(T) k_tile_cc(Shape sh, const unsigned long lon
     if (W & 2u) lunion(s_par, y * TC + TCe - 1, (y + 1) * TC);
   }
   __syncthreads();
+  // resolve each run start to its component root (minimum cell) ...
+  for (int e = threadIdx.x; e < NT; e += T) {
+    const int y = e / TC, x = e - y * TC;
+    const unsigned long long H = s_m[y * 5];
+    if (x == 0 || !((H >> (x - 1)) & 1ull)) s_par[e] = lfind(s_par, e);
+  }
+  __syncthreads();
+  // ... and give every labelled cell its run start's root
   const int64_t nbase = (int64_t)f * sh.cap;
   for (int e = threadIdx.x; e < NT; e += T) {
     const int y = e / TC, x = e - y * TC;
     if (y >= TRe || x >= TCe) continue;
     int pc = -1;
     if ((s_m[y * 5 + 3] >> x) & 1ull) {
-      const int lr = lfind(s_par, e);
+      const unsigned long long Z = ~s_m[y * 5] & ((1ull << x) - 1ull);
+      const int lr = s_par[y * TC + (Z ? 64 - __clzll((long long)Z) : 0)];
       pc = (r0 + lr / TC) * sh.Sk + c0 + lr % TC;
     }
     parent[nbase + (int64_t)(r0 + y) * sh.Sk + c0 + x] = pc;
@@ -420,28 +432,27 @@ __global__ void __launch_bounds__(T) k_tile_cc(Shape sh, const unsigned long lon
 template <int TR, int TC>
 __global__ void k_merge(Shape sh, const double* __restrict__ bnorm, double t0, double t1, double t2,
                         int32_t* __restrict__ parent) {
+  // blockIdx.y = frame; threads enumerate the frame's border cells
+  const int f = blockIdx.y;
   const int nbr = (sh.R + TR - 1) / TR;
   const int nbc = (sh.Sk + TC - 1) / TC;
-  const int64_t per = (int64_t)nbr * sh.Sk + (int64_t)nbc * sh.R;
-  const int64_t n = per * sh.F;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    const int f = (int)(t / per);
-    int64_t u = t - (int64_t)f * per;
+  const int per = nbr * sh.Sk + nbc * sh.R;
+  int32_t* par = parent + (int64_t)f * sh.cap;
+  const double* bn = bnorm + (int64_t)f * sh.cap * 3;
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < per; u += gridDim.x * blockDim.x) {
     int r, c;
-    if (u < (int64_t)nbr * sh.Sk) {
-      const int br = (int)(u / sh.Sk);
+    if (u < nbr * sh.Sk) {
+      const int br = u / sh.Sk;
       r = min(br * TR + TR - 1, sh.R - 1);
-      c = (int)(u - (int64_t)br * sh.Sk);
+      c = u - br * sh.Sk;
     } else {
-      u -= (int64_t)nbr * sh.Sk;
-      const int bc = (int)(u / sh.R);
+      const int v = u - nbr * sh.Sk;
+      const int bc = v / sh.R;
       c = min(bc * TC + TC - 1, sh.Sk - 1);
-      r = (int)(u - (int64_t)bc * sh.R);
+      r = v - bc * sh.R;
     }
-    int32_t* par = parent + (int64_t)f * sh.cap;
     const int p = r * sh.Sk + c;
     if (__ldcg(par + p) < 0) continue;  // no normal
-    const double* bn = bnorm + (int64_t)f * sh.cap * 3;
     const double a[3] = {__ldcg(bn + 3 * p), __ldcg(bn + 3 * p + 1), __ldcg(bn + 3 * p + 2)};
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
@@ -467,27 +478,27 @@ __device__ __forceinline__ int root_of(const int32_t* __restrict__ par, int x) {
 // and zero each root's histogram slot (labels are root cell + 1 until pruning).
 __global__ void k_root_flatten(Shape sh, int32_t* __restrict__ parent, uint32_t* __restrict__ rbits,
                                int32_t* __restrict__ hist, int64_t K) {
-  const int64_t nwords = (int64_t)sh.F * sh.R * sh.Wk;
+  // one CTA per ring row (f, i), one warp per 32-cell word: no 64-bit division
+  const int row = blockIdx.x;
+  const int f = row / sh.R, i = row - f * sh.R;
   const int lane = threadIdx.x & 31;
-  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nwords;
-       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t row = w / sh.Wk;
-    const int c = (int)(w - row * sh.Wk) * 32 + lane;
-    const int f = (int)(row / sh.R);
+  int32_t* par = parent + (int64_t)f * sh.cap;
+  int32_t* hf = hist + (int64_t)f * K;
+  for (int w = threadIdx.x >> 5; w < sh.Wk; w += blockDim.x >> 5) {
+    const int c = w * 32 + lane;
     bool root = false;
     if (c < sh.Sk) {
-      int32_t* par = parent + (int64_t)f * sh.cap;
-      const int cell = (int)(row - (int64_t)f * sh.R) * sh.Sk + c;
+      const int cell = i * sh.Sk + c;
       const int p = __ldcg(par + cell);
       if (p >= 0) {
         const int r = root_of(par, p);
         if (r != p) par[cell] = r;
         root = (r == cell);
-        if (root) hist[(int64_t)f * K + cell + 1] = 0;
+        if (root) hf[cell + 1] = 0;
       }
     }
     const uint32_t b = __ballot_sync(0xffffffffu, root);
-    if (lane == 0) rbits[w] = b;
+    if (lane == 0) rbits[(int64_t)row * sh.Wk + w] = b;
   }
 }
 
@@ -497,8 +508,61 @@ __device__ __forceinline__ int rank_label(const uint32_t* bf, const int32_t* pf,
   return 1 + node_id_at(bf + (int64_t)rr * Wk, pf + (int64_t)rr * Wk, cc);
 }
 
-// Node labels + backfill + histogram for one ring row per CTA.
-template <int T, int ITEMS>
+// Nearest donor of target cell s in a ring row (reference segment.py:91-106:
+// cyclic step distance, ties to the smaller actual step index), from the
+// row's donor bitmask in shared memory.  Scans 32-cell words outward from s;
+// the row must hold at least one donor.
+__device__ __forceinline__ int nearest_donor(const uint32_t* s_dm, int nw, int S, int s) {
+  const int w = s >> 5, b = s & 31;
+  // left: highest donor < s (cyclic)
+  int left;
+  {
+    uint32_t m = s_dm[w] & ((1u << b) - 1u);
+    int ww = w;
+    while (!m) {
+      ww = (ww == 0) ? nw - 1 : ww - 1;
+      m = s_dm[ww];
+      if (ww == w) m &= ~((1u << b) - 1u) & ~(1u << b);  // wrapped to own word: only cells > s remain
+    }
+    left = ww * 32 + 31 - __clz(m);
+  }
+  int right;
+  {
+    uint32_t m = (b == 31) ? 0u : (s_dm[w] & ~((2u << b) - 1u));
+    int ww = w;
+    while (!m) {
+      ww = (ww + 1 == nw) ? 0 : ww + 1;
+      m = s_dm[ww];
+      if (ww == w) m &= (1u << b) - 1u;  // wrapped to own word: only cells < s remain
+    }
+    right = ww * 32 + __ffs(m) - 1;
+  }
+  int dl = s - left;
+  if (dl <= 0) dl += S;
+  int dr = right - s;
+  if (dr <= 0) dr += S;
+  return dl < dr ? left : (dr < dl ? right : min(left, right));
+}
+
+// Shared body of the two ring-row kernels: s_val[s] holds a donor label (> 0),
+// 0 (passive: stays 0) or -2 (target: nearest donor's label, 0 if the row has
+// no donor); s_dm the donor bits.  Returns the filled label of cell s.
+__device__ __forceinline__ int fill_one(const int* s_val, const uint32_t* s_dm, int nw, int S, int s, bool any) {
+  const int v = s_val[s];
+  if (v != -2) return v > 0 ? v : 0;
+  return any ? s_val[nearest_donor(s_dm, nw, S, s)] : 0;
+}
+
+// Warp-aggregated histogram increment (adjacent cells mostly share a label).
+__device__ __forceinline__ void hist_add(int32_t* hw, int lab) {
+  const unsigned m = __match_any_sync(0xffffffffu, lab);
+  if (lab > 0 && (threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(hw + lab, __popc(m));
+}
+
+// Node labels + backfill + histogram, one CTA per ring row.  Provisional
+// label ids are root cell + 1 (ascending root cell == ascending reference
+// label, so the compaction in k_prune_rows reproduces the reference ids).
+template <int T>
 __global__ void __launch_bounds__(T) k_labels_backfill(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
                                                        const uint32_t* __restrict__ vbits,
                                                        const int32_t* __restrict__ parent,
@@ -506,111 +570,49 @@ __global__ void __launch_bounds__(T) k_labels_backfill(lseg_sensor sn, Shape sh,
                                                        const int32_t* __restrict__ rpre,
                                                        int32_t* __restrict__ node_labels, int32_t* __restrict__ out,
                                                        int32_t* __restrict__ hist, int64_t K) {
-  using Scan = cub::BlockScan<int, T>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ int s_first[T];
-  __shared__ int s_next[T];
-  __shared__ int s_gfirst, s_glast;
-  extern __shared__ int s_row[];
-  const int64_t row = blockIdx.x;
-  const int f = (int)(row / sh.R), i = (int)(row - (int64_t)f * sh.R);
-  const int S = sh.S;
-  const uint32_t* vbr = vbits + row * sh.Wk;
-  const int32_t* par = parent + (int64_t)f * sh.cap;
-
-  // node labels of this row, provisional ids = root cell + 1 (ascending root
-  // cell == ascending reference label, so the final compaction in
-  // k_prune_rows reproduces the reference ids); -1 marks an invalid kept cell
-  // (so k = 1 needs no ranges read for validity)
+  extern __shared__ int s_dynrow[];
+  const int S = sh.S, nw = (S + 31) / 32;
+  int* s_val = s_dynrow;
+  uint32_t* s_dm = reinterpret_cast<uint32_t*>(s_dynrow + nw * 32);
+  __shared__ int s_any;
+  const int row = blockIdx.x;
+  const int f = row / sh.R, i = row - f * sh.R;
+  const uint32_t* vbr = vbits + (int64_t)row * sh.Wk;
+  const int32_t* par = parent + (int64_t)f * sh.cap + (int64_t)i * sh.Sk;
   const uint32_t* rbf = rbits + (int64_t)f * sh.R * sh.Wk;
   const int32_t* rpf = rpre + (int64_t)f * sh.R * sh.Wk;
-  for (int s = threadIdx.x; s < S; s += T) {
-    int lab = 0;
-    if (s % sh.k == 0) {
-      const int c = s / sh.k;
-      const int p = __ldcg(par + i * sh.Sk + c);  // flattened: p is the root cell
-      if (p >= 0) lab = p + 1;
-      else if (!((__ldg(vbr + (c >> 5)) >> (c & 31)) & 1u)) lab = -1;
-    }
-    s_row[s] = lab;
-  }
+  const int64_t rb = (int64_t)row * S;
+  if (threadIdx.x == 0) s_any = 0;
   __syncthreads();
-  if (node_labels)  // reference segment() output: 1 + rank of the root
-    for (int s = threadIdx.x; s < S; s += T) {
-      const int v = s_row[s];
-      node_labels[row * S + s] = v > 0 ? rank_label(rbf, rpf, sh.Wk, sh.Sk, v - 1) : 0;
-    }
-
-  const int s0 = threadIdx.x * ITEMS;
-  int lab[ITEMS];
-  bool valid[ITEMS];
-  int last = INT_MIN, first = INT_MAX;
-#pragma unroll
-  for (int j = 0; j < ITEMS; ++j) {
-    const int s = s0 + j;
-    lab[j] = 0;
-    valid[j] = false;
+  bool any = false;
+  for (int s = threadIdx.x; s < nw * 32; s += T) {  // classify: donor label / target -2 / passive 0
+    int v = 0;
     if (s < S) {
-      const int v = s_row[s];
-      if (sh.k == 1) valid[j] = (v >= 0);
-      else valid[j] = (v > 0) || in_window(__ldg(ranges + row * S + s), sn.r_min, sn.r_max);
-      lab[j] = max(v, 0);
-      if (lab[j] > 0) { if (first == INT_MAX) first = s; last = s; }
+      if (s % sh.k == 0) {
+        const int c = s / sh.k;
+        const int p = __ldcg(par + c);  // flattened: the root cell
+        v = p >= 0 ? p + 1 : (((__ldg(vbr + (c >> 5)) >> (c & 31)) & 1u) ? -2 : 0);
+      } else {
+        v = in_window(__ldg(ranges + rb + s), sn.r_min, sn.r_max) ? -2 : 0;
+      }
+      if (node_labels)  // reference segment() output: 1 + rank of the root
+        node_labels[rb + s] = v > 0 ? rank_label(rbf, rpf, sh.Wk, sh.Sk, v - 1) : 0;
     }
+    s_val[s] = v;
+    const uint32_t dm = __ballot_sync(0xffffffffu, v > 0);
+    if ((s & 31) == 0) s_dm[s >> 5] = dm;
+    any |= dm != 0;
   }
-  int prev;
-  Scan(tmp).ExclusiveScan(last, prev, INT_MIN, cub::Max());
+  if (any && (threadIdx.x & 31) == 0) s_any = 1;
   __syncthreads();
-  s_first[threadIdx.x] = first;
-  __syncthreads();
-  int rout;
-  Scan(tmp).ExclusiveScan(s_first[T - 1 - threadIdx.x], rout, INT_MAX, cub::Min());
-  s_next[T - 1 - threadIdx.x] = rout;
-  if (threadIdx.x == T - 1) s_glast = (last != INT_MIN) ? last : prev;
-  __syncthreads();
-  const int next = s_next[threadIdx.x];
-  if (threadIdx.x == 0) s_gfirst = (first != INT_MAX) ? first : next;
-  __syncthreads();
-  const int gfirst = s_gfirst, glast = s_glast;
-  const bool has_donor = (gfirst != INT_MAX);
-  int nxt[ITEMS];
-  {
-    int nd = next;
-#pragma unroll
-    for (int j = ITEMS - 1; j >= 0; --j) {
-      nxt[j] = nd;
-      if (lab[j] > 0) nd = s0 + j;
-    }
-  }
-  int pd = prev;
-  int run_lab = -1, run_len = 0;
+  const bool rany = s_any != 0;
   int32_t* hw = hist + (int64_t)f * K;
-#pragma unroll
-  for (int j = 0; j < ITEMS; ++j) {
-    const int s = s0 + j;
-    if (s >= S) break;
-    int res = lab[j];
-    if (res == 0 && valid[j] && has_donor) {
-      const int left = (pd != INT_MIN) ? pd : glast - S;
-      const int right = (nxt[j] != INT_MAX) ? nxt[j] : gfirst + S;
-      const int dl = s - left, dr = right - s;
-      const int ls = left < 0 ? left + S : left;
-      const int rs = right >= S ? right - S : right;
-      res = max(s_row[dl < dr ? ls : (dr < dl ? rs : min(ls, rs))], 0);
-    }
-    if (lab[j] > 0) pd = s;
-    out[row * S + s] = res;
-    if (res == run_lab) ++run_len;
-    else {
-      if (run_len > 0 && run_lab > 0) atomicAdd(hw + run_lab, run_len);
-      run_lab = res;
-      run_len = 1;
-    }
+  for (int s = threadIdx.x; s < nw * 32; s += T) {
+    const int r = (s < S) ? fill_one(s_val, s_dm, nw, S, s, rany) : 0;
+    if (s < S) out[rb + s] = r;
+    hist_add(hw, r);
   }
-  if (run_len > 0 && run_lab > 0) atomicAdd(hw + run_lab, run_len);
-  (void)i;
 }
-
 
 // ---------------------------------------------------------------- binning
 static constexpr double kTwoPiF = 6.283185307179586;  // == 2.0 * np.pi
@@ -674,23 +676,16 @@ __device__ __forceinline__ bool bin_one(const lseg_sensor& sn, const float* __re
 template <int T>
 __global__ void __launch_bounds__(T) k_bin_rows(lseg_sensor sn, Shape sh, const float* __restrict__ xyz,
                                                 const int32_t* __restrict__ ring, const int64_t* __restrict__ off,
-                                                double* __restrict__ ranges, uint32_t* __restrict__ vbits,
-                                                int32_t* __restrict__ fallback) {
+                                                const int64_t* __restrict__ seg, double* __restrict__ ranges,
+                                                uint32_t* __restrict__ vbits, int32_t* __restrict__ fallback) {
   extern __shared__ unsigned long long s_cell[];
   __shared__ int s_bad;
   const int64_t row = blockIdx.x;
   const int f = (int)(row / sh.R), i = (int)(row - (int64_t)f * sh.R);
   const int S = sh.S;
-  __shared__ int64_t s_lohi[2];
   const int64_t p0 = __ldg(off + f), p1 = __ldg(off + f + 1);
-  const int warp = threadIdx.x >> 5;
-  if (warp < 2) {
-    const int64_t b = warp_lower_bound(ring, p0, p1, i + warp, threadIdx.x & 31);
-    if ((threadIdx.x & 31) == 0) s_lohi[warp] = b;
-  }
+  const int64_t lo = __ldg(seg + f * (sh.R + 1) + i), hi = __ldg(seg + f * (sh.R + 1) + i + 1);
   for (int s = threadIdx.x; s < S; s += T) s_cell[s] = ~0ull;
-  __syncthreads();
-  const int64_t lo = s_lohi[0], hi = s_lohi[1];
   if (threadIdx.x == 0) s_bad = (hi < lo) ? 1 : 0;
   __syncthreads();
   int bad = 0;
@@ -719,6 +714,18 @@ __global__ void __launch_bounds__(T) k_bin_rows(lseg_sensor sn, Shape sh, const 
     const uint32_t b = __ballot_sync(0xffffffffu, v);
     if (lane == 0) vbits[row * sh.Wk + w] = b;
   }
+}
+
+// Ring segment bounds of ring-major input: seg[f][i] = first point of frame f
+// with ring >= i, i = 0..R, one warp per entry (32-ary search).
+__global__ void k_ring_bounds(Shape sh, const int32_t* __restrict__ ring, const int64_t* __restrict__ off,
+                             int64_t* __restrict__ seg) {
+  const int f = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // one warp per bound
+  if (i > sh.R) return;
+  const int64_t b = warp_lower_bound(ring, __ldg(off + f), __ldg(off + f + 1), i, lane);
+  if (lane == 0) seg[(int64_t)f * (sh.R + 1) + i] = b;
 }
 
 // Generic path for frames flagged by k_bin_rows: reset the frame's row / bits.
@@ -760,7 +767,8 @@ void launch_bin_fused(const lseg_sensor& sn, const Shape& sh, const float* xyz, 
   const size_t smem = sizeof(unsigned long long) * sh.S;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_bin_rows<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_bin_rows<256><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, xyz, ring, off, ranges, ws.vbits, ws.fallback);
+  k_ring_bounds<<<dim3((sh.R + 1 + 7) / 8, sh.F), 256, 0, st>>>(sh, ring, off, ws.seg);
+  k_bin_rows<256><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, xyz, ring, off, ws.seg, ranges, ws.vbits, ws.fallback);
   prof_mark("bin_rows", st);
   k_bin_reset<<<sh.F * sh.R, 256, 0, st>>>(sh, ws.fallback, ranges, ws.vbits);
   k_bin_atomic<<<dim3(8, sh.F), 256, 0, st>>>(sn, sh, xyz, ring, off, ws.fallback, ranges, ws.vbits);
@@ -774,112 +782,64 @@ void launch_bin_fused(const lseg_sensor& sn, const Shape& sh, const float* xyz, 
 // segment.py:136-140: otherwise labels stay as they are).
 __global__ void k_survivors(Shape sh, const uint32_t* __restrict__ rbits, const int32_t* __restrict__ hist, int64_t K,
                             int32_t min_size, uint32_t* __restrict__ sbits, int32_t* __restrict__ fscal) {
-  const int64_t nwords = (int64_t)sh.F * sh.R * sh.Wk;
+  const int row = blockIdx.x;  // one CTA per ring row, one warp per word
+  const int f = row / sh.R, i = row - f * sh.R;
   const int lane = threadIdx.x & 31;
-  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nwords;
-       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t row = w / sh.Wk;
-    const int f = (int)(row / sh.R);
-    const uint32_t rb = __ldg(rbits + w);
+  const int32_t* hf = hist + (int64_t)f * K;
+  bool any = false;
+  for (int w = threadIdx.x >> 5; w < sh.Wk; w += blockDim.x >> 5) {
+    const uint32_t rb = __ldg(rbits + (int64_t)row * sh.Wk + w);
     bool surv = false, small = false;
     if ((rb >> lane) & 1u) {
-      const int cell = (int)(row - (int64_t)f * sh.R) * sh.Sk + (int)(w - row * sh.Wk) * 32 + lane;
-      const int cnt = __ldg(hist + (int64_t)f * K + cell + 1);
+      const int cnt = __ldg(hf + i * sh.Sk + w * 32 + lane + 1);
       small = (min_size > 0) && (cnt < min_size);
       surv = !small;
     }
     const uint32_t b = __ballot_sync(0xffffffffu, surv);
-    const uint32_t sm = __ballot_sync(0xffffffffu, small);
-    if (lane == 0) {
-      sbits[w] = b;
-      if (sm) atomicOr(fscal + f * 4, 1);
-    }
+    any |= __any_sync(0xffffffffu, small);
+    if (lane == 0) sbits[(int64_t)row * sh.Wk + w] = b;
   }
+  if (lane == 0 && any) atomicOr(fscal + f * 4, 1);
 }
 
 // Dissolve small segments into the nearest surviving ring donor (reference
 // segment.py:141-154) and write the final compacted ids, one CTA per ring row.
-template <int T, int ITEMS>
+template <int T>
 __global__ void __launch_bounds__(T) k_prune_rows(Shape sh, const int32_t* __restrict__ lab_in,
                                                   int32_t* __restrict__ out, const int32_t* __restrict__ hist,
                                                   int64_t K, int32_t min_size, const int32_t* __restrict__ fscal,
                                                   const uint32_t* __restrict__ rbits, const int32_t* __restrict__ rpre,
                                                   const uint32_t* __restrict__ sbits,
                                                   const int32_t* __restrict__ spre) {
-  using Scan = cub::BlockScan<int, T>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ int s_first[T];
-  __shared__ int s_next[T];
-  __shared__ int s_gfirst, s_glast;
-  extern __shared__ int s_row[];
-  const int64_t row = blockIdx.x;
-  const int f = (int)(row / sh.R);
-  const int S = sh.S;
+  extern __shared__ int s_dynrow[];
+  const int S = sh.S, nw = (S + 31) / 32;
+  int* s_val = s_dynrow;
+  uint32_t* s_dm = reinterpret_cast<uint32_t*>(s_dynrow + nw * 32);
+  __shared__ int s_any;
+  const int row = blockIdx.x;
+  const int f = row / sh.R;
   const bool any_small = fscal[f * 4] != 0;
   const int32_t* hf = hist + (int64_t)f * K;
   const uint32_t* bb = (any_small ? sbits : rbits) + (int64_t)f * sh.R * sh.Wk;
   const int32_t* bp = (any_small ? spre : rpre) + (int64_t)f * sh.R * sh.Wk;
-  const int s0 = threadIdx.x * ITEMS;
-  int lab[ITEMS];
-  bool gone[ITEMS];
-  int last = INT_MIN, first = INT_MAX;
-#pragma unroll
-  for (int j = 0; j < ITEMS; ++j) {
-    const int s = s0 + j;
-    lab[j] = 0;
-    gone[j] = false;
-    if (s < S) {
-      lab[j] = __ldcg(lab_in + row * S + s);
-      gone[j] = any_small && lab[j] > 0 && __ldg(hf + lab[j]) < min_size;
-      if (lab[j] > 0 && !gone[j]) { if (first == INT_MAX) first = s; last = s; }
-      s_row[s] = gone[j] ? 0 : lab[j];  // donor labels only
-    }
+  const int64_t rb = (int64_t)row * S;
+  if (threadIdx.x == 0) s_any = 0;
+  __syncthreads();
+  bool any = false;
+  for (int s = threadIdx.x; s < nw * 32; s += T) {
+    int v = (s < S) ? __ldcg(lab_in + rb + s) : 0;
+    if (any_small && v > 0 && __ldg(hf + v) < min_size) v = -2;  // dissolved: becomes a target
+    s_val[s] = v;
+    const uint32_t dm = __ballot_sync(0xffffffffu, v > 0);
+    if ((s & 31) == 0) s_dm[s >> 5] = dm;
+    any |= dm != 0;
   }
+  if (any && (threadIdx.x & 31) == 0) s_any = 1;
   __syncthreads();
-  int prev;
-  Scan(tmp).ExclusiveScan(last, prev, INT_MIN, cub::Max());
-  __syncthreads();
-  s_first[threadIdx.x] = first;
-  __syncthreads();
-  int rout;
-  Scan(tmp).ExclusiveScan(s_first[T - 1 - threadIdx.x], rout, INT_MAX, cub::Min());
-  s_next[T - 1 - threadIdx.x] = rout;
-  if (threadIdx.x == T - 1) s_glast = (last != INT_MIN) ? last : prev;
-  __syncthreads();
-  const int next = s_next[threadIdx.x];
-  if (threadIdx.x == 0) s_gfirst = (first != INT_MAX) ? first : next;
-  __syncthreads();
-  const int gfirst = s_gfirst, glast = s_glast;
-  const bool has_donor = (gfirst != INT_MAX);
-  int nxt[ITEMS];
-  {
-    int nd = next;
-#pragma unroll
-    for (int j = ITEMS - 1; j >= 0; --j) {
-      nxt[j] = nd;
-      if (lab[j] > 0 && !gone[j]) nd = s0 + j;
-    }
-  }
-  int pd = prev;
-#pragma unroll
-  for (int j = 0; j < ITEMS; ++j) {
-    const int s = s0 + j;
-    if (s >= S) break;
-    int res = lab[j];
-    if (gone[j]) {
-      res = 0;
-      if (has_donor) {
-        const int left = (pd != INT_MIN) ? pd : glast - S;
-        const int right = (nxt[j] != INT_MAX) ? nxt[j] : gfirst + S;
-        const int dl = s - left, dr = right - s;
-        const int ls = left < 0 ? left + S : left;
-        const int rs = right >= S ? right - S : right;
-        res = s_row[dl < dr ? ls : (dr < dl ? rs : min(ls, rs))];
-      }
-    } else if (res > 0) {
-      pd = s;
-    }
-    out[row * S + s] = res > 0 ? rank_label(bb, bp, sh.Wk, sh.Sk, res - 1) : 0;
+  const bool rany = s_any != 0;
+  for (int s = threadIdx.x; s < S; s += T) {
+    const int v = fill_one(s_val, s_dm, nw, S, s, rany);
+    out[rb + s] = v > 0 ? rank_label(bb, bp, sh.Wk, sh.Sk, v - 1) : 0;
   }
 }
 
@@ -887,23 +847,17 @@ void launch_prune_fused(const Shape& sh, const Workspace& ws, int32_t min_size, 
   cudaMemsetAsync(ws.fscal, 0, sizeof(int32_t) * 4 * sh.F, st);
   const int64_t nwords = (int64_t)sh.F * sh.R * sh.Wk;
   const int64_t blocks = (nwords * 32 + 255) / 256;
-  k_survivors<<<(unsigned)(blocks < 148 * 64 ? blocks : 148 * 64), 256, 0, st>>>(sh, ws.rbits, ws.hist, ws.K, min_size,
-                                                                                ws.sbits, ws.fscal);
+  (void)blocks;
+  k_survivors<<<sh.F * sh.R, sh.Wk >= 8 ? 256 : 32 * sh.Wk, 0, st>>>(sh, ws.rbits, ws.hist, ws.K, min_size, ws.sbits,
+                                                                     ws.fscal);
   launch_scan_bits(sh, ws.sbits, ws.spre, ws.fscal_cnt, nullptr, 0, st);
   prof_mark("prune_plan", st);
-  const size_t smem = sizeof(int) * sh.S;
-#define PR(T_, I_)                                                                                            \
-  do {                                                                                                        \
-    if (smem > 48 * 1024)                                                                                     \
-      cudaFuncSetAttribute(k_prune_rows<T_, I_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
-    k_prune_rows<T_, I_><<<sh.F * sh.R, T_, smem, st>>>(sh, ws.lab_tmp, labels, ws.hist, ws.K, min_size,      \
-                                                        ws.fscal, ws.rbits, ws.rpre, ws.sbits, ws.spre);      \
-  } while (0)
-  if (sh.S <= 1024) PR(256, 4);
-  else if (sh.S <= 2048) PR(256, 8);
-  else if (sh.S <= 4096) PR(256, 16);
-  else PR(512, 32);
-#undef PR
+  const int nwr = (sh.S + 31) / 32;
+  const size_t smem = sizeof(int) * (size_t)nwr * 33;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_prune_rows<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_prune_rows<256><<<sh.F * sh.R, 256, smem, st>>>(sh, ws.lab_tmp, labels, ws.hist, ws.K, min_size, ws.fscal, ws.rbits,
+                                                    ws.rpre, ws.sbits, ws.spre);
   prof_mark("prune_apply", st);
 }
 
@@ -926,33 +880,27 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   prof_mark("tile", st);
   k_tile_cc<TILE_R, TILE_C, 128><<<(unsigned)nt, 128, 0, st>>>(sh, ws.masks, ws.parent);
   prof_mark("tile_cc", st);
-  const int64_t nb = ((int64_t)tilesR * sh.Sk + (int64_t)tilesC * sh.R) * sh.F;
-  k_merge<TILE_R, TILE_C><<<(unsigned)((nb + 255) / 256 < 148 * 32 ? (nb + 255) / 256 : 148 * 32), 256, 0, st>>>(
+  const int per = tilesR * sh.Sk + tilesC * sh.R;
+  k_merge<TILE_R, TILE_C><<<dim3((per + 255) / 256, sh.F), 256, 0, st>>>(
       sh, ws.bnorm, thr[0], thr[1], thr[2], ws.parent);
   prof_mark("merge", st);
   {
     const int64_t nwords = (int64_t)sh.F * sh.R * sh.Wk;
     const int64_t blocks = (nwords * 32 + 255) / 256;
-    k_root_flatten<<<(unsigned)(blocks < 148 * 64 ? blocks : 148 * 64), 256, 0, st>>>(sh, ws.parent, ws.rbits,
-                                                                                     ws.hist, ws.K);
+    (void)blocks;
+    const int thr = sh.Wk >= 8 ? 256 : 32 * sh.Wk;
+    k_root_flatten<<<sh.F * sh.R, thr, 0, st>>>(sh, ws.parent, ws.rbits, ws.hist, ws.K);
     prof_mark("root_flatten", st);
     launch_scan_bits(sh, ws.rbits, ws.rpre, n_labels, nullptr, 0, st);
     prof_mark("root_scan", st);
   }
   // labels + backfill -> lab_tmp (+ histogram)
-  const size_t smem = sizeof(int) * sh.S;
-#define LB(T_, I_)                                                                                              \
-  do {                                                                                                          \
-    if (smem > 48 * 1024)                                                                                       \
-      cudaFuncSetAttribute(k_labels_backfill<T_, I_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
-    k_labels_backfill<T_, I_><<<sh.F * sh.R, T_, smem, st>>>(sn, sh, ranges, ws.vbits, ws.parent, ws.rbits,      \
-                                                             ws.rpre, node_labels, ws.lab_tmp, ws.hist, ws.K);  \
-  } while (0)
-  if (sh.S <= 1024) LB(256, 4);
-  else if (sh.S <= 2048) LB(256, 8);
-  else if (sh.S <= 4096) LB(256, 16);
-  else LB(512, 32);
-#undef LB
+  const int nwr = (sh.S + 31) / 32;
+  const size_t smem = sizeof(int) * (size_t)nwr * 33;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_labels_backfill<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_labels_backfill<256><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, ranges, ws.vbits, ws.parent, ws.rbits, ws.rpre,
+                                                         node_labels, ws.lab_tmp, ws.hist, ws.K);
   prof_mark("labels_backfill", st);
 }
 
