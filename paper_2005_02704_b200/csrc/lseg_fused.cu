@@ -381,22 +381,26 @@ __global__ void __launch_bounds__(T) k_tile_cc(Shape sh, const unsigned long lon
     s_par[e] = y * TC + (Z ? 64 - __clzll((long long)Z) : 0);
   }
   __syncthreads();
-  // vertical / diagonal unions, one warp per row pair: edges whose parallel
-  // edge one column to the left already joins the same two runs are dropped
-  // with 64-bit mask arithmetic before any union-find work
-  const int lane = threadIdx.x & 31;
-  for (int y = threadIdx.x >> 5; y + 1 < TRe; y += T / 32) {
-    const unsigned long long Hy = s_m[y * 5], V0 = s_m[y * 5 + 1], V1 = s_m[y * 5 + 2];
-    const unsigned long long Hn = s_m[(y + 1) * 5];
-    const unsigned long long U0 = V0 & ~((Hy << 1) & (Hn << 1) & (V0 << 1));
-    const unsigned long long U1 = V1 & ~((V0 & Hn) | ((Hy << 1) & Hn & (V1 << 1)));
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const int x = lane + 32 * half;
-      const int e = y * TC + x;
-      if ((U0 >> x) & 1ull) lunion(s_par, e, e + TC);
-      if ((U1 >> x) & 1ull) lunion(s_par, e, e + TC + 1);
+  // vertical / diagonal unions: edges whose parallel edge one column to the
+  // left already joins the same two runs are dropped with 64-bit mask
+  // arithmetic (one thread per row pair), the rest are unioned cell-parallel
+  __shared__ unsigned long long s_U[TR * 2];
+  for (int y = threadIdx.x; y < TR; y += T) {
+    unsigned long long U0 = 0, U1 = 0;
+    if (y + 1 < TRe) {
+      const unsigned long long Hy = s_m[y * 5], V0 = s_m[y * 5 + 1], V1 = s_m[y * 5 + 2];
+      const unsigned long long Hn = s_m[(y + 1) * 5];
+      U0 = V0 & ~((Hy << 1) & (Hn << 1) & (V0 << 1));
+      U1 = V1 & ~((V0 & Hn) | ((Hy << 1) & Hn & (V1 << 1)));
     }
+    s_U[2 * y] = U0;
+    s_U[2 * y + 1] = U1;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < NT; e += T) {
+    const int y = e / TC, x = e - y * TC;
+    if ((s_U[2 * y] >> x) & 1ull) lunion(s_par, e, e + TC);
+    if ((s_U[2 * y + 1] >> x) & 1ull) lunion(s_par, e, e + TC + 1);
   }
   for (int y = threadIdx.x; y < TRe; y += T) {  // full-width column wrap (x = S'-1 -> 0)
     const unsigned W = (unsigned)s_m[y * 5 + 4];
@@ -878,7 +882,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
                                                                   thr[2], node_ids, neighbors, n32, nmask, ws.masks,
                                                                   ws.bnorm);
   prof_mark("tile", st);
-  k_tile_cc<TILE_R, TILE_C, 128><<<(unsigned)nt, 128, 0, st>>>(sh, ws.masks, ws.parent);
+  k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent);
   prof_mark("tile_cc", st);
   const int per = tilesR * sh.Sk + tilesC * sh.R;
   k_merge<TILE_R, TILE_C><<<dim3((per + 255) / 256, sh.F), 256, 0, st>>>(
