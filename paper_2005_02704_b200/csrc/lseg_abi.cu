@@ -77,10 +77,11 @@ Workspace carve(const Shape& s, int64_t label_bound, void* base) {
   w.remap = reinterpret_cast<int32_t*>(take((size_t)s.F * K * 4));
   w.fscal = reinterpret_cast<int32_t*>(take((size_t)s.F * 4 * 4));
   w.lab_tmp = reinterpret_cast<int32_t*>(take((size_t)s.F * s.R * s.S * 4));
-  w.bnorm = reinterpret_cast<double*>(take((size_t)s.F * s.cap * 3 * 8));
+  w.bnorm = reinterpret_cast<double*>(
+      take((size_t)s.F * (2 * ((s.R + kTileR - 1) / kTileR) * (size_t)s.Sk + 2 * ((s.Sk + kTileC - 1) / kTileC) * (size_t)s.R) * 3 * 8));
   {
-    const size_t tiles = (size_t)s.F * ((s.R + 15) / 16) * ((s.Sk + 63) / 64);
-    w.masks = reinterpret_cast<unsigned long long*>(take(tiles * 16 * 5 * 8));
+    const size_t tiles = (size_t)s.F * ((s.R + kTileR - 1) / kTileR) * ((s.Sk + kTileC - 1) / kTileC);
+    w.masks = reinterpret_cast<unsigned long long*>(take(tiles * kTileR * 5 * 8));
   }
   w.fallback = reinterpret_cast<int32_t*>(take((size_t)s.F * 4));
   w.seg = reinterpret_cast<int64_t*>(take((size_t)s.F * (s.R + 1) * 8));

@@ -18,8 +18,8 @@
 
 namespace lseg {
 
-static constexpr int TILE_R = 16;
-static constexpr int TILE_C = 64;
+static constexpr int TILE_R = kTileR;
+static constexpr int TILE_C = kTileC;
 static constexpr int TILE_T = 256;
 
 __device__ __forceinline__ int wrapc(int c, int Sk) { return c < 0 ? c + Sk : (c >= Sk ? c - Sk : c); }
@@ -61,6 +61,18 @@ __device__ __forceinline__ bool edge_internal(int r, int c, int s, int Sk) {
   if (tc >= Sk) tc -= Sk;
   return (tr / TR == r / TR) && (tc / TC == c / TC);
 }
+
+// Border-normal store of one frame: for each tile row, its first and last
+// ring rows (all S' columns), then for each tile column its first and last
+// columns (all R rows); 3 doubles per cell, so every write run is contiguous.
+__device__ __forceinline__ int64_t bn_frame(const Shape& sh, int TR, int TC) {
+  return ((int64_t)2 * ((sh.R + TR - 1) / TR) * sh.Sk + (int64_t)2 * ((sh.Sk + TC - 1) / TC) * sh.R) * 3;
+}
+__device__ __forceinline__ int64_t bn_row(const Shape& sh, int slot, int c) { return ((int64_t)slot * sh.Sk + c) * 3; }
+__device__ __forceinline__ int64_t bn_col(const Shape& sh, int TR, int slot, int r) {
+  return ((int64_t)2 * ((sh.R + TR - 1) / TR) * sh.Sk + (int64_t)slot * sh.R + r) * 3;
+}
+__device__ __forceinline__ void bn_put(double* o, double a, double b, double c) { o[0] = a; o[1] = b; o[2] = c; }
 
 // Normal of a node whose 6 slots are all present: the same operation sequence
 // as Fan (pairs (0,1)..(4,5),(5,0) accumulated in order) but straight-line, so
@@ -280,11 +292,13 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       o[2] = has ? (float)s_nz[e] : qn;
     }
     nmask[nbase + id] = has ? 1 : 0;
-    if (has && (y == 0 || y == TRe - 1 || x == 0 || x == TCe - 1)) {
-      double* o = bnorm + (nbase + cell) * 3;
-      o[0] = s_nx[e];
-      o[1] = s_ny[e];
-      o[2] = s_nz[e];
+    if (has) {  // fp64 normals of the tile's border rows / columns for k_merge (coalesced)
+      double* bf = bnorm + (int64_t)f * bn_frame(sh, TR, TC);
+      const int tr = r0 / TR, tc = c0 / TC;
+      if (y == 0) bn_put(bf + bn_row(sh, 2 * tr, cc), s_nx[e], s_ny[e], s_nz[e]);
+      if (y == TRe - 1) bn_put(bf + bn_row(sh, 2 * tr + 1, cc), s_nx[e], s_ny[e], s_nz[e]);
+      if (x == 0) bn_put(bf + bn_col(sh, TR, 2 * tc, rr), s_nx[e], s_ny[e], s_nz[e]);
+      if (x == TCe - 1) bn_put(bf + bn_col(sh, TR, 2 * tc + 1, rr), s_nx[e], s_ny[e], s_nz[e]);
     }
   }
 
@@ -442,7 +456,7 @@ __global__ void k_merge(Shape sh, const double* __restrict__ bnorm, double t0, d
   const int nbc = (sh.Sk + TC - 1) / TC;
   const int per = nbr * sh.Sk + nbc * sh.R;
   int32_t* par = parent + (int64_t)f * sh.cap;
-  const double* bn = bnorm + (int64_t)f * sh.cap * 3;
+  const double* bn = bnorm + (int64_t)f * bn_frame(sh, TR, TC);
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < per; u += gridDim.x * blockDim.x) {
     int r, c;
     if (u < nbr * sh.Sk) {
@@ -457,14 +471,30 @@ __global__ void k_merge(Shape sh, const double* __restrict__ bnorm, double t0, d
     }
     const int p = r * sh.Sk + c;
     if (__ldcg(par + p) < 0) continue;  // no normal
-    const double a[3] = {__ldcg(bn + 3 * p), __ldcg(bn + 3 * p + 1), __ldcg(bn + 3 * p + 2)};
+    const int tr = r / TR, tc = c / TC;
+    const bool last_row = (r == min(tr * TR + TR - 1, sh.R - 1));
+    const bool last_col = (c == min(tc * TC + TC - 1, sh.Sk - 1));
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
       if (r + slot_dr(s) >= sh.R) continue;
       if (edge_internal<TR, TC>(r, c, s, sh.Sk)) continue;
-      const int q = (r + slot_dr(s)) * sh.Sk + wrapc(c + slot_dc(s), sh.Sk);
+      const int rq = r + slot_dr(s), cq = wrapc(c + slot_dc(s), sh.Sk);
+      const int q = rq * sh.Sk + cq;
       if (__ldcg(par + q) < 0) continue;
-      const double b[3] = {__ldcg(bn + 3 * q), __ldcg(bn + 3 * q + 1), __ldcg(bn + 3 * q + 2)};
+      // an edge that crosses a tile-row boundary reads both normals from the
+      // row border store, one that only crosses a column boundary from the
+      // column border store
+      const double *pa, *pb;
+      if (slot_dr(s) == 1 && last_row) {
+        pa = bn + bn_row(sh, 2 * tr + 1, c);
+        pb = bn + bn_row(sh, 2 * (rq / TR), cq);
+      } else {
+        pa = bn + bn_col(sh, TR, 2 * tc + 1, r);
+        pb = bn + bn_col(sh, TR, 2 * (cq / TC), rq);
+      }
+      (void)last_col;
+      const double a[3] = {__ldcg(pa), __ldcg(pa + 1), __ldcg(pa + 2)};
+      const double b[3] = {__ldcg(pb), __ldcg(pb + 1), __ldcg(pb + 2)};
       if (normals_pass(a, b, t0, t1, t2)) uf_union(par, p, q);
     }
   }
