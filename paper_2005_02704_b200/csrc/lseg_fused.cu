@@ -94,10 +94,11 @@ __device__ __forceinline__ bool fan6(const double* vx, const double* vy, const d
     ws = __dadd_rn(ws, w);
   }
   if (!(ws > 0.0)) return false;
-  const double m0 = __ddiv_rn(a0, ws), m1 = __ddiv_rn(a1, ws), m2 = __ddiv_rn(a2, ws);
+  double m0, m1, m2, u0, u1, u2;
+  div3(a0, a1, a2, ws, m0, m1, m2);
   const double mag = norm3(m0, m1, m2);
   if (!(mag >= 1e-12)) return false;
-  double u0 = __ddiv_rn(m0, mag), u1 = __ddiv_rn(m1, mag), u2 = __ddiv_rn(m2, mag);
+  div3(m0, m1, m2, mag, u0, u1, u2);
   const double dot = __dadd_rn(__dadd_rn(__dmul_rn(u0, p.x), __dmul_rn(u2, p.z)), __dmul_rn(u1, p.y));
   if (dot > 0.0) { u0 = -u0; u1 = -u1; u2 = -u2; }
   out[0] = u0; out[1] = u1; out[2] = u2;
@@ -149,21 +150,45 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   const int64_t nbase = (int64_t)f * sh.cap;
   const int tid = threadIdx.x;
 
-  // A. halo positions dir*r (reference product order) and node ids (-1 absent)
-  for (int e = tid; e < GR * GC; e += T) {
-    const int y = e / GC, x = e - y * GC;
-    const int rr = r0 - 1 + y;
-    Vec3 q = {0.0, 0.0, 0.0};
-    int id = -1;
-    if (rr >= 0 && rr < sh.R) {
-      const int cc = wrapc(c0 - 1 + x, sh.Sk);
-      id = id_at(vbf, wpf, sh.Wk, rr, cc);
-      if (id >= 0) q = cell_pos(sn, rr, cc * sh.k, __ldg(rf + (int64_t)rr * sh.S + (int64_t)cc * sh.k));
+  // A. halo positions dir*r (reference product order) and node ids (-1 absent).
+  // All of a thread's loads are issued before any is used (one memory round
+  // trip for the whole halo instead of one per cell).
+  {
+    constexpr int NA = (GR * GC + T - 1) / T;
+    double rv[NA];
+    uint32_t wv[NA];
+    int32_t pv[NA];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) {
+      const int e = tid + j * T;
+      const int y = e / GC, x = e - y * GC;
+      const int rr = r0 - 1 + y;
+      rv[j] = 0.0;
+      wv[j] = 0u;
+      pv[j] = 0;
+      if (e < GR * GC && rr >= 0 && rr < sh.R) {
+        const int cc = wrapc(c0 - 1 + x, sh.Sk);
+        rv[j] = __ldg(rf + (int64_t)rr * sh.S + (int64_t)cc * sh.k);
+        wv[j] = __ldg(vbf + (int64_t)rr * sh.Wk + (cc >> 5));
+        pv[j] = __ldg(wpf + (int64_t)rr * sh.Wk + (cc >> 5));
+      }
     }
-    s_px[e] = q.x;
-    s_py[e] = q.y;
-    s_pz[e] = q.z;
-    s_id[e] = id;
+#pragma unroll
+    for (int j = 0; j < NA; ++j) {
+      const int e = tid + j * T;
+      if (e >= GR * GC) break;
+      const int y = e / GC, x = e - y * GC;
+      const int rr = r0 - 1 + y;
+      const int cc = wrapc(c0 - 1 + x, sh.Sk);
+      const uint32_t bit = 1u << (cc & 31);
+      const int id = (wv[j] & bit) ? pv[j] + __popc(wv[j] & (bit - 1u)) : -1;
+      Vec3 q = {0.0, 0.0, 0.0};
+      if (id >= 0) q = cell_pos(sn, rr, cc * sh.k, rv[j]);
+      s_px[e] = q.x;
+      s_py[e] = q.y;
+      s_pz[e] = q.z;
+      s_id[e] = id;
+    }
   }
   __syncthreads();
 
