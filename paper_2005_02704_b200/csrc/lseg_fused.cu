@@ -18,6 +18,9 @@
 
 namespace lseg {
 
+#ifndef LSEG_CC_SV
+#define LSEG_CC_SV 1
+#endif
 static constexpr int TILE_R = kTileR;
 static constexpr int TILE_C = kTileC;
 static constexpr int TILE_T = 256;
@@ -436,6 +439,66 @@ __global__ void __launch_bounds__(T) k_tile_cc(Shape sh, const unsigned long lon
     s_U[2 * y + 1] = U1;
   }
   __syncthreads();
+#if LSEG_CC_SV
+  // Run-level label propagation (Shiloach-Vishkin style, every thread doing
+  // the same work -- the serial union-find chains of divergent lanes were the
+  // cost here): labels live at run starts, L[start] <= start.  Hook: for every
+  // kept vertical edge link the larger of the two current labels to the
+  // smaller (atomicMin); shortcut: L[a] = L[L[a]].  Repeat until nothing
+  // changes; then every run's label is its component's minimum run start.
+  constexpr int NJ = (NT + T - 1) / T;
+  int ea[2 * NJ + 2], eb[2 * NJ + 2];
+  int ne = 0;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int e = threadIdx.x + j * T;
+    const int y = e / TC, x = e - y * TC;
+    if (e < NT) {
+      const unsigned long long Zs = ~s_m[y * 5] & ((1ull << x) - 1ull);
+      const int a = y * TC + (Zs ? 64 - __clzll((long long)Zs) : 0);
+      if ((s_U[2 * y] >> x) & 1ull) {
+        const int t = e + TC;
+        const unsigned long long Zt = ~s_m[(y + 1) * 5] & ((1ull << x) - 1ull);
+        ea[ne] = a; eb[ne] = (y + 1) * TC + (Zt ? 64 - __clzll((long long)Zt) : 0); ++ne;
+        (void)t;
+      }
+      if ((s_U[2 * y + 1] >> x) & 1ull) {
+        const int xt = x + 1;
+        const unsigned long long Zt = ~s_m[(y + 1) * 5] & ((1ull << xt) - 1ull);
+        ea[ne] = a; eb[ne] = (y + 1) * TC + (Zt ? 64 - __clzll((long long)Zt) : 0); ++ne;
+      }
+    }
+  }
+  if (threadIdx.x < TRe) {  // full-width column wrap (x = S'-1 -> 0)
+    const int y = threadIdx.x;
+    const unsigned W = (unsigned)s_m[y * 5 + 4];
+    const int x = TCe - 1;
+    const unsigned long long Zs = ~s_m[y * 5] & ((1ull << x) - 1ull);
+    const int a = y * TC + (Zs ? 64 - __clzll((long long)Zs) : 0);
+    if (W & 1u) { ea[ne] = a; eb[ne] = y * TC; ++ne; }
+    if (W & 2u) { ea[ne] = a; eb[ne] = (y + 1) * TC; ++ne; }
+  }
+  while (true) {
+    int changed = 0;
+    for (int k = 0; k < ne; ++k) {
+      const int la = s_par[ea[k]], lb = s_par[eb[k]];
+      if (la != lb) {
+        const int hi = max(la, lb), lo = min(la, lb);
+        changed |= atomicMin(s_par + hi, lo) > lo;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int e = threadIdx.x + j * T;
+      if (e >= NT) break;
+      const int l = s_par[e];
+      const int ll = s_par[l];
+      if (ll != l) { s_par[e] = ll; changed = 1; }
+    }
+    if (!__syncthreads_or(changed)) break;
+  }
+#else
   for (int e = threadIdx.x; e < NT; e += T) {
     const int y = e / TC, x = e - y * TC;
     if ((s_U[2 * y] >> x) & 1ull) lunion(s_par, e, e + TC);
@@ -454,6 +517,7 @@ __global__ void __launch_bounds__(T) k_tile_cc(Shape sh, const unsigned long lon
     if (x == 0 || !((H >> (x - 1)) & 1ull)) s_par[e] = lfind(s_par, e);
   }
   __syncthreads();
+#endif
   // ... and give every labelled cell its run start's root
   const int64_t nbase = (int64_t)f * sh.cap;
   for (int e = threadIdx.x; e < NT; e += T) {
