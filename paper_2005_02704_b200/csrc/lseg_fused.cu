@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(T) k_tile_cc(Shape sh, const unsigned long lon
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) {
+    for (int j = 0; j < NJ; ++j) {  // shortcut
       const int e = threadIdx.x + j * T;
       if (e >= NT) break;
       const int l = s_par[e];
@@ -768,9 +768,7 @@ __device__ __forceinline__ int64_t warp_lower_bound(const int32_t* __restrict__ 
 // float) inputs decides it whenever phi*S/2pi is clearly away from a
 // half-integer (its error is < 1e-5 rad, far inside the guard), otherwise the
 // fp64 formula runs -- the result is the fp64 formula's either way.
-__device__ __forceinline__ bool bin_one(const lseg_sensor& sn, const float* __restrict__ xyz, int64_t p, double& r,
-                                        int& step) {
-  const float xf = __ldg(xyz + 3 * p), yf = __ldg(xyz + 3 * p + 1), zf = __ldg(xyz + 3 * p + 2);
+__device__ __forceinline__ bool bin_xyz(const lseg_sensor& sn, float xf, float yf, float zf, double& r, int& step) {
   const double x = (double)xf, y = (double)yf, z = (double)zf;
   r = __dsqrt_rn(__dadd_rn(__dadd_rn(x * x, y * y), z * z));
   if (!in_window(r, sn.r_min, sn.r_max)) return false;
@@ -788,6 +786,11 @@ __device__ __forceinline__ bool bin_one(const lseg_sensor& sn, const float* __re
   if (phi < 0.0) phi = __dadd_rn(phi, kTwoPiF);
   step = (int)rint(__ddiv_rn(__dmul_rn(phi, (double)sn.steps), kTwoPiF)) % sn.steps;
   return true;
+}
+
+__device__ __forceinline__ bool bin_one(const lseg_sensor& sn, const float* __restrict__ xyz, int64_t p, double& r,
+                                        int& step) {
+  return bin_xyz(sn, __ldg(xyz + 3 * p), __ldg(xyz + 3 * p + 1), __ldg(xyz + 3 * p + 2), r, step);
 }
 
 // Fast path for ring-major input (the sensor's firing order): one CTA per
@@ -812,11 +815,32 @@ __global__ void __launch_bounds__(T) k_bin_rows(lseg_sensor sn, Shape sh, const 
   if (threadIdx.x == 0) s_bad = (hi < lo) ? 1 : 0;
   __syncthreads();
   int bad = 0;
-  for (int64_t p = lo + threadIdx.x; p < hi; p += T) {
-    if (__ldg(ring + p) != i) { bad = 1; continue; }
-    double r;
-    int st;
-    if (bin_one(sn, xyz, p, r, st)) atomicMin(s_cell + st, (unsigned long long)__double_as_longlong(r));
+  // batches of B points per thread: all loads of a batch are issued first
+  constexpr int B = 4;
+  for (int64_t base = lo; base < hi; base += (int64_t)T * B) {
+    float px[B], py[B], pz[B];
+    int pr[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const int64_t p = base + threadIdx.x + (int64_t)j * T;
+      pr[j] = i;
+      px[j] = py[j] = pz[j] = 0.0f;
+      if (p < hi) {
+        pr[j] = __ldg(ring + p);
+        px[j] = __ldg(xyz + 3 * p);
+        py[j] = __ldg(xyz + 3 * p + 1);
+        pz[j] = __ldg(xyz + 3 * p + 2);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const int64_t p = base + threadIdx.x + (int64_t)j * T;
+      if (p >= hi) break;
+      if (pr[j] != i) { bad = 1; continue; }
+      double r;
+      int st;
+      if (bin_xyz(sn, px[j], py[j], pz[j], r, st)) atomicMin(s_cell + st, (unsigned long long)__double_as_longlong(r));
+    }
   }
   if (i == 0)
     for (int64_t p = p0 + threadIdx.x; p < lo; p += T) bad |= (__ldg(ring + p) >= 0) ? 1 : 0;
