@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--also-interval", type=int, default=5,
+                    help="also time this interval (reference default 5); 0 disables")
     ap.add_argument("--seed", type=int, default=2005)
     return ap.parse_args()
 
@@ -116,7 +118,8 @@ def stage_bytes(P, C, Ck, N):
         "frame_scan": Ck / 4,                          # valid bits in, word prefix out
         # ranges + valid bits in; node ids, neighbours, normals, mask, parent,
         # fp64 border normals (first/last row and column of 16 x 64 tiles) out
-        "tile": 8 * Ck + Ck / 4 + 4 * Ck + 24 * N + 12 * N + N + 4 * Ck + 24 * bnd,
+        "tile": 8 * Ck + Ck / 4 + 4 * Ck + 24 * N + 12 * N + N + 24 * bnd + 5 * Ck / 8,
+        "tile_cc": 5 * Ck / 8 + 4 * Ck,                # pass masks in, tile-local parents out
         "merge": 4 * bnd + 24 * bnd,
         "root_flatten": 4 * Ck + Ck / 8,
         "root_scan": Ck / 4,
@@ -127,6 +130,20 @@ def stage_bytes(P, C, Ck, N):
         "bin_fill": 8 * C, "bin": 24 * P, "valid_bits": 8 * Ck, "mesh": 4 * Ck + 24 * N,
         "normals": 12 * Ck + 24 * N + 37 * N,
     }
+
+
+def committed_traffic(kernel, frames, interval):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/traffic.json), if it was taken on this workload."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            t = json.load(fh)
+    except (OSError, ValueError):
+        return None
+    e = t.get(kernel)
+    if e and e.get("frames") == frames and e.get("interval") == interval:
+        return e["dram_bytes_per_launch"]
+    return None
 
 
 def pipeline_bytes(P, C, N):
@@ -209,7 +226,8 @@ def main():
     if a.impl == "reference":
         return run_reference(a, shape)
 
-    ws, rank, local = dist_env()
+    from paper_2005_02704_b200 import dist as D
+    ws, rank, local = D.env()
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -252,15 +270,13 @@ def main():
     stages = _lib.profile_end()
     clk = clocks.stop()
     barrier()
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    tot_pts = torch.tensor([float(P)], dtype=torch.float64, device=dev)
-    if ws > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(tot_pts)
-    ms = float(t.item())
+    # the run's only collective: totals + max elapsed over ranks
+    run = D.reduce_run(P * a.steps, F * a.steps, int(bp.n_labels.sum().item()) * a.steps, e0.elapsed_time(e1),
+                       device=dev)
+    ms = run["elapsed_ms"]
     ms_step = ms / a.steps
-    value = float(tot_pts.item()) * a.steps / (ms / 1e3)
+    tot_pts = torch.tensor([run["points"] / a.steps], dtype=torch.float64)
+    value = run["points"] / (ms / 1e3)
 
     # ---- roofline of the dominant kernel + of the whole pipeline
     peak, peak_kind = measured_peak_hbm()
@@ -271,13 +287,33 @@ def main():
         dom_ms = stages[dom][0] / stages[dom][1]
         ach = sb.get(dom, 0) / (dom_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "peak_kind": peak_kind,
-                "unit": "GB/s", "frac": ach / peak, "traffic": None, "ms_per_launch": dom_ms,
+                "unit": "GB/s", "frac": ach / peak, "traffic": committed_traffic(dom, F, a.interval),
+                "ms_per_launch": dom_ms,
                 "share_of_step": stages[dom][0] / a.steps / ms_step,
                 "alg_bytes_per_launch": sb.get(dom, 0)}
     pb = pipeline_bytes(P, C, N)
     pipe_roof = {"alg_bytes_per_step": pb, "achieved_gbs": pb / (ms_step / 1e3) / 1e9,
                  "frac": pb / (ms_step / 1e3) / 1e9 / peak, "frac_of_8tbs": pb / (ms_step / 1e3) / 1e9 / 8000.0}
     stage_ms = {k: round(v[0] / v[1], 4) for k, v in stages.items()}
+
+    # ---- the same batch at the reference's default interval (pipeline.py:25)
+    other = None
+    if a.also_interval and a.also_interval != a.interval:
+        bp2 = L.BatchPipeline(cfg, a.also_interval, frames=F, device=dev)
+        for _ in range(3):
+            bp2.run(xyz, ring, off)
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(a.steps):
+            bp2.run(xyz, ring, off)
+        e1.record(st)
+        torch.cuda.synchronize()
+        r2 = D.reduce_run(P * a.steps, F * a.steps, 0, e0.elapsed_time(e1), device=dev)
+        other = {"interval": a.also_interval, "value": r2["points"] / (r2["elapsed_ms"] / 1e3), "unit": UNIT,
+                 "ms_per_step": r2["elapsed_ms"] / a.steps,
+                 "frames_per_s": r2["frames"] / (r2["elapsed_ms"] / 1e3)}
+        del bp2
 
     # ---- e2e through the public API (StreamingPipeline): pinned host points in,
     # pinned host label grid out, H2D / kernels / D2H overlapped in chunks
@@ -322,8 +358,10 @@ def main():
                                        f"(BASELINE configs[3])", "interval": a.interval, "frames_per_rank": F,
                            "points_per_rank": P, "nodes_per_rank": N, "parallelism": f"frame-shard x{ws}",
                            "l2": "inputs (>1 GB per step) exceed the 126 MB L2; no flush needed"},
-                "frames_per_s": F * ws * a.steps / (ms / 1e3),
+                "frames_per_s": run["frames"] / (ms / 1e3),
+                "segments_per_frame": run["segments"] / max(run["frames"], 1),
                 "roofline": roof, "pipeline_roofline": pipe_roof, "stage_ms": stage_ms,
+                "at_interval_%d" % a.also_interval if other else "at_other_interval": other,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk}
         print(json.dumps(line), flush=True)
     if ws > 1:
