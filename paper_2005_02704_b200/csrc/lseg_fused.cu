@@ -626,8 +626,9 @@ __global__ void k_root_flatten(Shape sh, int32_t* __restrict__ parent, uint32_t*
 }
 
 // 1 + rank of root cell rc among the set bits of (bits, pre) = its label.
-__device__ __forceinline__ int rank_label(const uint32_t* bf, const int32_t* pf, int Wk, int Sk, int rc) {
-  const int rr = rc / Sk, cc = rc - rr * Sk;
+__device__ __forceinline__ int rank_label(const uint32_t* bf, const int32_t* pf, int Wk, int Sk, int rc,
+                                          double inv_Sk) {
+  const int rr = fdiv(rc, Sk, inv_Sk), cc = rc - rr * Sk;
   return 1 + node_id_at(bf + (int64_t)rr * Wk, pf + (int64_t)rr * Wk, cc);
 }
 
@@ -711,15 +712,15 @@ __global__ void __launch_bounds__(T) k_labels_backfill(lseg_sensor sn, Shape sh,
   for (int s = threadIdx.x; s < nw * 32; s += T) {  // classify: donor label / target -2 / passive 0
     int v = 0;
     if (s < S) {
-      if (s % sh.k == 0) {
-        const int c = s / sh.k;
+      const int c = (sh.k == 1) ? s : s / sh.k;
+      if (sh.k == 1 || c * sh.k == s) {
         const int p = __ldcg(par + c);  // flattened: the root cell
         v = p >= 0 ? p + 1 : (((__ldg(vbr + (c >> 5)) >> (c & 31)) & 1u) ? -2 : 0);
       } else {
         v = in_window(__ldg(ranges + rb + s), sn.r_min, sn.r_max) ? -2 : 0;
       }
       if (node_labels)  // reference segment() output: 1 + rank of the root
-        node_labels[rb + s] = v > 0 ? rank_label(rbf, rpf, sh.Wk, sh.Sk, v - 1) : 0;
+        node_labels[rb + s] = v > 0 ? rank_label(rbf, rpf, sh.Wk, sh.Sk, v - 1, sh.inv_Sk) : 0;
     }
     s_val[s] = v;
     const uint32_t dm = __ballot_sync(0xffffffffu, v > 0);
@@ -986,7 +987,7 @@ __global__ void __launch_bounds__(T) k_prune_rows(Shape sh, const int32_t* __res
   const bool rany = s_any != 0;
   for (int s = threadIdx.x; s < S; s += T) {
     const int v = fill_one(s_val, s_dm, nw, S, s, rany);
-    out[rb + s] = v > 0 ? rank_label(bb, bp, sh.Wk, sh.Sk, v - 1) : 0;
+    out[rb + s] = v > 0 ? rank_label(bb, bp, sh.Wk, sh.Sk, v - 1, sh.inv_Sk) : 0;
   }
 }
 
