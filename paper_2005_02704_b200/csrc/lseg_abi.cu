@@ -86,6 +86,7 @@ Workspace carve(const Shape& s, int64_t label_bound, void* base) {
   w.fallback = reinterpret_cast<int32_t*>(take((size_t)s.F * 4));
   w.seg = reinterpret_cast<int64_t*>(take((size_t)s.F * (s.R + 1) * 8));
   w.rbits = reinterpret_cast<uint32_t*>(take(words * 4));
+  w.lroots = reinterpret_cast<uint32_t*>(take(words * 4));
   w.rpre = reinterpret_cast<int32_t*>(take(words * 4));
   w.sbits = reinterpret_cast<uint32_t*>(take(words * 4));
   w.spre = reinterpret_cast<int32_t*>(take(words * 4));

@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
 // parent[cell] = minimum cell of its tile-local component (-1 without normal).
 template <int TR, int TC, int T>
 __global__ void __launch_bounds__(T) k_tile_cc(Shape sh, const unsigned long long* __restrict__ masks,
-                                               int32_t* __restrict__ parent) {
+                                               int32_t* __restrict__ parent, uint32_t* __restrict__ lroots) {
   constexpr int NT = TR * TC;
   __shared__ int s_par[NT];
   __shared__ unsigned long long s_m[TR * 5];
@@ -518,18 +518,24 @@ __global__ void __launch_bounds__(T) k_tile_cc(Shape sh, const unsigned long lon
   }
   __syncthreads();
 #endif
-  // ... and give every labelled cell its run start's root
+  // ... and give every labelled cell its run start's root; tile-local roots
+  // (cells that are their own root) also get a bit in `lroots`, so the global
+  // flatten only has to chase those
   const int64_t nbase = (int64_t)f * sh.cap;
-  for (int e = threadIdx.x; e < NT; e += T) {
+  for (int e = threadIdx.x; e < NT; e += T) {  // NT is a multiple of T: whole warps
     const int y = e / TC, x = e - y * TC;
-    if (y >= TRe || x >= TCe) continue;
+    const bool in = (y < TRe && x < TCe);
     int pc = -1;
-    if ((s_m[y * 5 + 3] >> x) & 1ull) {
+    if (in && ((s_m[y * 5 + 3] >> x) & 1ull)) {
       const unsigned long long Z = ~s_m[y * 5] & ((1ull << x) - 1ull);
       const int lr = s_par[y * TC + (Z ? 64 - __clzll((long long)Z) : 0)];
       pc = (r0 + lr / TC) * sh.Sk + c0 + lr % TC;
     }
-    parent[nbase + (int64_t)(r0 + y) * sh.Sk + c0 + x] = pc;
+    const int cell = (r0 + y) * sh.Sk + c0 + x;
+    if (in) parent[nbase + cell] = pc;
+    const uint32_t b = __ballot_sync(0xffffffffu, in && pc == cell);
+    const int word = (c0 + x) >> 5;
+    if ((threadIdx.x & 31) == 0 && y < TRe && word < sh.Wk) lroots[((int64_t)f * sh.R + r0 + y) * sh.Wk + word] = b;
   }
 }
 
@@ -599,26 +605,28 @@ __device__ __forceinline__ int root_of(const int32_t* __restrict__ par, int x) {
 // After k_merge: point every labelled cell straight at its final root, mark
 // roots with a bit per kept cell (k_frame_scan over these gives label ranks)
 // and zero each root's histogram slot (labels are root cell + 1 until pruning).
-__global__ void k_root_flatten(Shape sh, int32_t* __restrict__ parent, uint32_t* __restrict__ rbits,
-                               int32_t* __restrict__ hist, int64_t K) {
-  // one CTA per ring row (f, i), one warp per 32-cell word: no 64-bit division
+__global__ void k_root_flatten(Shape sh, int32_t* __restrict__ parent, const uint32_t* __restrict__ lroots,
+                               uint32_t* __restrict__ rbits, int32_t* __restrict__ hist, int64_t K) {
+  // after k_merge: point every tile-local root straight at its final root
+  // (the only cells whose chains can be long; every other cell points at its
+  // tile-local root, so its final root is parent[parent[cell]]), mark final
+  // roots and zero their histogram slots.  One CTA per ring row, one warp per
+  // 32-cell word, no 64-bit division.
   const int row = blockIdx.x;
   const int f = row / sh.R, i = row - f * sh.R;
   const int lane = threadIdx.x & 31;
   int32_t* par = parent + (int64_t)f * sh.cap;
   int32_t* hf = hist + (int64_t)f * K;
   for (int w = threadIdx.x >> 5; w < sh.Wk; w += blockDim.x >> 5) {
-    const int c = w * 32 + lane;
+    const uint32_t lr = __ldg(lroots + (int64_t)row * sh.Wk + w);
     bool root = false;
-    if (c < sh.Sk) {
-      const int cell = i * sh.Sk + c;
+    if ((lr >> lane) & 1u) {
+      const int cell = i * sh.Sk + w * 32 + lane;
       const int p = __ldcg(par + cell);
-      if (p >= 0) {
-        const int r = root_of(par, p);
-        if (r != p) par[cell] = r;
-        root = (r == cell);
-        if (root) hf[cell + 1] = 0;
-      }
+      const int r = root_of(par, p);
+      if (r != p) par[cell] = r;
+      root = (r == cell);
+      if (root) hf[cell + 1] = 0;
     }
     const uint32_t b = __ballot_sync(0xffffffffu, root);
     if (lane == 0) rbits[(int64_t)row * sh.Wk + w] = b;
@@ -702,7 +710,8 @@ __global__ void __launch_bounds__(T) k_labels_backfill(lseg_sensor sn, Shape sh,
   const int row = blockIdx.x;
   const int f = row / sh.R, i = row - f * sh.R;
   const uint32_t* vbr = vbits + (int64_t)row * sh.Wk;
-  const int32_t* par = parent + (int64_t)f * sh.cap + (int64_t)i * sh.Sk;
+  const int32_t* parf = parent + (int64_t)f * sh.cap;
+  const int32_t* par = parf + (int64_t)i * sh.Sk;
   const uint32_t* rbf = rbits + (int64_t)f * sh.R * sh.Wk;
   const int32_t* rpf = rpre + (int64_t)f * sh.R * sh.Wk;
   const int64_t rb = (int64_t)row * S;
@@ -714,8 +723,8 @@ __global__ void __launch_bounds__(T) k_labels_backfill(lseg_sensor sn, Shape sh,
     if (s < S) {
       const int c = (sh.k == 1) ? s : s / sh.k;
       if (sh.k == 1 || c * sh.k == s) {
-        const int p = __ldcg(par + c);  // flattened: the root cell
-        v = p >= 0 ? p + 1 : (((__ldg(vbr + (c >> 5)) >> (c & 31)) & 1u) ? -2 : 0);
+        const int p = __ldcg(par + c);  // tile-local root, whose parent is the final root
+        v = p >= 0 ? __ldcg(parf + p) + 1 : (((__ldg(vbr + (c >> 5)) >> (c & 31)) & 1u) ? -2 : 0);
       } else {
         v = in_window(__ldg(ranges + rb + s), sn.r_min, sn.r_max) ? -2 : 0;
       }
@@ -1026,7 +1035,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
                                                                   thr[2], node_ids, neighbors, n32, nmask, ws.masks,
                                                                   ws.bnorm);
   prof_mark("tile", st);
-  k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent);
+  k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
   prof_mark("tile_cc", st);
   const int per = tilesR * sh.Sk + tilesC * sh.R;
   k_merge<TILE_R, TILE_C><<<dim3((per + 255) / 256, sh.F), 256, 0, st>>>(
@@ -1037,7 +1046,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
     const int64_t blocks = (nwords * 32 + 255) / 256;
     (void)blocks;
     const int thr = sh.Wk >= 8 ? 256 : 32 * sh.Wk;
-    k_root_flatten<<<sh.F * sh.R, thr, 0, st>>>(sh, ws.parent, ws.rbits, ws.hist, ws.K);
+    k_root_flatten<<<sh.F * sh.R, thr, 0, st>>>(sh, ws.parent, ws.lroots, ws.rbits, ws.hist, ws.K);
     prof_mark("root_flatten", st);
     launch_scan_bits(sh, ws.rbits, ws.rpre, n_labels, nullptr, 0, st);
     prof_mark("root_scan", st);
