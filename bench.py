@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--also-interval", type=int, default=5,
                     help="also time this interval (reference default 5); 0 disables")
     ap.add_argument("--seed", type=int, default=2005)
+    ap.add_argument("--streams", type=int, default=1, help="frame chunks on concurrent streams")
     return ap.parse_args()
 
 
@@ -241,7 +242,7 @@ def main():
     P = int(xyz.shape[0])
     cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
                          r_max=shape.r_max)
-    bp = L.BatchPipeline(cfg, a.interval, frames=F, device=dev)
+    bp = L.BatchPipeline(cfg, a.interval, frames=F, device=dev, streams=a.streams)
     st = torch.cuda.current_stream()
 
     def barrier():

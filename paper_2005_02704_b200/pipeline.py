@@ -102,7 +102,7 @@ class BatchPipeline:
     """
 
     def __init__(self, config: SensorConfig, interval: int, segmenter: SegmenterConfig | None = None,
-                 frames: int = 1, device=None, keep_node_labels: bool = False):
+                 frames: int = 1, device=None, keep_node_labels: bool = False, streams: int = 1):
         self.L = _lib.lib()
         self.config = config
         self.interval = int(interval)
@@ -125,17 +125,37 @@ class BatchPipeline:
         self.labels = torch.empty((F, R, S), dtype=torch.int32, device=dev)
         self.n_nodes = torch.empty(F, dtype=torch.int32, device=dev)
         self.n_labels = torch.empty(F, dtype=torch.int32, device=dev)
-        self.ws_bytes = _lib.workspace_bytes(F, R, S, interval)
-        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        # frames are independent: with streams > 1 the batch is cut into that
+        # many chunks, each enqueued on its own stream (own workspace) so the
+        # latency-bound kernels of one chunk overlap those of another
+        self.nstreams = max(1, min(int(streams), F))
+        per = -(-F // self.nstreams)
+        self.chunks = [(f0, min(F, f0 + per)) for f0 in range(0, F, per)]
+        self.ws_bytes = _lib.workspace_bytes(per, R, S, interval)
+        self.ws = [torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev) for _ in self.chunks]
+        self.streams = [torch.cuda.Stream(dev) for _ in self.chunks] if len(self.chunks) > 1 else None
+
+    def _call(self, f0, f1, ws, xyz, ring, offsets):
+        P = int(xyz.shape[0])
+        sl = lambda t: None if t is None else t[f0:f1]
+        _lib.check(self.L.lseg_run_pipeline(
+            self.sn, f1 - f0, self.interval, self.thr, int(self.seg.min_segment_size), _lib.ptr(xyz),
+            _lib.ptr(ring), _lib.ptr(offsets[f0:]), P, _lib.ptr(sl(self.ranges)), _lib.ptr(sl(self.node_ids)),
+            _lib.ptr(sl(self.neighbors)), _lib.ptr(sl(self.normals)), _lib.ptr(sl(self.nmask)),
+            _lib.ptr(sl(self.node_labels)), _lib.ptr(sl(self.labels)), _lib.ptr(sl(self.n_nodes)),
+            _lib.ptr(sl(self.n_labels)), _lib.ptr(ws), self.ws_bytes, _lib.stream_ptr()))
 
     def run(self, xyz, ring, offsets):
-        P = int(xyz.shape[0])
-        _lib.check(self.L.lseg_run_pipeline(
-            self.sn, self.frames, self.interval, self.thr, int(self.seg.min_segment_size), _lib.ptr(xyz),
-            _lib.ptr(ring), _lib.ptr(offsets), P, _lib.ptr(self.ranges), _lib.ptr(self.node_ids),
-            _lib.ptr(self.neighbors), _lib.ptr(self.normals), _lib.ptr(self.nmask), _lib.ptr(self.node_labels),
-            _lib.ptr(self.labels), _lib.ptr(self.n_nodes), _lib.ptr(self.n_labels), _lib.ptr(self.ws),
-            self.ws_bytes, _lib.stream_ptr()))
+        if self.streams is None:
+            self._call(0, self.frames, self.ws[0], xyz, ring, offsets)
+            return self.labels
+        cur = torch.cuda.current_stream(self.device)
+        for (f0, f1), ws, st in zip(self.chunks, self.ws, self.streams):
+            st.wait_stream(cur)
+            with torch.cuda.stream(st):
+                self._call(f0, f1, ws, xyz, ring, offsets)
+        for st in self.streams:
+            cur.wait_stream(st)
         return self.labels
 
     def frame(self, f: int) -> dict:
