@@ -718,23 +718,46 @@ __global__ void __launch_bounds__(T) k_labels_backfill(lseg_sensor sn, Shape sh,
   if (threadIdx.x == 0) s_any = 0;
   __syncthreads();
   bool any = false;
-  for (int s = threadIdx.x; s < nw * 32; s += T) {  // classify: donor label / target -2 / passive 0
-    int v = 0;
-    if (s < S) {
-      const int c = (sh.k == 1) ? s : s / sh.k;
-      if (sh.k == 1 || c * sh.k == s) {
-        const int p = __ldcg(par + c);  // tile-local root, whose parent is the final root
-        v = p >= 0 ? __ldcg(parf + p) + 1 : (((__ldg(vbr + (c >> 5)) >> (c & 31)) & 1u) ? -2 : 0);
-      } else {
-        v = in_window(__ldg(ranges + rb + s), sn.r_min, sn.r_max) ? -2 : 0;
+  // classify: donor label / target -2 / passive 0.  Chunks of PF cells per
+  // thread with all loads of a chunk issued before they are used (the two
+  // dependent parent loads would otherwise serialise per cell).
+  constexpr int PF = 8;
+  for (int s0 = 0; s0 < nw * 32; s0 += T * PF) {
+    int pv[PF], lv[PF];
+#pragma unroll
+    for (int j = 0; j < PF; ++j) {
+      const int s = s0 + threadIdx.x + j * T;
+      pv[j] = -1;
+      if (s < S) {
+        const int c = (sh.k == 1) ? s : s / sh.k;
+        if (sh.k == 1 || c * sh.k == s) pv[j] = __ldcg(par + c);  // tile-local root
+        else pv[j] = -2;
       }
-      if (node_labels)  // reference segment() output: 1 + rank of the root
-        node_labels[rb + s] = v > 0 ? rank_label(rbf, rpf, sh.Wk, sh.Sk, v - 1, sh.inv_Sk) : 0;
     }
-    s_val[s] = v;
-    const uint32_t dm = __ballot_sync(0xffffffffu, v > 0);
-    if ((s & 31) == 0) s_dm[s >> 5] = dm;
-    any |= dm != 0;
+#pragma unroll
+    for (int j = 0; j < PF; ++j) lv[j] = pv[j] >= 0 ? __ldcg(parf + pv[j]) : 0;  // its parent: the final root
+#pragma unroll
+    for (int j = 0; j < PF; ++j) {
+      const int s = s0 + threadIdx.x + j * T;
+      if (s >= nw * 32) break;
+      int v = 0;
+      if (s < S) {
+        if (pv[j] >= 0) {
+          v = lv[j] + 1;
+        } else if (pv[j] == -1) {  // kept cell without a normal: valid?
+          const int c = (sh.k == 1) ? s : s / sh.k;
+          v = ((__ldg(vbr + (c >> 5)) >> (c & 31)) & 1u) ? -2 : 0;
+        } else {
+          v = in_window(__ldg(ranges + rb + s), sn.r_min, sn.r_max) ? -2 : 0;
+        }
+        if (node_labels)  // reference segment() output: 1 + rank of the root
+          node_labels[rb + s] = v > 0 ? rank_label(rbf, rpf, sh.Wk, sh.Sk, v - 1, sh.inv_Sk) : 0;
+      }
+      s_val[s] = v;
+      const uint32_t dm = __ballot_sync(0xffffffffu, v > 0);
+      if ((s & 31) == 0) s_dm[s >> 5] = dm;
+      any |= dm != 0;
+    }
   }
   if (any && (threadIdx.x & 31) == 0) s_any = 1;
   __syncthreads();
@@ -983,13 +1006,26 @@ __global__ void __launch_bounds__(T) k_prune_rows(Shape sh, const int32_t* __res
   if (threadIdx.x == 0) s_any = 0;
   __syncthreads();
   bool any = false;
-  for (int s = threadIdx.x; s < nw * 32; s += T) {
-    int v = (s < S) ? __ldcg(lab_in + rb + s) : 0;
-    if (any_small && v > 0 && __ldg(hf + v) < min_size) v = -2;  // dissolved: becomes a target
-    s_val[s] = v;
-    const uint32_t dm = __ballot_sync(0xffffffffu, v > 0);
-    if ((s & 31) == 0) s_dm[s >> 5] = dm;
-    any |= dm != 0;
+  constexpr int PF = 8;
+  for (int s0 = 0; s0 < nw * 32; s0 += T * PF) {
+    int lv[PF], hv[PF];
+#pragma unroll
+    for (int j = 0; j < PF; ++j) {
+      const int s = s0 + threadIdx.x + j * T;
+      lv[j] = (s < S) ? __ldcg(lab_in + rb + s) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < PF; ++j) hv[j] = (any_small && lv[j] > 0) ? __ldg(hf + lv[j]) : INT_MAX;
+#pragma unroll
+    for (int j = 0; j < PF; ++j) {
+      const int s = s0 + threadIdx.x + j * T;
+      if (s >= nw * 32) break;
+      const int v = (hv[j] < min_size) ? -2 : lv[j];  // dissolved: becomes a target
+      s_val[s] = v;
+      const uint32_t dm = __ballot_sync(0xffffffffu, v > 0);
+      if ((s & 31) == 0) s_dm[s >> 5] = dm;
+      any |= dm != 0;
+    }
   }
   if (any && (threadIdx.x & 31) == 0) s_any = 1;
   __syncthreads();
