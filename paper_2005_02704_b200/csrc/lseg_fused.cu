@@ -18,6 +18,9 @@
 
 namespace lseg {
 
+#ifndef LSEG_FAN6
+#define LSEG_FAN6 0
+#endif
 #ifndef LSEG_CC_SV
 #define LSEG_CC_SV 1
 #endif
@@ -255,7 +258,9 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     const int y = e / TC, x = e - y * TC;
     const int g = (y + 1) * GC + (x + 1);
     const Vec3 p = {s_px[g], s_py[g], s_pz[g]};
-    double vx[6], vy[6], vz[6], nv[3];
+    double nv[3];
+#if LSEG_FAN6
+    double vx[6], vy[6], vz[6];
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       const int gq = g + slot_dr(s) * GC + slot_dc(s);
@@ -263,7 +268,19 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       vy[s] = __dsub_rn(s_py[gq], p.y);
       vz[s] = __dsub_rn(s_pz[gq], p.z);
     }
-    if (fan6(vx, vy, vz, p, nv)) {
+    const bool okn = fan6(vx, vy, vz, p, nv);
+#else
+    // streamed: only first / previous / current vectors live (fewer registers,
+    // more resident warps)
+    Fan fan;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const int gq = g + slot_dr(s) * GC + slot_dc(s);
+      fan.add(__dsub_rn(s_px[gq], p.x), __dsub_rn(s_py[gq], p.y), __dsub_rn(s_pz[gq], p.z));
+    }
+    const bool okn = fan.finish(p, nv);
+#endif
+    if (okn) {
       s_nx[e] = nv[0];
       s_ny[e] = nv[1];
       s_nz[e] = nv[2];
