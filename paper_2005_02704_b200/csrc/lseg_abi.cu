@@ -130,6 +130,9 @@ extern "C" {
 
 const char* lseg_last_error(void) { return g_last_error.c_str(); }
 
+// Debug hook: summed per-phase SM cycles of k_tile (builds with LSEG_PHASES=1).
+void lseg_debug_tile_phases(double* out8) { lseg::debug_phases(out8); }
+
 const char* lseg_version(void) { return "lidarseg_b200 0.1.0 sm_100a"; }
 
 int lseg_profile_begin(void) {

@@ -18,6 +18,12 @@
 
 namespace lseg {
 
+#ifndef LSEG_PHASES
+#define LSEG_PHASES 0
+#endif
+#if LSEG_PHASES
+__device__ unsigned long long g_ph[8];
+#endif
 #ifndef LSEG_FAN6
 #define LSEG_FAN6 0
 #endif
@@ -130,6 +136,19 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
                                                 double* __restrict__ bnorm) {
   constexpr int GR = TR + 2, GC = TC + 2;  // halo rows r0-1..r0+TR, cols c0-1..c0+TC
   constexpr int NT = TR * TC;
+#if LSEG_PHASES
+  long long ph_prev = clock64();
+#define PH_MARK(i)                                                   \
+  do {                                                               \
+    if (threadIdx.x == 0) {                                          \
+      const long long now = clock64();                               \
+      atomicAdd(&g_ph[i], (unsigned long long)(now - ph_prev));       \
+      ph_prev = now;                                                 \
+    }                                                                \
+  } while (0)
+#else
+#define PH_MARK(i) do {} while (0)
+#endif
   // dynamic shared memory (58 KB > the 48 KB static limit), see tile_smem_bytes()
   extern __shared__ __align__(16) unsigned char s_dyn[];
   double* s_px = reinterpret_cast<double*>(s_dyn);
@@ -197,6 +216,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     }
   }
   __syncthreads();
+  PH_MARK(1);
 
   // B. fp64 normals (reference normals.py:94-145 operation order).  Nodes are
   // first sorted into two work lists so that no warp runs both code paths:
@@ -252,6 +272,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     if (tid == 0) { s_cnt[2 * (T / 32)] = ta; s_cnt[2 * (T / 32) + 1] = tb; }
   }
   __syncthreads();
+  PH_MARK(2);
   const int nfan6 = s_cnt[2 * (T / 32)], ngen = s_cnt[2 * (T / 32) + 1];
   for (int i = tid; i < nfan6; i += T) {
     const int e = s_list[i];
@@ -309,6 +330,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     }
   }
   __syncthreads();
+  PH_MARK(3);
 
   // C. per-node outputs
   for (int e = tid; e < NT; e += T) {
@@ -347,6 +369,10 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     }
   }
 
+#if LSEG_PHASES
+  __syncthreads();
+#endif
+  PH_MARK(4);
   // D. homogeneity test on the tile's internal forward edges, one warp per
   // tile row, as 64-bit masks per row (bit x = column x):
   //   H  (y,x)->(y,x+1)   V0 (y,x)->(y+1,x)   V1 (y,x)->(y+1,x+1)
@@ -409,6 +435,10 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       mrow[y * 5 + 4] = W;
     }
   }
+#if LSEG_PHASES
+  __syncthreads();
+#endif
+  PH_MARK(5);
 }
 
 // Tile-local connected components from k_tile's masks (one small CTA per
@@ -1072,6 +1102,17 @@ void launch_prune_fused(const Shape& sh, const Workspace& ws, int32_t min_size, 
 }
 
 // ---------------------------------------------------------------- launchers
+void debug_phases(double* out) {
+#if LSEG_PHASES
+  unsigned long long h[8];
+  cudaMemcpyFromSymbol(h, g_ph, sizeof(h));
+  for (int i = 0; i < 8; ++i) out[i] = (double)h[i];
+  unsigned long long z[8] = {0};
+  cudaMemcpyToSymbol(g_ph, z, sizeof(z));
+#else
+  for (int i = 0; i < 8; ++i) out[i] = -1.0;
+#endif
+}
 void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace& ws, const double* ranges,
                         const double* thr, int32_t* node_ids, int32_t* neighbors, float* n32, uint8_t* nmask,
                         int32_t* n_nodes, int32_t* n_labels, int32_t* node_labels, cudaStream_t st) {

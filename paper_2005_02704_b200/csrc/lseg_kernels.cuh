@@ -34,4 +34,5 @@ void launch_frame_scan(const Shape& sh, const Workspace& ws, int32_t* n_nodes, c
 void launch_scan_bits(const Shape& sh, const uint32_t* bits, int32_t* pre, int32_t* counts, int32_t* hist, int64_t K,
                       cudaStream_t st);
 void launch_prune_fused(const Shape& sh, const Workspace& ws, int32_t min_size, int32_t* labels, cudaStream_t st);
+void debug_phases(double* out);
 }  // namespace lseg
