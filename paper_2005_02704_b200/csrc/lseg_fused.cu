@@ -848,16 +848,32 @@ __device__ __forceinline__ int64_t warp_lower_bound(const int32_t* __restrict__ 
 // float) inputs decides it whenever phi*S/2pi is clearly away from a
 // half-integer (its error is < 1e-5 rad, far inside the guard), otherwise the
 // fp64 formula runs -- the result is the fp64 formula's either way.
+// atan2 from one reciprocal and a degree-9 odd minimax polynomial for atan on
+// [0, 1] (Abramowitz & Stegun 4.4.49, |error| <= 1e-5 rad) plus octant
+// reduction; float rounding adds < 2e-7 rad.  Only used to pick the azimuth
+// step away from half-step boundaries (see the guard in bin_xyz).
+__device__ __forceinline__ float fast_atan2(float y, float x) {
+  const float ax = fabsf(x), ay = fabsf(y);
+  const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+  const float a = mx > 0.0f ? __fdividef(mn, mx) : 0.0f;
+  const float s = a * a;
+  float r = fmaf(fmaf(fmaf(fmaf(0.0208351f, s, -0.0851330f), s, 0.1801410f), s, -0.3302995f), s, 0.9998660f) * a;
+  if (ay > ax) r = 1.57079637f - r;
+  if (x < 0.0f) r = 3.14159274f - r;
+  return y < 0.0f ? -r : r;
+}
+
 __device__ __forceinline__ bool bin_xyz(const lseg_sensor& sn, float xf, float yf, float zf, double& r, int& step) {
   const double x = (double)xf, y = (double)yf, z = (double)zf;
   r = __dsqrt_rn(__dadd_rn(__dadd_rn(x * x, y * y), z * z));
   if (!in_window(r, sn.r_min, sn.r_max)) return false;
   const float scale = (float)sn.steps * 0.15915494309189535f;  // S / (2 pi)
-  float ph = atan2f(yf, xf);
+  float ph = fast_atan2(yf, xf);  // |error| <= 1.2e-5 rad
   if (ph < 0.0f) ph += 6.283185307179586f;
   const float t = ph * scale;
   const float fr = t - floorf(t);
-  if (fabsf(fr - 0.5f) > 1e-3f + 2e-5f * scale) {
+  // guard: 2x the angle error in step units + float rounding of t
+  if (fabsf(fr - 0.5f) > 1e-3f + 2.6e-5f * scale) {
     int st = (int)rintf(t);
     step = st >= sn.steps ? st - sn.steps : st;
     return true;
