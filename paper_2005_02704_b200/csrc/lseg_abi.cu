@@ -85,6 +85,7 @@ Workspace carve(const Shape& s, int64_t label_bound, void* base) {
   }
   w.fallback = reinterpret_cast<int32_t*>(take((size_t)s.F * 4));
   w.seg = reinterpret_cast<int64_t*>(take((size_t)s.F * (s.R + 1) * 8));
+  w.fbits = reinterpret_cast<uint32_t*>(take((size_t)s.F * s.R * ((s.S + 31) / 32) * 4));
   w.rbits = reinterpret_cast<uint32_t*>(take(words * 4));
   w.lroots = reinterpret_cast<uint32_t*>(take(words * 4));
   w.rpre = reinterpret_cast<int32_t*>(take(words * 4));
@@ -314,14 +315,15 @@ int lseg_run_pipeline(const lseg_sensor* sensor, int32_t frames, int32_t interva
     return fail(LSEG_EINVAL, "NULL buffer");
   cudaStream_t st = (cudaStream_t)stream;
   prof_mark(nullptr, st);
-  if (sensor->steps <= 8192) {
+  const bool fused_bin = sensor->steps <= 8192;
+  if (fused_bin) {
     launch_bin_fused(*sensor, sh, xyz, ring, frame_offsets, ws, ranges, n_nodes, st);
   } else {
     launch_bin(*sensor, frames, xyz, ring, frame_offsets, total_points, ranges, nullptr, st);
     launch_valid_scan(*sensor, sh, ranges, ws, n_nodes, st);
   }
   launch_fused_graph(*sensor, sh, ws, ranges, thresholds, node_ids, neighbors, normals32, nmask, n_nodes, n_labels,
-                     node_labels, st);
+                     node_labels, fused_bin, st);
   launch_prune_fused(sh, ws, min_segment_size, labels, st);
   return check_launch("run_pipeline");
 }

@@ -744,6 +744,7 @@ __device__ __forceinline__ void hist_add(int32_t* hw, int lab) {
 template <int T>
 __global__ void __launch_bounds__(T) k_labels_backfill(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
                                                        const uint32_t* __restrict__ vbits,
+                                                       const uint32_t* __restrict__ fbits,
                                                        const int32_t* __restrict__ parent,
                                                        const uint32_t* __restrict__ rbits,
                                                        const int32_t* __restrict__ rpre,
@@ -757,6 +758,7 @@ __global__ void __launch_bounds__(T) k_labels_backfill(lseg_sensor sn, Shape sh,
   const int row = blockIdx.x;
   const int f = row / sh.R, i = row - f * sh.R;
   const uint32_t* vbr = vbits + (int64_t)row * sh.Wk;
+  const uint32_t* fbr = fbits ? fbits + (int64_t)row * ((S + 31) / 32) : nullptr;
   const int32_t* parf = parent + (int64_t)f * sh.cap;
   const int32_t* par = parf + (int64_t)i * sh.Sk;
   const uint32_t* rbf = rbits + (int64_t)f * sh.R * sh.Wk;
@@ -776,7 +778,7 @@ __global__ void __launch_bounds__(T) k_labels_backfill(lseg_sensor sn, Shape sh,
       const int s = s0 + threadIdx.x + j * T;
       pv[j] = -1;
       if (s < S) {
-        const int c = (sh.k == 1) ? s : s / sh.k;
+        const int c = (sh.k == 1) ? s : fdiv(s, sh.k, sh.inv_k);
         if (sh.k == 1 || c * sh.k == s) pv[j] = __ldcg(par + c);  // tile-local root
         else pv[j] = -2;
       }
@@ -792,10 +794,11 @@ __global__ void __launch_bounds__(T) k_labels_backfill(lseg_sensor sn, Shape sh,
         if (pv[j] >= 0) {
           v = lv[j] + 1;
         } else if (pv[j] == -1) {  // kept cell without a normal: valid?
-          const int c = (sh.k == 1) ? s : s / sh.k;
+          const int c = (sh.k == 1) ? s : fdiv(s, sh.k, sh.inv_k);
           v = ((__ldg(vbr + (c >> 5)) >> (c & 31)) & 1u) ? -2 : 0;
-        } else {
-          v = in_window(__ldg(ranges + rb + s), sn.r_min, sn.r_max) ? -2 : 0;
+        } else {  // not a kept cell: valid full-resolution cell? (bits from k_bin_rows)
+          v = fbr ? (((__ldg(fbr + (s >> 5)) >> (s & 31)) & 1u) ? -2 : 0)
+                  : (in_window(__ldg(ranges + rb + s), sn.r_min, sn.r_max) ? -2 : 0);
         }
         if (node_labels)  // reference segment() output: 1 + rank of the root
           node_labels[rb + s] = v > 0 ? rank_label(rbf, rpf, sh.Wk, sh.Sk, v - 1, sh.inv_Sk) : 0;
@@ -899,7 +902,8 @@ template <int T>
 __global__ void __launch_bounds__(T) k_bin_rows(lseg_sensor sn, Shape sh, const float* __restrict__ xyz,
                                                 const int32_t* __restrict__ ring, const int64_t* __restrict__ off,
                                                 const int64_t* __restrict__ seg, double* __restrict__ ranges,
-                                                uint32_t* __restrict__ vbits, int32_t* __restrict__ fallback) {
+                                                uint32_t* __restrict__ vbits, uint32_t* __restrict__ fbits,
+                                                int32_t* __restrict__ fallback) {
   extern __shared__ unsigned long long s_cell[];
   __shared__ int s_bad;
   const int64_t row = blockIdx.x;
@@ -957,6 +961,15 @@ __global__ void __launch_bounds__(T) k_bin_rows(lseg_sensor sn, Shape sh, const 
     const uint32_t b = __ballot_sync(0xffffffffu, v);
     if (lane == 0) vbits[row * sh.Wk + w] = b;
   }
+  if (fbits && sh.k > 1) {  // full-resolution valid bits (the backfill's target test)
+    const int Wf = (S + 31) / 32;
+    for (int w = threadIdx.x >> 5; w < Wf; w += T / 32) {
+      const int c = w * 32 + lane;
+      const bool v = (c < S) && in_window(__longlong_as_double((long long)s_cell[c]), sn.r_min, sn.r_max);
+      const uint32_t b = __ballot_sync(0xffffffffu, v);
+      if (lane == 0) fbits[row * Wf + w] = b;
+    }
+  }
 }
 
 // Ring segment bounds of ring-major input: seg[f][i] = first point of frame f
@@ -973,19 +986,21 @@ __global__ void k_ring_bounds(Shape sh, const int32_t* __restrict__ ring, const 
 
 // Generic path for frames flagged by k_bin_rows: reset the frame's row / bits.
 __global__ void k_bin_reset(Shape sh, const int32_t* __restrict__ fallback, double* __restrict__ ranges,
-                            uint32_t* __restrict__ vbits) {
+                            uint32_t* __restrict__ vbits, uint32_t* __restrict__ fbits) {
   const int64_t row = blockIdx.x;
   const int f = (int)(row / sh.R);
   if (!__ldg(fallback + f)) return;
   for (int s = threadIdx.x; s < sh.S; s += blockDim.x)
     ranges[row * sh.S + s] = __longlong_as_double(~0ll);
   for (int w = threadIdx.x; w < sh.Wk; w += blockDim.x) vbits[row * sh.Wk + w] = 0u;
+  const int Wf = (sh.S + 31) / 32;
+  for (int w = threadIdx.x; w < Wf; w += blockDim.x) fbits[row * Wf + w] = 0u;
 }
 
 // Generic path: global 64-bit atomicMin per point + atomicOr of the kept bit.
 __global__ void k_bin_atomic(lseg_sensor sn, Shape sh, const float* __restrict__ xyz, const int32_t* __restrict__ ring,
                              const int64_t* __restrict__ off, const int32_t* __restrict__ fallback,
-                             double* __restrict__ ranges, uint32_t* __restrict__ vbits) {
+                             double* __restrict__ ranges, uint32_t* __restrict__ vbits, uint32_t* __restrict__ fbits) {
   const int f = blockIdx.y;
   if (!__ldg(fallback + f)) return;
   const int64_t p0 = __ldg(off + f), p1 = __ldg(off + f + 1);
@@ -1001,6 +1016,7 @@ __global__ void k_bin_atomic(lseg_sensor sn, Shape sh, const float* __restrict__
       const int c = st / sh.k;
       atomicOr(vbits + row * sh.Wk + (c >> 5), 1u << (c & 31));
     }
+    atomicOr(fbits + row * ((sh.S + 31) / 32) + (st >> 5), 1u << (st & 31));
   }
 }
 
@@ -1011,10 +1027,11 @@ void launch_bin_fused(const lseg_sensor& sn, const Shape& sh, const float* xyz, 
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_bin_rows<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_ring_bounds<<<dim3((sh.R + 1 + 7) / 8, sh.F), 256, 0, st>>>(sh, ring, off, ws.seg);
-  k_bin_rows<256><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, xyz, ring, off, ws.seg, ranges, ws.vbits, ws.fallback);
+  k_bin_rows<256><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, xyz, ring, off, ws.seg, ranges, ws.vbits, ws.fbits,
+                                                 ws.fallback);
   prof_mark("bin_rows", st);
-  k_bin_reset<<<sh.F * sh.R, 256, 0, st>>>(sh, ws.fallback, ranges, ws.vbits);
-  k_bin_atomic<<<dim3(8, sh.F), 256, 0, st>>>(sn, sh, xyz, ring, off, ws.fallback, ranges, ws.vbits);
+  k_bin_reset<<<sh.F * sh.R, 256, 0, st>>>(sh, ws.fallback, ranges, ws.vbits, ws.fbits);
+  k_bin_atomic<<<dim3(8, sh.F), 256, 0, st>>>(sn, sh, xyz, ring, off, ws.fallback, ranges, ws.vbits, ws.fbits);
   prof_mark("bin_fallback", st);
   launch_frame_scan(sh, ws, n_nodes, st);
 }
@@ -1131,7 +1148,8 @@ void debug_phases(double* out) {
 }
 void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace& ws, const double* ranges,
                         const double* thr, int32_t* node_ids, int32_t* neighbors, float* n32, uint8_t* nmask,
-                        int32_t* n_nodes, int32_t* n_labels, int32_t* node_labels, cudaStream_t st) {
+                        int32_t* n_nodes, int32_t* n_labels, int32_t* node_labels, bool fbits_valid,
+                        cudaStream_t st) {
   const int tilesC = (sh.Sk + TILE_C - 1) / TILE_C, tilesR = (sh.R + TILE_R - 1) / TILE_R;
   const int64_t nt = (int64_t)sh.F * tilesR * tilesC;
   const size_t tsmem = (size_t)(3 * (TILE_R + 2) * (TILE_C + 2) + 3 * TILE_R * TILE_C) * 8 +
@@ -1164,9 +1182,10 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   // labels + backfill -> lab_tmp (+ histogram)
   const int nwr = (sh.S + 31) / 32;
   const size_t smem = sizeof(int) * (size_t)nwr * 33;
+  const uint32_t* fb = (sh.k > 1 && fbits_valid) ? ws.fbits : nullptr;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_labels_backfill<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_labels_backfill<256><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, ranges, ws.vbits, ws.parent, ws.rbits, ws.rpre,
+  k_labels_backfill<256><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits, ws.rpre,
                                                          node_labels, ws.lab_tmp, ws.hist, ws.K);
   prof_mark("labels_backfill", st);
 }

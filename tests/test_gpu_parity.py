@@ -183,3 +183,23 @@ def test_unsorted_points_take_generic_binning(L):
     torch.cuda.synchronize()
     assert torch.equal(got, want)
     assert torch.equal(torch.nan_to_num(bp.ranges, nan=-1.0), torch.nan_to_num(want_r, nan=-1.0))
+
+
+def test_unsorted_points_k5(L, oracle):
+    """Generic binning path at k = 5 (full-resolution valid bits come from the
+    atomic path), checked against the oracle."""
+    from paper_2005_02704_b200 import synth
+    shape = synth.CONFIGS["vlp16"]
+    xyz, ring, off = synth.make_batch(shape, frames=1, seed=8, device="cuda")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1)
+    perm = torch.randperm(xyz.shape[0], device="cuda", generator=g)
+    xs, rs = xyz[perm].contiguous(), ring[perm].contiguous()
+    cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
+                         r_max=shape.r_max)
+    bp = L.BatchPipeline(cfg, 5, frames=1)
+    bp.run(xs, rs, off)
+    torch.cuda.synchronize()
+    want = oracle.run_from_points(xyz.cpu().numpy(), ring.cpu().numpy(), shape.elevations, shape.steps, 5,
+                                  shape.r_min, shape.r_max)
+    np.testing.assert_array_equal(bp.frame(0)["labels"], want["labels"])
