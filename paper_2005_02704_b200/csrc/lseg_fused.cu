@@ -24,6 +24,9 @@ namespace lseg {
 #if LSEG_PHASES
 __device__ unsigned long long g_ph[8];
 #endif
+#ifndef LSEG_FUSE_CC
+#define LSEG_FUSE_CC 0
+#endif
 #ifndef LSEG_FAN6
 #define LSEG_FAN6 0
 #endif
@@ -117,6 +120,11 @@ __device__ __forceinline__ bool fan6(const double* vx, const double* vy, const d
   return true;
 }
 
+template <int TR, int TC, int T>
+__device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int c0, int TRe, int TCe,
+                                             const unsigned long long* s_m, int* s_par, int32_t* __restrict__ parent,
+                                             uint32_t* __restrict__ lroots);
+
 // One CTA per (frame, TR x TC tile of kept cells).
 //   A  ranges + node ids of the tile and a 1-cell halo into shared memory
 //   B  fp64 normals of the tile's nodes (shared memory)
@@ -133,7 +141,8 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
                                                 double t0, double t1, double t2, int32_t* __restrict__ node_ids,
                                                 int32_t* __restrict__ neighbors, float* __restrict__ n32,
                                                 uint8_t* __restrict__ nmask, unsigned long long* __restrict__ masks,
-                                                double* __restrict__ bnorm) {
+                                                double* __restrict__ bnorm, int32_t* __restrict__ parent,
+                                                uint32_t* __restrict__ lroots) {
   constexpr int GR = TR + 2, GC = TC + 2;  // halo rows r0-1..r0+TR, cols c0-1..c0+TC
   constexpr int NT = TR * TC;
 #if LSEG_PHASES
@@ -383,6 +392,10 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   const int lane = tid & 31;
   const bool full_width = (c0 == 0 && TCe == sh.Sk);
   unsigned long long* mrow = masks + (((int64_t)f * tilesR + r0 / TR) * tilesC + c0 / TC) * (TR * 5);
+#if LSEG_FUSE_CC
+  __shared__ unsigned long long s_mk[TR * 5];
+  (void)mrow;
+#endif
   for (int y = tid >> 5; y < TR; y += T / 32) {
     unsigned long long H = 0, V0 = 0, V1 = 0, HS = 0;
     bool w0 = false, w1 = false;
@@ -428,13 +441,27 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     }
     const unsigned W = (__ballot_sync(0xffffffffu, w0) ? 1u : 0u) | (__ballot_sync(0xffffffffu, w1) ? 2u : 0u);
     if (lane == 0) {
+#if LSEG_FUSE_CC
+      s_mk[y * 5 + 0] = H;
+      s_mk[y * 5 + 1] = V0;
+      s_mk[y * 5 + 2] = V1;
+      s_mk[y * 5 + 3] = HS;
+      s_mk[y * 5 + 4] = W;
+#else
       mrow[y * 5 + 0] = H;
       mrow[y * 5 + 1] = V0;
       mrow[y * 5 + 2] = V1;
       mrow[y * 5 + 3] = HS;
       mrow[y * 5 + 4] = W;
+#endif
     }
   }
+#if LSEG_FUSE_CC
+  __syncthreads();
+  // positions are dead after the normals: their shared memory holds the
+  // union-find array of the tile-local components
+  tile_cc_body<TR, TC, T>(sh, f, r0, c0, TRe, TCe, s_mk, reinterpret_cast<int*>(s_px), parent, lroots);
+#endif
 #if LSEG_PHASES
   __syncthreads();
 #endif
@@ -447,22 +474,13 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
 // union-find -- skipping an edge when the parallel edge one column to the left
 // already joins the same two runs -- and each labelled cell gets
 // parent[cell] = minimum cell of its tile-local component (-1 without normal).
+// Tile-local connected components from the pass masks in shared memory (the
+// body of k_tile_cc, also run inside k_tile when the two are fused).
 template <int TR, int TC, int T>
-__global__ void __launch_bounds__(T) k_tile_cc(Shape sh, const unsigned long long* __restrict__ masks,
-                                               int32_t* __restrict__ parent, uint32_t* __restrict__ lroots) {
+__device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int c0, int TRe, int TCe,
+                                             const unsigned long long* s_m, int* s_par, int32_t* __restrict__ parent,
+                                             uint32_t* __restrict__ lroots) {
   constexpr int NT = TR * TC;
-  __shared__ int s_par[NT];
-  __shared__ unsigned long long s_m[TR * 5];
-  const int tilesC = (sh.Sk + TC - 1) / TC;
-  const int tilesR = (sh.R + TR - 1) / TR;
-  const int64_t b = blockIdx.x;
-  const int f = (int)(b / ((int64_t)tilesR * tilesC));
-  const int rem = (int)(b - (int64_t)f * tilesR * tilesC);
-  const int r0 = (rem / tilesC) * TR, c0 = (rem % tilesC) * TC;
-  const int TRe = min(TR, sh.R - r0), TCe = min(TC, sh.Sk - c0);
-  const unsigned long long* mrow = masks + b * (TR * 5);
-  for (int j = threadIdx.x; j < TR * 5; j += T) s_m[j] = __ldg(mrow + j);
-  __syncthreads();
   // run starts: parent of every cell = first cell of its horizontal run
   for (int e = threadIdx.x; e < NT; e += T) {
     const int y = e / TC, x = e - y * TC;
@@ -584,6 +602,24 @@ __global__ void __launch_bounds__(T) k_tile_cc(Shape sh, const unsigned long lon
     const int word = (c0 + x) >> 5;
     if ((threadIdx.x & 31) == 0 && y < TRe && word < sh.Wk) lroots[((int64_t)f * sh.R + r0 + y) * sh.Wk + word] = b;
   }
+}
+
+template <int TR, int TC, int T>
+__global__ void __launch_bounds__(T) k_tile_cc(Shape sh, const unsigned long long* __restrict__ masks,
+                                               int32_t* __restrict__ parent, uint32_t* __restrict__ lroots) {
+  __shared__ int s_par[TR * TC];
+  __shared__ unsigned long long s_m[TR * 5];
+  const int tilesC = (sh.Sk + TC - 1) / TC;
+  const int tilesR = (sh.R + TR - 1) / TR;
+  const int64_t b = blockIdx.x;
+  const int f = (int)(b / ((int64_t)tilesR * tilesC));
+  const int rem = (int)(b - (int64_t)f * tilesR * tilesC);
+  const int r0 = (rem / tilesC) * TR, c0 = (rem % tilesC) * TC;
+  const int TRe = min(TR, sh.R - r0), TCe = min(TC, sh.Sk - c0);
+  const unsigned long long* mrow = masks + b * (TR * 5);
+  for (int j = threadIdx.x; j < TR * 5; j += T) s_m[j] = __ldg(mrow + j);
+  __syncthreads();
+  tile_cc_body<TR, TC, T>(sh, f, r0, c0, TRe, TCe, s_m, s_par, parent, lroots);
 }
 
 // Global union over the forward edges that leave a tile.  Threads enumerate
@@ -1161,10 +1197,12 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   }
   k_tile<TILE_R, TILE_C, TILE_T><<<(unsigned)nt, TILE_T, tsmem, st>>>(sn, sh, ranges, ws.vbits, ws.wpre, thr[0], thr[1],
                                                                   thr[2], node_ids, neighbors, n32, nmask, ws.masks,
-                                                                  ws.bnorm);
+                                                                  ws.bnorm, ws.parent, ws.lroots);
   prof_mark("tile", st);
+#if !LSEG_FUSE_CC
   k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
   prof_mark("tile_cc", st);
+#endif
   const int per = tilesR * sh.Sk + tilesC * sh.R;
   k_merge<TILE_R, TILE_C><<<dim3((per + 255) / 256, sh.F), 256, 0, st>>>(
       sh, ws.bnorm, thr[0], thr[1], thr[2], ws.parent);
