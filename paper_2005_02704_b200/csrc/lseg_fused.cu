@@ -27,6 +27,10 @@ __device__ unsigned long long g_ph[8];
 #ifndef LSEG_FUSE_CC
 #define LSEG_FUSE_CC 0
 #endif
+#ifndef LSEG_UNR
+#define LSEG_UNR 1
+#endif
+static constexpr int kUnrollNormals = LSEG_UNR;
 #ifndef LSEG_FAN6
 #define LSEG_FAN6 0
 #endif
@@ -283,6 +287,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   __syncthreads();
   PH_MARK(2);
   const int nfan6 = s_cnt[2 * (T / 32)], ngen = s_cnt[2 * (T / 32) + 1];
+#pragma unroll kUnrollNormals
   for (int i = tid; i < nfan6; i += T) {
     const int e = s_list[i];
     const int y = e / TC, x = e - y * TC;
