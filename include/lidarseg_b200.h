@@ -142,6 +142,27 @@ int lseg_run_pipeline(const lseg_sensor* sensor, int32_t frames, int32_t interva
                       uint8_t* nmask, int32_t* node_labels, int32_t* labels, int32_t* n_nodes,
                       int32_t* n_labels, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- edge-based evaluation (reference evaluate.py:40-94).
+ * Label grids (F,R,S) i32, 0 = unlabelled.  Scratch sized by
+ * lseg_eval_workspace_bytes. */
+size_t lseg_eval_workspace_bytes(int32_t frames, int32_t rings, int32_t steps);
+
+/* Replaces the counting inside edge_prf (evaluate.py:73-94): per frame
+ * counts[f] = {n_pred_edges, n_truth_edges, pred edges within the Chebyshev
+ * radius of a truth edge, truth edges within the radius of a pred edge}. */
+int lseg_edge_counts(int32_t frames, int32_t rings, int32_t steps, const int32_t* pred,
+                     const int32_t* truth, int32_t radius, int32_t* counts, void* workspace,
+                     size_t workspace_bytes, void* stream);
+
+/* Replaces extract_edges (evaluate.py:40-55): edges (F,R,S) u8. */
+int lseg_extract_edges(int32_t frames, int32_t rings, int32_t steps, const int32_t* labels,
+                       uint8_t* edges, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Replaces dilate_chebyshev (evaluate.py:58-70): out (F,R,S) u8. */
+int lseg_dilate_chebyshev(int32_t frames, int32_t rings, int32_t steps, const uint8_t* mask,
+                          int32_t radius, uint8_t* out, void* workspace, size_t workspace_bytes,
+                          void* stream);
+
 #ifdef __cplusplus
 }
 #endif

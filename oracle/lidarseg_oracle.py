@@ -362,3 +362,53 @@ def run_from_points(xyz, ring, elevations, steps, interval, r_min, r_max,
     out["ranges"] = ranges
     out["cell"] = cell
     return out
+
+
+# ---------------------------------------------------------------- evaluation
+def extract_edges(labels):
+    """Reference evaluate.py:40-55: labelled cells with a differently labelled
+    (nonzero) 4-neighbour; azimuth wraps, rings clamp."""
+    lab = np.asarray(labels)
+    pos = lab > 0
+    edge = np.zeros(lab.shape, dtype=bool)
+    for sh in (1, -1):
+        nb = np.roll(lab, sh, axis=1)
+        edge |= pos & (nb > 0) & (nb != lab)
+    up = lab[:-1]
+    edge[1:] |= pos[1:] & (up > 0) & (up != lab[1:])
+    dn = lab[1:]
+    edge[:-1] |= pos[:-1] & (dn > 0) & (dn != lab[:-1])
+    return edge
+
+
+def dilate_chebyshev(mask, radius):
+    """Reference evaluate.py:58-70: (2r+1)^2 square, azimuth wraps, rings clamp."""
+    mask = np.asarray(mask, dtype=bool)
+    if radius == 0:
+        return mask.copy()
+    v = mask.copy()
+    for d in range(1, radius + 1):
+        v[d:] |= mask[:-d]
+        v[:-d] |= mask[d:]
+    out = v.copy()
+    for d in range(1, radius + 1):
+        out |= np.roll(v, d, axis=1) | np.roll(v, -d, axis=1)
+    return out
+
+
+def edge_counts(pred, truth, radius):
+    """(n_pred, n_truth, pred edges matched, truth edges matched)."""
+    pe, te = extract_edges(pred), extract_edges(truth)
+    return (int(pe.sum()), int(te.sum()), int((pe & dilate_chebyshev(te, radius)).sum()),
+            int((te & dilate_chebyshev(pe, radius)).sum()))
+
+
+def edge_prf(pred, truth, radius):
+    """Reference evaluate.py:73-94 -> (precision, recall, f1)."""
+    n_p, n_t, m_p, m_t = edge_counts(pred, truth, radius)
+    if n_p == 0 and n_t == 0:
+        return 1.0, 1.0, 1.0
+    p = m_p / n_p if n_p else 0.0
+    r = m_t / n_t if n_t else 0.0
+    f = 2.0 * p * r / (p + r) if p > 0.0 and r > 0.0 else 0.0
+    return p, r, f

@@ -8,7 +8,9 @@ pkg/src/lidarseg/__init__.py:21-35): data model, ``build_mesh``,
 include/lidarseg_b200.h); there is no CPU fallback.
 """
 
-from .mesh import Mesh, build_mesh, mesh_triangles
+from .evaluate import (EvalConfig, EvalReport, StageStats, bench, dilate_chebyshev, edge_prf, edge_prf_batch,
+                       extract_edges, time_total)
+from .mesh import Mesh, MeshBuilder, build_mesh, mesh_triangles
 from .normals import NormalMap, estimate_normals, node_positions, normal_from_neighbors, normals_to_grid, point_normal
 from .pipeline import BatchPipeline, PipelineConfig, PipelineResult, StreamingPipeline, bin_points, run_pipeline
 from .scan import (INVALID, GridIndex, Point3, ScanGrid, SensorConfig, polar_to_cartesian, subsample_steps,

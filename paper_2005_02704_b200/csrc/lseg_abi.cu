@@ -328,4 +328,42 @@ int lseg_run_pipeline(const lseg_sensor* sensor, int32_t frames, int32_t interva
   return check_launch("run_pipeline");
 }
 
+// ---------------------------------------------------------------- evaluator (F1)
+size_t lseg_eval_workspace_bytes(int32_t frames, int32_t rings, int32_t steps) {
+  if (frames < 0 || rings < 1 || steps < 1) return 0;
+  return eval_workspace_bytes(frames, rings, steps);
+}
+
+static int check_eval(int32_t frames, int32_t rings, int32_t steps, int32_t radius, void* ws, size_t ws_bytes) {
+  if (frames < 0 || rings < 1 || steps < 1) return fail(LSEG_EINVAL, "bad shape");
+  if (radius < 0) return fail(LSEG_EINVAL, "dilation_radius must be >= 0");
+  if (frames > 0 && (!ws || ws_bytes < eval_workspace_bytes(frames, rings, steps)))
+    return fail(LSEG_EWORKSPACE, "workspace too small");
+  return LSEG_OK;
+}
+
+int lseg_edge_counts(int32_t frames, int32_t rings, int32_t steps, const int32_t* pred, const int32_t* truth,
+                     int32_t radius, int32_t* counts, void* workspace, size_t workspace_bytes, void* stream) {
+  if (int e = check_eval(frames, rings, steps, radius, workspace, workspace_bytes)) return e;
+  if (frames == 0) return LSEG_OK;
+  if (!pred || !truth || !counts) return fail(LSEG_EINVAL, "NULL buffer");
+  return eval_counts(frames, rings, steps, pred, truth, radius, counts, workspace, (cudaStream_t)stream);
+}
+
+int lseg_extract_edges(int32_t frames, int32_t rings, int32_t steps, const int32_t* labels, uint8_t* edges,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+  if (int e = check_eval(frames, rings, steps, 0, workspace, workspace_bytes)) return e;
+  if (frames == 0) return LSEG_OK;
+  if (!labels || !edges) return fail(LSEG_EINVAL, "NULL buffer");
+  return eval_extract(frames, rings, steps, labels, edges, workspace, (cudaStream_t)stream);
+}
+
+int lseg_dilate_chebyshev(int32_t frames, int32_t rings, int32_t steps, const uint8_t* mask, int32_t radius,
+                          uint8_t* out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (int e = check_eval(frames, rings, steps, radius, workspace, workspace_bytes)) return e;
+  if (frames == 0) return LSEG_OK;
+  if (!mask || !out) return fail(LSEG_EINVAL, "NULL buffer");
+  return eval_dilate(frames, rings, steps, mask, radius, out, workspace, (cudaStream_t)stream);
+}
+
 }  // extern "C"

@@ -36,4 +36,9 @@ void launch_scan_bits(const Shape& sh, const uint32_t* bits, int32_t* pre, int32
                       cudaStream_t st);
 void launch_prune_fused(const Shape& sh, const Workspace& ws, int32_t min_size, int32_t* labels, cudaStream_t st);
 void debug_phases(double* out);
+size_t eval_workspace_bytes(int F, int R, int S);
+int eval_counts(int F, int R, int S, const int32_t* pred, const int32_t* truth, int r, int32_t* counts, void* ws,
+                cudaStream_t st);
+int eval_extract(int F, int R, int S, const int32_t* labels, uint8_t* out, void* ws, cudaStream_t st);
+int eval_dilate(int F, int R, int S, const uint8_t* mask, int r, uint8_t* out, void* ws, cudaStream_t st);
 }  // namespace lseg

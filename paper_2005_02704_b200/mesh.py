@@ -78,7 +78,7 @@ class Mesh:
         return d
 
 
-def build_mesh(grid: ScanGrid, interval: int, max_edge_length: float | None = None) -> Mesh:
+def build_mesh(grid: ScanGrid, interval: int, max_edge_length: float | None = None, _device_ranges=None) -> Mesh:
     """GPU build_mesh (reference mesh.py:105-136)."""
     kept = subsample_steps(grid.config, interval)  # ValueError contract
     L = _lib.lib()
@@ -87,7 +87,7 @@ def build_mesh(grid: ScanGrid, interval: int, max_edge_length: float | None = No
     cap = R * Sk
     dev = torch.device("cuda")
     _, sn = device_tables(cfg, dev)
-    ranges = grid.device_ranges(dev)
+    ranges = grid.device_ranges(dev) if _device_ranges is None else _device_ranges
     node_ids = torch.empty((1, R, Sk), dtype=torch.int32, device=dev)
     nbrs = torch.empty((1, cap, 6), dtype=torch.int32, device=dev)
     node_rings = torch.empty((1, cap), dtype=torch.int32, device=dev)
@@ -105,6 +105,46 @@ def build_mesh(grid: ScanGrid, interval: int, max_edge_length: float | None = No
                 node_steps=node_steps[0, :n].cpu().numpy().astype(np.int64),
                 node_ids=node_ids[0].cpu().numpy(), neighbors=nbrs[0, :n].cpu().numpy(),
                 _dev={"node_ids": node_ids, "neighbors": nbrs, "n_nodes": n_nodes})
+
+
+class MeshBuilder:
+    """Incremental mesh construction, one kept azimuth column at a time
+    (reference mesh.py:139-170).
+
+    Columns arrive in sweep order while the sensor spins; each is copied to its
+    slot of a device range grid as it arrives (asynchronously, from pinned
+    memory), so ``finish()`` only runs the GPU mesh build on data already
+    resident in HBM.  The result equals ``build_mesh`` on the assembled grid.
+    """
+
+    def __init__(self, grid_config, interval: int):
+        self.config = grid_config
+        self.interval = int(interval)
+        self.kept = subsample_steps(grid_config, interval)
+        self._n = 0
+        _lib.lib()
+        R, S = grid_config.rings, grid_config.azimuth_steps
+        self._dev = torch.full((R, S), float("nan"), dtype=torch.float64, device="cuda")
+        self._host = torch.empty((self.kept.size, R), dtype=torch.float64).pin_memory()
+        self._cols = []
+
+    def add_column(self, ranges) -> None:
+        col = np.asarray(ranges, dtype=float).reshape(-1)
+        if col.size != self.config.rings:
+            raise ValueError(f"column length {col.size} != ring count {self.config.rings}")
+        if self._n >= self.kept.size:
+            raise ValueError("all kept columns already supplied")
+        self._host[self._n].copy_(torch.from_numpy(col))
+        self._dev[:, int(self.kept[self._n])].copy_(self._host[self._n], non_blocking=True)
+        self._cols.append(col)
+        self._n += 1
+
+    def finish(self) -> Mesh:
+        if self._n != self.kept.size:
+            raise ValueError(f"expected {self.kept.size} kept columns, got {self._n}")
+        full = np.full((self.config.rings, self.config.azimuth_steps), np.nan)
+        full[:, self.kept] = np.stack(self._cols, axis=1)
+        return build_mesh(ScanGrid(config=self.config, ranges=full), self.interval, _device_ranges=self._dev)
 
 
 def mesh_triangles(mesh: Mesh) -> np.ndarray:

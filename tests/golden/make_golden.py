@@ -121,6 +121,21 @@ def main(ref_src="/root/reference/pkg/src"):
         out[f"fill{i}"] = dict(elev=elev, steps=S, ranges=rr, labels_in=lab, filled=filled,
                                mseg=m, pruned=L.prune_small(filled, m))
 
+    # --- edge evaluator (reference evaluate.py:40-94) on pipeline labels vs truth-like grids
+    for i, (R, S, r) in enumerate([(16, 180, 2), (8, 37, 1), (5, 12, 0), (6, 64, 3)]):
+        pred = rng.integers(0, 6, size=(R, S)).astype(np.int32)
+        pred[rng.random((R, S)) < 0.2] = 0
+        truth = np.repeat(rng.integers(0, 4, size=(R, 1 + S // 8)), 8, axis=1)[:, :S].astype(np.int32)
+        rep = L.edge_prf(pred, truth, L.EvalConfig(dilation_radius=r))
+        out[f"edges{i}"] = dict(pred=pred, truth=truth, radius=r, pe=L.extract_edges(pred),
+                                te=L.extract_edges(truth), dil=L.dilate_chebyshev(L.extract_edges(truth), r),
+                                prf=np.array([rep.precision, rep.recall, rep.f1]))
+    g = out["vlp16_k1"]
+    cfg = L.SensorConfig(ring_elevations=g["elev"], azimuth_steps=int(g["steps"]))
+    rep = L.edge_prf(g["labels"], out["vlp16_k5"]["labels"], L.EvalConfig())
+    out["edges_vlp"] = dict(pred=g["labels"], truth=out["vlp16_k5"]["labels"], radius=2,
+                            prf=np.array([rep.precision, rep.recall, rep.f1]))
+
     for name, d in out.items():
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
     print(f"wrote {len(out)} golden files to {HERE}")

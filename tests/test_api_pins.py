@@ -306,3 +306,27 @@ def test_prune_rules(L):
     out = L.prune_small(lab, 5)
     assert out[0, 0] == 1 and out[0, 13] == 2 and out[0, 30] == 3
     np.testing.assert_array_equal(L.prune_small(lab, 0), lab)
+
+
+# ---------------------------------------------------------------- streaming builder (F2)
+@pytest.mark.parametrize("k", [1, 3])
+def test_streaming_builder_equals_batch(L, k):
+    rng = np.random.default_rng(42)
+    g = mask_grid(L, rng.random((6, 12)) < 0.8)
+    batch = L.build_mesh(g, k)
+    b = L.MeshBuilder(g.config, k)
+    for step in L.subsample_steps(g.config, k):
+        b.add_column(np.asarray(g.ranges)[:, step])
+    m = b.finish()
+    np.testing.assert_array_equal(batch.neighbors, m.neighbors)
+    np.testing.assert_array_equal(batch.node_ids, m.node_ids)
+
+
+def test_streaming_builder_contract(L):
+    g = const_grid(L)
+    b = L.MeshBuilder(g.config, 1)
+    b.add_column(np.full(4, 5.0))
+    with pytest.raises(ValueError):
+        b.finish()
+    with pytest.raises(ValueError):
+        b.add_column(np.full(3, 5.0))

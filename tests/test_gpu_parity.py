@@ -203,3 +203,26 @@ def test_unsorted_points_k5(L, oracle):
     want = oracle.run_from_points(xyz.cpu().numpy(), ring.cpu().numpy(), shape.elevations, shape.steps, 5,
                                   shape.r_min, shape.r_max)
     np.testing.assert_array_equal(bp.frame(0)["labels"], want["labels"])
+
+
+@pytest.mark.parametrize("name", golden_names("edges"))
+def test_edge_evaluator_golden(L, name):
+    g = load_golden(name)
+    r = int(g["radius"])
+    if "pe" in g:
+        np.testing.assert_array_equal(L.extract_edges(g["pred"]), g["pe"])
+        np.testing.assert_array_equal(L.extract_edges(g["truth"]), g["te"])
+        np.testing.assert_array_equal(L.dilate_chebyshev(g["te"], r), g["dil"])
+    rep = L.edge_prf(g["pred"], g["truth"], L.EvalConfig(dilation_radius=r))
+    np.testing.assert_array_equal([rep.precision, rep.recall, rep.f1], g["prf"])
+
+
+def test_edge_prf_batch_matches_oracle(L, oracle):
+    """Batched device scoring of pipeline labels against a second labelling."""
+    shape, cfg, bp, xyz, ring, off = _run_batch(L, "hdl64", 3, 1, seed=6)
+    other = L.BatchPipeline(cfg, 5, frames=3)
+    other.run(torch.from_numpy(xyz).cuda(), torch.from_numpy(ring).cuda(), torch.from_numpy(off).cuda())
+    prf = L.edge_prf_batch(bp.labels, other.labels, 2).cpu().numpy()
+    for f in range(3):
+        want = oracle.edge_prf(bp.labels[f].cpu().numpy(), other.labels[f].cpu().numpy(), 2)
+        np.testing.assert_allclose(prf[f], want, rtol=1e-12)

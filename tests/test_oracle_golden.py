@@ -91,3 +91,14 @@ def test_bin_collision_and_ring_convention(oracle):
     assert got[1, 2] == 3.0
     assert cell.tolist() == [0, 0, 10, -1, -1]  # r=0.2 < r_min, r=200 > r_max
     assert np.isnan(got).sum() == 14
+
+
+@pytest.mark.parametrize("name", golden_names("edges"))
+def test_edge_evaluator(oracle, name):
+    g = load_golden(name)
+    r = int(g["radius"])
+    if "pe" in g:
+        np.testing.assert_array_equal(oracle.extract_edges(g["pred"]), g["pe"])
+        np.testing.assert_array_equal(oracle.extract_edges(g["truth"]), g["te"])
+        np.testing.assert_array_equal(oracle.dilate_chebyshev(g["te"], r), g["dil"])
+    np.testing.assert_allclose(oracle.edge_prf(g["pred"], g["truth"], r), g["prf"], rtol=0, atol=0)
