@@ -1103,6 +1103,68 @@ __global__ void k_survivors(Shape sh, const uint32_t* __restrict__ rbits, const 
   if (lane == 0 && any) atomicOr(fscal + f * 4, 1);
 }
 
+// Survivor bits + their per-frame exclusive word prefix in one pass (one CTA
+// per frame): replaces k_survivors + k_frame_scan.
+template <int T, int ITEMS>
+__global__ void __launch_bounds__(T) k_survivor_scan(Shape sh, const uint32_t* __restrict__ rbits,
+                                                     const int32_t* __restrict__ hist, int64_t K, int32_t min_size,
+                                                     uint32_t* __restrict__ sbits, int32_t* __restrict__ spre,
+                                                     int32_t* __restrict__ fscal, int32_t* __restrict__ nsurv) {
+  using Scan = cub::BlockScan<int, T>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry, s_any;
+  const int f = blockIdx.x;
+  const int n = sh.R * sh.Wk;
+  const uint32_t* rb = rbits + (int64_t)f * n;
+  uint32_t* sb = sbits + (int64_t)f * n;
+  int32_t* sp = spre + (int64_t)f * n;
+  const int32_t* hf = hist + (int64_t)f * K;
+  if (threadIdx.x == 0) { carry = 0; s_any = 0; }
+  __syncthreads();
+  int any = 0;
+  for (int base = 0; base < n; base += T * ITEMS) {
+    uint32_t w[ITEMS];
+    int cnt[ITEMS];
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      const int idx = base + threadIdx.x * ITEMS + j;
+      w[j] = idx < n ? __ldg(rb + idx) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      const int idx = base + threadIdx.x * ITEMS + j;
+      uint32_t surv = w[j];
+      if (min_size > 0 && w[j]) {
+        const int row = idx / sh.Wk;
+        const int cell0 = row * sh.Sk + (idx - row * sh.Wk) * 32 + 1;  // hist slot of the word's first cell
+        for (uint32_t m = w[j]; m; m &= m - 1) {
+          const int b = __ffs(m) - 1;
+          if (__ldg(hf + cell0 + b) < min_size) { surv &= ~(1u << b); any = 1; }
+        }
+      }
+      w[j] = surv;
+      cnt[j] = __popc(surv);
+    }
+    int x[ITEMS], total;
+    Scan(tmp).ExclusiveSum(cnt, x, total);
+    const int c0 = carry;
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      const int idx = base + threadIdx.x * ITEMS + j;
+      if (idx < n) { sb[idx] = w[j]; sp[idx] = c0 + x[j]; }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry = c0 + total;
+    __syncthreads();
+  }
+  if (any) s_any = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fscal[f * 4] = s_any;
+    nsurv[f] = carry;
+  }
+}
+
 // Dissolve small segments into the nearest surviving ring donor (reference
 // segment.py:141-154) and write the final compacted ids, one CTA per ring row.
 template <int T>
@@ -1158,13 +1220,8 @@ __global__ void __launch_bounds__(T) k_prune_rows(Shape sh, const int32_t* __res
 }
 
 void launch_prune_fused(const Shape& sh, const Workspace& ws, int32_t min_size, int32_t* labels, cudaStream_t st) {
-  cudaMemsetAsync(ws.fscal, 0, sizeof(int32_t) * 4 * sh.F, st);
-  const int64_t nwords = (int64_t)sh.F * sh.R * sh.Wk;
-  const int64_t blocks = (nwords * 32 + 255) / 256;
-  (void)blocks;
-  k_survivors<<<sh.F * sh.R, sh.Wk >= 8 ? 256 : 32 * sh.Wk, 0, st>>>(sh, ws.rbits, ws.hist, ws.K, min_size, ws.sbits,
-                                                                     ws.fscal);
-  launch_scan_bits(sh, ws.sbits, ws.spre, ws.fscal_cnt, nullptr, 0, st);
+  k_survivor_scan<512, 4><<<sh.F, 512, 0, st>>>(sh, ws.rbits, ws.hist, ws.K, min_size, ws.sbits, ws.spre, ws.fscal,
+                                                 ws.fscal_cnt);
   prof_mark("prune_plan", st);
   const int nwr = (sh.S + 31) / 32;
   const size_t smem = sizeof(int) * (size_t)nwr * 33;
