@@ -321,13 +321,15 @@ def main():
     e2e = None
     if not a.no_e2e:
         hx = xyz.cpu().pin_memory()
-        hr = ring.cpu().pin_memory()
+        # ring ids travel as one byte each (<= 256 rings): 13 B instead of 16 B per point
+        rdt = torch.uint8 if cfg.rings <= 256 else torch.int32
+        hr = ring.to(rdt).cpu().pin_memory()
         ho = off.cpu()
         hl = torch.empty(bp.labels.shape, dtype=torch.int32).pin_memory()
         cf = min(64, F)
         maxp = max(int(ho[min(f + cf, F)] - ho[f]) for f in range(0, F, cf))
         del bp  # free the device-resident pipeline before allocating the streaming one
-        sp = L.StreamingPipeline(cfg, a.interval, chunk_frames=cf, max_chunk_points=maxp, device=dev)
+        sp = L.StreamingPipeline(cfg, a.interval, chunk_frames=cf, max_chunk_points=maxp, device=dev, ring_dtype=rdt)
         for _ in range(2):
             sp.run_host(hx, hr, ho, hl)
         torch.cuda.synchronize()
@@ -340,10 +342,10 @@ def main():
         te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if ws > 1:
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-        h2d = hx.numel() * 4 + hr.numel() * 4 + ho.numel() * 8
+        h2d = hx.numel() * hx.element_size() + hr.numel() * hr.element_size() + ho.numel() * ho.element_size()
         e2e = {"value": float(tot_pts.item()) * a.steps / (float(te.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(hl.numel() * 4),
-               "ms_per_step": float(te.item()) / a.steps, "chunk_frames": cf}
+               "ms_per_step": float(te.item()) / a.steps, "chunk_frames": cf, "ring_dtype": str(rdt).replace("torch.", "")}
 
     cpu = None
     if rank == 0 and ws == 1 and not a.no_cpu_baseline:

@@ -142,6 +142,16 @@ int lseg_run_pipeline(const lseg_sensor* sensor, int32_t frames, int32_t interva
                       uint8_t* nmask, int32_t* node_labels, int32_t* labels, int32_t* n_nodes,
                       int32_t* n_labels, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Same as lseg_run_pipeline with one-byte ring ids (every real spinning
+ * sensor has <= 256 rings): 13 instead of 16 bytes per input point, which is
+ * what bounds the host-to-device copy of a streamed batch. */
+int lseg_run_pipeline_r8(const lseg_sensor* sensor, int32_t frames, int32_t interval,
+                         const double* thresholds, int32_t min_segment_size, const float* xyz,
+                         const uint8_t* ring, const int64_t* frame_offsets, int64_t total_points,
+                         double* ranges, int32_t* node_ids, int32_t* neighbors, float* normals32,
+                         uint8_t* nmask, int32_t* node_labels, int32_t* labels, int32_t* n_nodes,
+                         int32_t* n_labels, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- edge-based evaluation (reference evaluate.py:40-94).
  * Label grids (F,R,S) i32, 0 = unlabelled.  Scratch sized by
  * lseg_eval_workspace_bytes. */

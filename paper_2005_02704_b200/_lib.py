@@ -46,6 +46,8 @@ _SIGS = {
                                C.c_size_t, _P]),
     "lseg_backfill": (C.c_int, [C.POINTER(lseg_sensor), _I32, _P, _P, _P, _P]),
     "lseg_prune_small": (C.c_int, [_I32, _I32, _I32, _P, _I32, _I64, _P, _P, C.c_size_t, _P]),
+    "lseg_run_pipeline_r8": (C.c_int, [C.POINTER(lseg_sensor), _I32, _I32, C.POINTER(C.c_double), _I32, _P, _P, _P,
+                                       _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
     "lseg_eval_workspace_bytes": (C.c_size_t, [_I32, _I32, _I32]),
     "lseg_edge_counts": (C.c_int, [_I32, _I32, _I32, _P, _P, _I32, _P, _P, C.c_size_t, _P]),
     "lseg_extract_edges": (C.c_int, [_I32, _I32, _I32, _P, _P, _P, C.c_size_t, _P]),

@@ -295,12 +295,12 @@ int lseg_prune_small(int32_t frames, int32_t rings, int32_t steps, const int32_t
   return check_launch("prune_small");
 }
 
-int lseg_run_pipeline(const lseg_sensor* sensor, int32_t frames, int32_t interval, const double* thresholds,
-                      int32_t min_segment_size, const float* xyz, const int32_t* ring,
-                      const int64_t* frame_offsets, int64_t total_points, double* ranges, int32_t* node_ids,
-                      int32_t* neighbors, float* normals32, uint8_t* nmask, int32_t* node_labels,
-                      int32_t* labels, int32_t* n_nodes, int32_t* n_labels, void* workspace,
-                      size_t workspace_bytes, void* stream) {
+static int run_pipeline_impl(const lseg_sensor* sensor, int32_t frames, int32_t interval, const double* thresholds,
+                             int32_t min_segment_size, const float* xyz, const void* ring, int ring_bytes,
+                             const int64_t* frame_offsets, int64_t total_points, double* ranges, int32_t* node_ids,
+                             int32_t* neighbors, float* normals32, uint8_t* nmask, int32_t* node_labels,
+                             int32_t* labels, int32_t* n_nodes, int32_t* n_labels, void* workspace,
+                             size_t workspace_bytes, void* stream) {
   if (int e = check_sensor(sensor)) return e;
   Shape sh;
   if (int e = check_shape(frames, sensor->rings, sensor->steps, interval, &sh)) return e;
@@ -316,16 +316,40 @@ int lseg_run_pipeline(const lseg_sensor* sensor, int32_t frames, int32_t interva
   cudaStream_t st = (cudaStream_t)stream;
   prof_mark(nullptr, st);
   const bool fused_bin = sensor->steps <= 8192;
+  if (!fused_bin && ring_bytes != 4) return fail(LSEG_EINVAL, "byte ring ids need azimuth_steps <= 8192");
   if (fused_bin) {
-    launch_bin_fused(*sensor, sh, xyz, ring, frame_offsets, ws, ranges, n_nodes, st);
+    launch_bin_fused(*sensor, sh, xyz, ring, ring_bytes, frame_offsets, ws, ranges, n_nodes, st);
   } else {
-    launch_bin(*sensor, frames, xyz, ring, frame_offsets, total_points, ranges, nullptr, st);
+    launch_bin(*sensor, frames, xyz, static_cast<const int32_t*>(ring), frame_offsets, total_points, ranges, nullptr,
+               st);
     launch_valid_scan(*sensor, sh, ranges, ws, n_nodes, st);
   }
   launch_fused_graph(*sensor, sh, ws, ranges, thresholds, node_ids, neighbors, normals32, nmask, n_nodes, n_labels,
                      node_labels, fused_bin, st);
   launch_prune_fused(sh, ws, min_segment_size, labels, st);
   return check_launch("run_pipeline");
+}
+
+int lseg_run_pipeline(const lseg_sensor* sensor, int32_t frames, int32_t interval, const double* thresholds,
+                      int32_t min_segment_size, const float* xyz, const int32_t* ring,
+                      const int64_t* frame_offsets, int64_t total_points, double* ranges, int32_t* node_ids,
+                      int32_t* neighbors, float* normals32, uint8_t* nmask, int32_t* node_labels,
+                      int32_t* labels, int32_t* n_nodes, int32_t* n_labels, void* workspace,
+                      size_t workspace_bytes, void* stream) {
+  return run_pipeline_impl(sensor, frames, interval, thresholds, min_segment_size, xyz, ring, 4, frame_offsets,
+                           total_points, ranges, node_ids, neighbors, normals32, nmask, node_labels, labels, n_nodes,
+                           n_labels, workspace, workspace_bytes, stream);
+}
+
+int lseg_run_pipeline_r8(const lseg_sensor* sensor, int32_t frames, int32_t interval, const double* thresholds,
+                         int32_t min_segment_size, const float* xyz, const uint8_t* ring,
+                         const int64_t* frame_offsets, int64_t total_points, double* ranges, int32_t* node_ids,
+                         int32_t* neighbors, float* normals32, uint8_t* nmask, int32_t* node_labels,
+                         int32_t* labels, int32_t* n_nodes, int32_t* n_labels, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  return run_pipeline_impl(sensor, frames, interval, thresholds, min_segment_size, xyz, ring, 1, frame_offsets,
+                           total_points, ranges, node_ids, neighbors, normals32, nmask, node_labels, labels, n_nodes,
+                           n_labels, workspace, workspace_bytes, stream);
 }
 
 // ---------------------------------------------------------------- evaluator (F1)

@@ -868,12 +868,13 @@ static constexpr double kTwoPiF = 6.283185307179586;  // == 2.0 * np.pi
 // 32-ary search (4 dependent probes for a 124 k-point frame instead of 17).
 // Exact for ring-major input; for other orders the result is arbitrary but in
 // range, and k_bin_rows' segment check sends the frame to the generic path.
-__device__ __forceinline__ int64_t warp_lower_bound(const int32_t* __restrict__ ring, int64_t lo, int64_t hi, int v,
+template <typename RT>
+__device__ __forceinline__ int64_t warp_lower_bound(const RT* __restrict__ ring, int64_t lo, int64_t hi, int v,
                                                     int lane) {
   while (hi - lo > 32) {
     const int64_t step = (hi - lo + 31) / 32;
     const int64_t q = lo + (int64_t)lane * step;
-    const bool less = (q < hi) && (__ldg(ring + q) < v);
+    const bool less = (q < hi) && ((int)__ldg(ring + q) < v);
     const unsigned m = __ballot_sync(0xffffffffu, less);
     const int c = (~m == 0u) ? 32 : __ffs(~m) - 1;  // leading lanes with ring < v
     const int64_t nlo = (c == 0) ? lo : lo + (int64_t)(c - 1) * step + 1;
@@ -882,7 +883,7 @@ __device__ __forceinline__ int64_t warp_lower_bound(const int32_t* __restrict__ 
     hi = nhi;
   }
   const int64_t q = lo + lane;
-  const unsigned m = __ballot_sync(0xffffffffu, (q < hi) && (__ldg(ring + q) < v));
+  const unsigned m = __ballot_sync(0xffffffffu, (q < hi) && ((int)__ldg(ring + q) < v));
   const int c = (~m == 0u) ? 32 : __ffs(~m) - 1;
   return min(hi, lo + c);
 }
@@ -939,9 +940,9 @@ __device__ __forceinline__ bool bin_one(const lseg_sensor& sn, const float* __re
 // (no memset, no global atomics).  The CTA verifies that its binary-searched
 // segment really holds only its ring (and ring 0 / R-1 check the prefix /
 // suffix), so any other input order flips the frame to the generic path.
-template <int T>
+template <int T, typename RT>
 __global__ void __launch_bounds__(T) k_bin_rows(lseg_sensor sn, Shape sh, const float* __restrict__ xyz,
-                                                const int32_t* __restrict__ ring, const int64_t* __restrict__ off,
+                                                const RT* __restrict__ ring, const int64_t* __restrict__ off,
                                                 const int64_t* __restrict__ seg, double* __restrict__ ranges,
                                                 uint32_t* __restrict__ vbits, uint32_t* __restrict__ fbits,
                                                 int32_t* __restrict__ fallback) {
@@ -967,7 +968,7 @@ __global__ void __launch_bounds__(T) k_bin_rows(lseg_sensor sn, Shape sh, const 
       pr[j] = i;
       px[j] = py[j] = pz[j] = 0.0f;
       if (p < hi) {
-        pr[j] = __ldg(ring + p);
+        pr[j] = (int)__ldg(ring + p);
         px[j] = __ldg(xyz + 3 * p);
         py[j] = __ldg(xyz + 3 * p + 1);
         pz[j] = __ldg(xyz + 3 * p + 2);
@@ -984,9 +985,9 @@ __global__ void __launch_bounds__(T) k_bin_rows(lseg_sensor sn, Shape sh, const 
     }
   }
   if (i == 0)
-    for (int64_t p = p0 + threadIdx.x; p < lo; p += T) bad |= (__ldg(ring + p) >= 0) ? 1 : 0;
+    for (int64_t p = p0 + threadIdx.x; p < lo; p += T) bad |= ((int)__ldg(ring + p) >= 0) ? 1 : 0;
   if (i == sh.R - 1)
-    for (int64_t p = hi + threadIdx.x; p < p1; p += T) bad |= (__ldg(ring + p) < sh.R) ? 1 : 0;
+    for (int64_t p = hi + threadIdx.x; p < p1; p += T) bad |= ((int)__ldg(ring + p) < sh.R) ? 1 : 0;
   if (bad) s_bad = 1;
   __syncthreads();
   if (s_bad) {
@@ -1015,7 +1016,8 @@ __global__ void __launch_bounds__(T) k_bin_rows(lseg_sensor sn, Shape sh, const 
 
 // Ring segment bounds of ring-major input: seg[f][i] = first point of frame f
 // with ring >= i, i = 0..R, one warp per entry (32-ary search).
-__global__ void k_ring_bounds(Shape sh, const int32_t* __restrict__ ring, const int64_t* __restrict__ off,
+template <typename RT>
+__global__ void k_ring_bounds(Shape sh, const RT* __restrict__ ring, const int64_t* __restrict__ off,
                              int64_t* __restrict__ seg) {
   const int f = blockIdx.y;
   const int lane = threadIdx.x & 31;
@@ -1039,14 +1041,15 @@ __global__ void k_bin_reset(Shape sh, const int32_t* __restrict__ fallback, doub
 }
 
 // Generic path: global 64-bit atomicMin per point + atomicOr of the kept bit.
-__global__ void k_bin_atomic(lseg_sensor sn, Shape sh, const float* __restrict__ xyz, const int32_t* __restrict__ ring,
+template <typename RT>
+__global__ void k_bin_atomic(lseg_sensor sn, Shape sh, const float* __restrict__ xyz, const RT* __restrict__ ring,
                              const int64_t* __restrict__ off, const int32_t* __restrict__ fallback,
                              double* __restrict__ ranges, uint32_t* __restrict__ vbits, uint32_t* __restrict__ fbits) {
   const int f = blockIdx.y;
   if (!__ldg(fallback + f)) return;
   const int64_t p0 = __ldg(off + f), p1 = __ldg(off + f + 1);
   for (int64_t p = p0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < p1; p += (int64_t)gridDim.x * blockDim.x) {
-    const int rg = __ldg(ring + p);
+    const int rg = (int)__ldg(ring + p);
     double r;
     int st;
     if (rg < 0 || rg >= sh.R || !bin_one(sn, xyz, p, r, st)) continue;
@@ -1061,19 +1064,26 @@ __global__ void k_bin_atomic(lseg_sensor sn, Shape sh, const float* __restrict__
   }
 }
 
-void launch_bin_fused(const lseg_sensor& sn, const Shape& sh, const float* xyz, const int32_t* ring,
-                      const int64_t* off, const Workspace& ws, double* ranges, int32_t* n_nodes, cudaStream_t st) {
+template <typename RT>
+static void bin_fused_t(const lseg_sensor& sn, const Shape& sh, const float* xyz, const RT* ring, const int64_t* off,
+                        const Workspace& ws, double* ranges, cudaStream_t st) {
   cudaMemsetAsync(ws.fallback, 0, sizeof(int32_t) * sh.F, st);
   const size_t smem = sizeof(unsigned long long) * sh.S;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_bin_rows<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_ring_bounds<<<dim3((sh.R + 1 + 7) / 8, sh.F), 256, 0, st>>>(sh, ring, off, ws.seg);
-  k_bin_rows<256><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, xyz, ring, off, ws.seg, ranges, ws.vbits, ws.fbits,
-                                                 ws.fallback);
+    cudaFuncSetAttribute(k_bin_rows<256, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_ring_bounds<RT><<<dim3((sh.R + 1 + 7) / 8, sh.F), 256, 0, st>>>(sh, ring, off, ws.seg);
+  k_bin_rows<256, RT><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, xyz, ring, off, ws.seg, ranges, ws.vbits, ws.fbits,
+                                                     ws.fallback);
   prof_mark("bin_rows", st);
   k_bin_reset<<<sh.F * sh.R, 256, 0, st>>>(sh, ws.fallback, ranges, ws.vbits, ws.fbits);
-  k_bin_atomic<<<dim3(8, sh.F), 256, 0, st>>>(sn, sh, xyz, ring, off, ws.fallback, ranges, ws.vbits, ws.fbits);
+  k_bin_atomic<RT><<<dim3(8, sh.F), 256, 0, st>>>(sn, sh, xyz, ring, off, ws.fallback, ranges, ws.vbits, ws.fbits);
   prof_mark("bin_fallback", st);
+}
+
+void launch_bin_fused(const lseg_sensor& sn, const Shape& sh, const float* xyz, const void* ring, int ring_bytes,
+                      const int64_t* off, const Workspace& ws, double* ranges, int32_t* n_nodes, cudaStream_t st) {
+  if (ring_bytes == 1) bin_fused_t(sn, sh, xyz, static_cast<const uint8_t*>(ring), off, ws, ranges, st);
+  else bin_fused_t(sn, sh, xyz, static_cast<const int32_t*>(ring), off, ws, ranges, st);
   launch_frame_scan(sh, ws, n_nodes, st);
 }
 

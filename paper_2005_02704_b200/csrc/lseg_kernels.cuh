@@ -29,7 +29,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
                         const double* thr, int32_t* node_ids, int32_t* neighbors, float* n32, uint8_t* nmask,
                         int32_t* n_nodes, int32_t* n_labels, int32_t* node_labels, bool fbits_valid,
                         cudaStream_t st);
-void launch_bin_fused(const lseg_sensor& sn, const Shape& sh, const float* xyz, const int32_t* ring,
+void launch_bin_fused(const lseg_sensor& sn, const Shape& sh, const float* xyz, const void* ring, int ring_bytes,
                       const int64_t* off, const Workspace& ws, double* ranges, int32_t* n_nodes, cudaStream_t st);
 void launch_frame_scan(const Shape& sh, const Workspace& ws, int32_t* n_nodes, cudaStream_t st);
 void launch_scan_bits(const Shape& sh, const uint32_t* bits, int32_t* pre, int32_t* counts, int32_t* hist, int64_t K,

@@ -138,7 +138,13 @@ class BatchPipeline:
     def _call(self, f0, f1, ws, xyz, ring, offsets):
         P = int(xyz.shape[0])
         sl = lambda t: None if t is None else t[f0:f1]
-        _lib.check(self.L.lseg_run_pipeline(
+        if ring.dtype == torch.uint8:
+            fn = self.L.lseg_run_pipeline_r8
+        elif ring.dtype == torch.int32:
+            fn = self.L.lseg_run_pipeline
+        else:
+            raise ValueError("ring ids must be int32 or uint8")
+        _lib.check(fn(
             self.sn, f1 - f0, self.interval, self.thr, int(self.seg.min_segment_size), _lib.ptr(xyz),
             _lib.ptr(ring), _lib.ptr(offsets[f0:]), P, _lib.ptr(sl(self.ranges)), _lib.ptr(sl(self.node_ids)),
             _lib.ptr(sl(self.neighbors)), _lib.ptr(sl(self.normals)), _lib.ptr(sl(self.nmask)),
@@ -181,14 +187,15 @@ class StreamingPipeline:
     """
 
     def __init__(self, config: SensorConfig, interval: int, segmenter: SegmenterConfig | None = None,
-                 chunk_frames: int = 64, max_chunk_points: int | None = None, device=None):
+                 chunk_frames: int = 64, max_chunk_points: int | None = None, device=None,
+                 ring_dtype=torch.int32):
         self.device = torch.device(device or "cuda")
         self.cf = int(chunk_frames)
         R, S = config.rings, config.azimuth_steps
         self.maxp = int(max_chunk_points or self.cf * R * S)
         self.bps = [BatchPipeline(config, interval, segmenter, frames=self.cf, device=self.device) for _ in range(2)]
         self.xyz = [torch.empty((self.maxp, 3), dtype=torch.float32, device=self.device) for _ in range(2)]
-        self.ring = [torch.empty(self.maxp, dtype=torch.int32, device=self.device) for _ in range(2)]
+        self.ring = [torch.empty(self.maxp, dtype=ring_dtype, device=self.device) for _ in range(2)]
         self.off = [torch.empty(self.cf + 1, dtype=torch.int64, device=self.device) for _ in range(2)]
         self.s_in, self.s_run, self.s_out = (torch.cuda.Stream(self.device) for _ in range(3))
         self.freed = [torch.cuda.Event() for _ in range(2)]     # d2h of the chunk that used buffer b done

@@ -226,3 +226,39 @@ def test_edge_prf_batch_matches_oracle(L, oracle):
     for f in range(3):
         want = oracle.edge_prf(bp.labels[f].cpu().numpy(), other.labels[f].cpu().numpy(), 2)
         np.testing.assert_allclose(prf[f], want, rtol=1e-12)
+
+
+def test_byte_ring_ids_match_int32(L):
+    """lseg_run_pipeline_r8 (one-byte ring ids) == lseg_run_pipeline."""
+    from paper_2005_02704_b200 import synth
+    for name in ("vlp16", "hdl64"):
+        shape = synth.CONFIGS[name]
+        xyz, ring, off = synth.make_batch(shape, frames=2, seed=12, device="cuda")
+        cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
+                             r_max=shape.r_max)
+        a = L.BatchPipeline(cfg, 1, frames=2)
+        b = L.BatchPipeline(cfg, 1, frames=2)
+        la = a.run(xyz, ring, off).clone()
+        lb = b.run(xyz, ring.to(torch.uint8), off).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(la, lb)
+        for f in range(2):
+            n = int(a.n_nodes[f])
+            assert n == int(b.n_nodes[f])
+            assert torch.equal(a.neighbors[f, :n], b.neighbors[f, :n])
+
+
+def test_streaming_pipeline_host_to_host(L):
+    from paper_2005_02704_b200 import synth
+    shape = synth.CONFIGS["hdl64"]
+    xyz, ring, off = synth.make_batch(shape, frames=5, seed=13, device="cuda")
+    cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
+                         r_max=shape.r_max)
+    ref = L.BatchPipeline(cfg, 1, frames=5)
+    want = ref.run(xyz, ring, off).cpu()
+    hx, hr, ho = xyz.cpu().pin_memory(), ring.to(torch.uint8).cpu().pin_memory(), off.cpu()
+    hl = torch.empty((5, shape.rings, shape.steps), dtype=torch.int32).pin_memory()
+    sp = L.StreamingPipeline(cfg, 1, chunk_frames=2, device="cuda", ring_dtype=torch.uint8)
+    sp.run_host(hx, hr, ho, hl)
+    torch.cuda.synchronize()
+    assert torch.equal(hl, want)

@@ -17,3 +17,4 @@ torch.cuda.synchronize(); f(out)
 names = ["", "A halo", "B1 lists", "B2 normals", "C outputs", "D masks"]
 tot = sum(out[1:6])
 for i in range(1, 6): print(f"{names[i]:12s} {100*out[i]/tot:5.1f}%")
+print("tile_cc label-propagation rounds per tile: %.2f" % (out[6] / max(out[7], 1)))
