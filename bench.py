@@ -47,6 +47,7 @@ def parse():
                     help="also time this interval (reference default 5); 0 disables")
     ap.add_argument("--seed", type=int, default=2005)
     ap.add_argument("--streams", type=int, default=1, help="frame chunks on concurrent streams")
+    ap.add_argument("--chunk", type=int, default=0, help="sequential frame chunks of this size (0 = whole batch)")
     return ap.parse_args()
 
 
@@ -242,7 +243,7 @@ def main():
     P = int(xyz.shape[0])
     cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
                          r_max=shape.r_max)
-    bp = L.BatchPipeline(cfg, a.interval, frames=F, device=dev, streams=a.streams)
+    bp = L.BatchPipeline(cfg, a.interval, frames=F, device=dev, streams=a.streams, chunk_frames=a.chunk or None)
     st = torch.cuda.current_stream()
 
     def barrier():

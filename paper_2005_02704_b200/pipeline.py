@@ -102,7 +102,8 @@ class BatchPipeline:
     """
 
     def __init__(self, config: SensorConfig, interval: int, segmenter: SegmenterConfig | None = None,
-                 frames: int = 1, device=None, keep_node_labels: bool = False, streams: int = 1):
+                 frames: int = 1, device=None, keep_node_labels: bool = False, streams: int = 1,
+                 chunk_frames: int | None = None):
         self.L = _lib.lib()
         self.config = config
         self.interval = int(interval)
@@ -130,10 +131,14 @@ class BatchPipeline:
         # latency-bound kernels of one chunk overlap those of another
         self.nstreams = max(1, min(int(streams), F))
         per = -(-F // self.nstreams)
+        if chunk_frames:  # sequential chunks on one stream (L2-sized intermediates)
+            per = max(1, min(int(chunk_frames), F))
+            self.nstreams = 1
         self.chunks = [(f0, min(F, f0 + per)) for f0 in range(0, F, per)]
         self.ws_bytes = _lib.workspace_bytes(per, R, S, interval)
         self.ws = [torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev) for _ in self.chunks]
-        self.streams = [torch.cuda.Stream(dev) for _ in self.chunks] if len(self.chunks) > 1 else None
+        self.streams = ([torch.cuda.Stream(dev) for _ in self.chunks] if len(self.chunks) > 1 and not chunk_frames
+                        else None)
 
     def _call(self, f0, f1, ws, xyz, ring, offsets):
         P = int(xyz.shape[0])
@@ -153,7 +158,8 @@ class BatchPipeline:
 
     def run(self, xyz, ring, offsets):
         if self.streams is None:
-            self._call(0, self.frames, self.ws[0], xyz, ring, offsets)
+            for (f0, f1), ws in zip(self.chunks, self.ws):
+                self._call(f0, f1, ws, xyz, ring, offsets)
             return self.labels
         cur = torch.cuda.current_stream(self.device)
         for (f0, f1), ws, st in zip(self.chunks, self.ws, self.streams):
