@@ -131,6 +131,14 @@ extern "C" {
 
 const char* lseg_last_error(void) { return g_last_error.c_str(); }
 
+// Self-test of the branch-free sqrt / reciprocal used by the pipeline kernels
+// (not part of the public header): mismatch counts vs __dsqrt_rn / __drcp_rn.
+int lseg_selftest_math(int64_t n, uint64_t seed, unsigned long long* bad, void* stream) {
+  if (n < 0 || !bad) return fail(LSEG_EINVAL, "bad arguments");
+  launch_selftest_math(n, seed, bad, (cudaStream_t)stream);
+  return check_launch("selftest_math");
+}
+
 // Debug hook: summed per-phase SM cycles of k_tile (builds with LSEG_PHASES=1).
 void lseg_debug_tile_phases(double* out8) { lseg::debug_phases(out8); }
 

@@ -31,6 +31,10 @@ __device__ unsigned long long g_ph[8];
 #define LSEG_UNR 1
 #endif
 static constexpr int kUnrollNormals = LSEG_UNR;
+#ifndef LSEG_FAST_MATH
+#define LSEG_FAST_MATH 1
+#endif
+static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_FAN6
 #define LSEG_FAN6 0
 #endif
@@ -307,7 +311,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
 #else
     // streamed: only first / previous / current vectors live (fewer registers,
     // more resident warps)
-    Fan fan;
+    FanT<kFastMath> fan;
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       const int gq = g + slot_dr(s) * GC + slot_dc(s);
@@ -328,7 +332,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     const int g = (y + 1) * GC + (x + 1);
     const unsigned m = s_m[e];
     const Vec3 p = {s_px[g], s_py[g], s_pz[g]};
-    Fan fan;
+    FanT<kFastMath> fan;
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       if (!((m >> s) & 1u)) continue;
@@ -910,7 +914,9 @@ __device__ __forceinline__ float fast_atan2(float y, float x) {
 
 __device__ __forceinline__ bool bin_xyz(const lseg_sensor& sn, float xf, float yf, float zf, double& r, int& step) {
   const double x = (double)xf, y = (double)yf, z = (double)zf;
-  r = __dsqrt_rn(__dadd_rn(__dadd_rn(x * x, y * y), z * z));
+  // squares of float inputs are exact and their sum is 0 or >= 2^-298: the
+  // branch-free sqrt is exact here (0 gives NaN, rejected like r = 0)
+  r = sqrt_pos(__dadd_rn(__dadd_rn(x * x, y * y), z * z));
   if (!in_window(r, sn.r_min, sn.r_max)) return false;
   const float scale = (float)sn.steps * 0.15915494309189535f;  // S / (2 pi)
   float ph = fast_atan2(yf, xf);  // |error| <= 1.2e-5 rad

@@ -41,4 +41,5 @@ int eval_counts(int F, int R, int S, const int32_t* pred, const int32_t* truth, 
                 cudaStream_t st);
 int eval_extract(int F, int R, int S, const int32_t* labels, uint8_t* out, void* ws, cudaStream_t st);
 int eval_dilate(int F, int R, int S, const uint8_t* mask, int r, uint8_t* out, void* ws, cudaStream_t st);
+void launch_selftest_math(int64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t st);
 }  // namespace lseg
