@@ -547,14 +547,15 @@ __global__ void __launch_bounds__(T) k_triangles(int R, int Sk, const int32_t* _
 
 // --------------------------------------------------------------------------
 // Self-test of sqrt_pos / rcp_pos against the IEEE intrinsics on n random
-// doubles (log-uniform exponents in [2^-40, 2^40], random mantissas).
+// doubles (random mantissas; log-uniform exponents in [2^-40, 2^40] for odd
+// seeds, [2^-300, 2^300] for even seeds).
 __global__ void k_selftest_math(int64_t n, uint64_t seed, unsigned long long* bad) {
   unsigned long long b0 = 0, b1 = 0;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     uint64_t h = (uint64_t)t * 0x9E3779B97F4A7C15ull ^ seed;
     h ^= h >> 33; h *= 0xff51afd7ed558ccdull; h ^= h >> 33; h *= 0xc4ceb9fe1a85ec53ull; h ^= h >> 33;
     const uint64_t mant = h & 0x000FFFFFFFFFFFFFull;
-    const int ex = (int)((h >> 52) % 81) - 40;
+    const int ex = (seed & 1) ? (int)((h >> 52) % 81) - 40 : (int)((h >> 52) % 601) - 300;
     const double x = __longlong_as_double((long long)(((uint64_t)(1023 + ex) << 52) | mant));
     b0 += sqrt_pos(x) != __dsqrt_rn(x);
     b1 += rcp_pos(x) != __drcp_rn(x);
