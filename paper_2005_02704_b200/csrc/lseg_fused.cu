@@ -35,6 +35,9 @@ static constexpr int kUnrollNormals = LSEG_UNR;
 #define LSEG_FAST_MATH 1
 #endif
 static constexpr bool kFastMath = LSEG_FAST_MATH;
+#ifndef LSEG_POS_RECOMPUTE
+#define LSEG_POS_RECOMPUTE 1
+#endif
 #ifndef LSEG_FAN6
 #define LSEG_FAN6 0
 #endif
@@ -142,7 +145,7 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
 //   E  parent[cell] = tile-local root cell (-1 for cells without a normal)
 template <int TR, int TC, int T>
 #ifndef LSEG_TILE_MINB
-#define LSEG_TILE_MINB 3
+#define LSEG_TILE_MINB 4
 #endif
 __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
                                                 const uint32_t* __restrict__ vbits, const int32_t* __restrict__ wpre,
@@ -168,10 +171,32 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
 #endif
   // dynamic shared memory (58 KB > the 48 KB static limit), see tile_smem_bytes()
   extern __shared__ __align__(16) unsigned char s_dyn[];
+#if LSEG_POS_RECOMPUTE
+  // ranges + separable direction tables; positions are rebuilt on use
+  // (5 multiplies) -- 19 KB less shared memory buys a 4th CTA per SM
+  double* s_r = reinterpret_cast<double*>(s_dyn);
+  double* s_ct = s_r + GR * GC;   // cos(elev) per halo row
+  double* s_st = s_ct + GR;       // sin(elev) per halo row
+  double* s_cp = s_st + GR;       // cos(az) per halo column
+  double* s_sp = s_cp + GC;       // sin(az) per halo column
+  double* s_nx = s_sp + GC;
+  double* s_px = s_r;  // dead after the normals: reused by the fused CC (union-find array)
+  auto posg = [&](int gi) -> Vec3 {
+    const int yy = gi / GC, xx = gi - yy * GC;
+    const double ct = s_ct[yy], r = s_r[gi];
+    Vec3 q;
+    q.x = __dmul_rn(__dmul_rn(ct, s_cp[xx]), r);
+    q.y = __dmul_rn(__dmul_rn(ct, s_sp[xx]), r);
+    q.z = __dmul_rn(s_st[yy], r);
+    return q;
+  };
+#else
   double* s_px = reinterpret_cast<double*>(s_dyn);
   double* s_py = s_px + GR * GC;
   double* s_pz = s_py + GR * GC;
   double* s_nx = s_pz + GR * GC;
+  auto posg = [&](int gi) -> Vec3 { return Vec3{s_px[gi], s_py[gi], s_pz[gi]}; };
+#endif
   double* s_ny = s_nx + NT;
   double* s_nz = s_ny + NT;
   int* s_id = reinterpret_cast<int*>(s_nz + NT);
@@ -224,13 +249,30 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       const int cc = wrapc(c0 - 1 + x, sh.Sk);
       const uint32_t bit = 1u << (cc & 31);
       const int id = (wv[j] & bit) ? pv[j] + __popc(wv[j] & (bit - 1u)) : -1;
+#if LSEG_POS_RECOMPUTE
+      s_r[e] = id >= 0 ? rv[j] : 0.0;
+#else
       Vec3 q = {0.0, 0.0, 0.0};
       if (id >= 0) q = cell_pos(sn, rr, cc * sh.k, rv[j]);
       s_px[e] = q.x;
       s_py[e] = q.y;
       s_pz[e] = q.z;
+#endif
       s_id[e] = id;
     }
+#if LSEG_POS_RECOMPUTE
+    for (int e = tid; e < GR + GC; e += T) {
+      if (e < GR) {
+        const int rr = min(max(r0 - 1 + e, 0), sh.R - 1);
+        s_ct[e] = __ldg(sn.cos_el + rr);
+        s_st[e] = __ldg(sn.sin_el + rr);
+      } else {
+        const int cc = wrapc(c0 - 1 + (e - GR), sh.Sk) * sh.k;
+        s_cp[e - GR] = __ldg(sn.cos_az + cc);
+        s_sp[e - GR] = __ldg(sn.sin_az + cc);
+      }
+    }
+#endif
   }
   __syncthreads();
   PH_MARK(1);
@@ -296,16 +338,17 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     const int e = s_list[i];
     const int y = e / TC, x = e - y * TC;
     const int g = (y + 1) * GC + (x + 1);
-    const Vec3 p = {s_px[g], s_py[g], s_pz[g]};
+    const Vec3 p = posg(g);
     double nv[3];
 #if LSEG_FAN6
     double vx[6], vy[6], vz[6];
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       const int gq = g + slot_dr(s) * GC + slot_dc(s);
-      vx[s] = __dsub_rn(s_px[gq], p.x);
-      vy[s] = __dsub_rn(s_py[gq], p.y);
-      vz[s] = __dsub_rn(s_pz[gq], p.z);
+      const Vec3 q = posg(gq);
+      vx[s] = __dsub_rn(q.x, p.x);
+      vy[s] = __dsub_rn(q.y, p.y);
+      vz[s] = __dsub_rn(q.z, p.z);
     }
     const bool okn = fan6(vx, vy, vz, p, nv);
 #else
@@ -315,7 +358,8 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       const int gq = g + slot_dr(s) * GC + slot_dc(s);
-      fan.add(__dsub_rn(s_px[gq], p.x), __dsub_rn(s_py[gq], p.y), __dsub_rn(s_pz[gq], p.z));
+      const Vec3 q = posg(gq);
+      fan.add(__dsub_rn(q.x, p.x), __dsub_rn(q.y, p.y), __dsub_rn(q.z, p.z));
     }
     const bool okn = fan.finish(p, nv);
 #endif
@@ -331,13 +375,14 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     const int y = e / TC, x = e - y * TC;
     const int g = (y + 1) * GC + (x + 1);
     const unsigned m = s_m[e];
-    const Vec3 p = {s_px[g], s_py[g], s_pz[g]};
+    const Vec3 p = posg(g);
     FanT<kFastMath> fan;
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       if (!((m >> s) & 1u)) continue;
       const int gq = g + slot_dr(s) * GC + slot_dc(s);
-      fan.add(__dsub_rn(s_px[gq], p.x), __dsub_rn(s_py[gq], p.y), __dsub_rn(s_pz[gq], p.z));
+      const Vec3 q = posg(gq);
+      fan.add(__dsub_rn(q.x, p.x), __dsub_rn(q.y, p.y), __dsub_rn(q.z, p.z));
     }
     double nv[3];
     if (fan.finish(p, nv)) {
@@ -1266,8 +1311,13 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
                         cudaStream_t st) {
   const int tilesC = (sh.Sk + TILE_C - 1) / TILE_C, tilesR = (sh.R + TILE_R - 1) / TILE_R;
   const int64_t nt = (int64_t)sh.F * tilesR * tilesC;
-  const size_t tsmem = (size_t)(3 * (TILE_R + 2) * (TILE_C + 2) + 3 * TILE_R * TILE_C) * 8 +
-                       (size_t)(TILE_R + 2) * (TILE_C + 2) * 4 + (size_t)TILE_R * TILE_C * 4;
+  const size_t tsmem =
+#if LSEG_POS_RECOMPUTE
+      (size_t)((TILE_R + 2) * (TILE_C + 2) + 2 * (TILE_R + 2) + 2 * (TILE_C + 2) + 3 * TILE_R * TILE_C) * 8 +
+#else
+      (size_t)(3 * (TILE_R + 2) * (TILE_C + 2) + 3 * TILE_R * TILE_C) * 8 +
+#endif
+      (size_t)(TILE_R + 2) * (TILE_C + 2) * 4 + (size_t)TILE_R * TILE_C * 4;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k_tile<TILE_R, TILE_C, TILE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
