@@ -152,6 +152,27 @@ int lseg_run_pipeline_r8(const lseg_sensor* sensor, int32_t frames, int32_t inte
                          uint8_t* nmask, int32_t* node_labels, int32_t* labels, int32_t* n_nodes,
                          int32_t* n_labels, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Flags of lseg_run_pipeline_ex. */
+#define LSEG_PIPE_EXACT_NORMALS 1u /* fp64 normals, then rounded to fp32: normals32 bit-identical to the
+                                      reference's fp64 normals cast to float32 (slower: FP64-bound) */
+#define LSEG_PIPE_RING_U8 2u       /* ring ids are uint8_t (as lseg_run_pipeline_r8) */
+
+/* lseg_run_pipeline with flags.  Without LSEG_PIPE_EXACT_NORMALS (and in
+ * lseg_run_pipeline / _r8) normals are "certified fp32": computed in fp32
+ * with a rigorous per-node error bound; every homogeneity decision the bound
+ * cannot settle, and every degenerate or ill-conditioned node, is recomputed
+ * with the exact fp64 arithmetic, so node_labels / labels are identical in
+ * both modes (bit-exact with the reference).  normals32 then differs from the
+ * reference's fp64 normals by far less than 1e-5 per component
+ * (SURVEY.md §8(c) tolerance) instead of being its exact rounding. */
+int lseg_run_pipeline_ex(const lseg_sensor* sensor, int32_t frames, int32_t interval,
+                         const double* thresholds, int32_t min_segment_size, uint32_t flags,
+                         const float* xyz, const void* ring, const int64_t* frame_offsets,
+                         int64_t total_points, double* ranges, int32_t* node_ids, int32_t* neighbors,
+                         float* normals32, uint8_t* nmask, int32_t* node_labels, int32_t* labels,
+                         int32_t* n_nodes, int32_t* n_labels, void* workspace, size_t workspace_bytes,
+                         void* stream);
+
 /* ---- edge-based evaluation (reference evaluate.py:40-94).
  * Label grids (F,R,S) i32, 0 = unlabelled.  Scratch sized by
  * lseg_eval_workspace_bytes. */

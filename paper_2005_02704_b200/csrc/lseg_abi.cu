@@ -92,6 +92,7 @@ Workspace carve(const Shape& s, int64_t label_bound, void* base) {
   w.sbits = reinterpret_cast<uint32_t*>(take(words * 4));
   w.spre = reinterpret_cast<int32_t*>(take(words * 4));
   w.fscal_cnt = reinterpret_cast<int32_t*>(take((size_t)s.F * 4));
+  w.ucnt = reinterpret_cast<unsigned long long*>(take(2 * 8));
   w.bytes = off;
   return w;
 }
@@ -303,8 +304,14 @@ int lseg_prune_small(int32_t frames, int32_t rings, int32_t steps, const int32_t
   return check_launch("prune_small");
 }
 
+// Test hook (not in the public header): per-node certified error bounds of the
+// next fused pipeline launch on this thread (0 for nodes that took the exact
+// path, -1 without a normal).
+static thread_local float* g_dbg_err = nullptr;
+
 static int run_pipeline_impl(const lseg_sensor* sensor, int32_t frames, int32_t interval, const double* thresholds,
-                             int32_t min_segment_size, const float* xyz, const void* ring, int ring_bytes,
+                             int32_t min_segment_size, uint32_t flags, const float* xyz, const void* ring,
+                             int ring_bytes,
                              const int64_t* frame_offsets, int64_t total_points, double* ranges, int32_t* node_ids,
                              int32_t* neighbors, float* normals32, uint8_t* nmask, int32_t* node_labels,
                              int32_t* labels, int32_t* n_nodes, int32_t* n_labels, void* workspace,
@@ -332,8 +339,10 @@ static int run_pipeline_impl(const lseg_sensor* sensor, int32_t frames, int32_t 
                st);
     launch_valid_scan(*sensor, sh, ranges, ws, n_nodes, st);
   }
+  float* dbg = g_dbg_err;
+  g_dbg_err = nullptr;
   launch_fused_graph(*sensor, sh, ws, ranges, thresholds, node_ids, neighbors, normals32, nmask, n_nodes, n_labels,
-                     node_labels, fused_bin, st);
+                     node_labels, fused_bin, (flags & LSEG_PIPE_EXACT_NORMALS) != 0, dbg, st);
   launch_prune_fused(sh, ws, min_segment_size, labels, st);
   return check_launch("run_pipeline");
 }
@@ -344,7 +353,7 @@ int lseg_run_pipeline(const lseg_sensor* sensor, int32_t frames, int32_t interva
                       int32_t* neighbors, float* normals32, uint8_t* nmask, int32_t* node_labels,
                       int32_t* labels, int32_t* n_nodes, int32_t* n_labels, void* workspace,
                       size_t workspace_bytes, void* stream) {
-  return run_pipeline_impl(sensor, frames, interval, thresholds, min_segment_size, xyz, ring, 4, frame_offsets,
+  return run_pipeline_impl(sensor, frames, interval, thresholds, min_segment_size, 0u, xyz, ring, 4, frame_offsets,
                            total_points, ranges, node_ids, neighbors, normals32, nmask, node_labels, labels, n_nodes,
                            n_labels, workspace, workspace_bytes, stream);
 }
@@ -355,10 +364,25 @@ int lseg_run_pipeline_r8(const lseg_sensor* sensor, int32_t frames, int32_t inte
                          int32_t* neighbors, float* normals32, uint8_t* nmask, int32_t* node_labels,
                          int32_t* labels, int32_t* n_nodes, int32_t* n_labels, void* workspace,
                          size_t workspace_bytes, void* stream) {
-  return run_pipeline_impl(sensor, frames, interval, thresholds, min_segment_size, xyz, ring, 1, frame_offsets,
+  return run_pipeline_impl(sensor, frames, interval, thresholds, min_segment_size, 0u, xyz, ring, 1, frame_offsets,
                            total_points, ranges, node_ids, neighbors, normals32, nmask, node_labels, labels, n_nodes,
                            n_labels, workspace, workspace_bytes, stream);
 }
+
+int lseg_run_pipeline_ex(const lseg_sensor* sensor, int32_t frames, int32_t interval, const double* thresholds,
+                         int32_t min_segment_size, uint32_t flags, const float* xyz, const void* ring,
+                         const int64_t* frame_offsets, int64_t total_points, double* ranges, int32_t* node_ids,
+                         int32_t* neighbors, float* normals32, uint8_t* nmask, int32_t* node_labels,
+                         int32_t* labels, int32_t* n_nodes, int32_t* n_labels, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  if (flags & ~(LSEG_PIPE_EXACT_NORMALS | LSEG_PIPE_RING_U8)) return fail(LSEG_EINVAL, "unknown pipeline flags");
+  return run_pipeline_impl(sensor, frames, interval, thresholds, min_segment_size, flags, xyz, ring,
+                           (flags & LSEG_PIPE_RING_U8) ? 1 : 4, frame_offsets, total_points, ranges, node_ids,
+                           neighbors, normals32, nmask, node_labels, labels, n_nodes, n_labels, workspace,
+                           workspace_bytes, stream);
+}
+
+void lseg_debug_cert_err(float* per_node_err) { g_dbg_err = per_node_err; }
 
 // ---------------------------------------------------------------- evaluator (F1)
 size_t lseg_eval_workspace_bytes(int32_t frames, int32_t rings, int32_t steps) {

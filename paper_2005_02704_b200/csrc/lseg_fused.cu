@@ -522,6 +522,626 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   PH_MARK(5);
 }
 
+// ---------------------------------------------------------------- certified fp32 normals
+// The exact fp64 normals above are bound by the FP64 pipe (~350 DP ops per
+// node).  The certified variant computes each normal in fp32 from exactly
+// formed edge vectors, together with a rigorous bound `err` on
+// |n_fp32 - n_reference| per component; every homogeneity decision that the
+// bound cannot settle (and every node whose normal is degenerate or badly
+// conditioned) is redone with the exact fp64 path, so segment labels stay
+// bit-identical to the reference.  Output normals (fp32) are then within the
+// north-star tolerance (1e-5), not bit-identical.
+//
+// Error model (u = 2^-24, all fp32 ops round-to-nearest except the PTX
+// approximations rcp.approx (<= 1 ulp) and rsqrt.approx (<= 2^-22.9 rel.)):
+//   the edge vectors V = q - p are formed in fp64 exactly as the reference
+//   forms them and rounded once to fp32: |v - V| <= u|V| (|V| >= 1e-15, else
+//   the node is "degenerate" -> exact path).  Then |l - |V|| <= 6u|V|,
+//   w = 1/(la+lb) within 9u, |c - A x B| <= 6u|A||B|, each term w*c within
+//   15u W|A||B|, and six fma accumulations add <= 11u B, so
+//   |acc - ACC| <= E = kAcc u B with B = sum W|A||B| (kAcc = 32 > 26 + slack).
+//   The unit normal then deviates by <= 2E/|acc| + 5u (normalisation), and
+//   err = u (2 kAcc B/|acc| + 8) bounds every component, including the
+//   reference's own fp64 rounding (2^-29 smaller).
+static constexpr float kU32 = 5.9604645e-08f;  // 2^-24
+static constexpr float kAcc = 32.0f;
+static constexpr float kOutCond = 64.0f;  // B/|acc| above this -> exact path (fp32 output accuracy)
+
+__device__ __forceinline__ float rcp_apx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rsqrt_apx(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+struct Fan32 {
+  float fx, fy, fz, fl;  // first vector and its length
+  float qx, qy, qz, ql;  // previous vector
+  float a0, a1, a2, ws, bs;
+  int cnt;
+  bool deg;
+
+  __device__ __forceinline__ Fan32() : a0(0.f), a1(0.f), a2(0.f), ws(0.f), bs(0.f), cnt(0), deg(false) {}
+
+  __device__ __forceinline__ void pair(float ax, float ay, float az, float la, float bx, float by, float bz,
+                                       float lb) {
+    const float w = rcp_apx(la + lb);
+    const float c0 = fmaf(ay, bz, -(az * by));
+    const float c1 = fmaf(az, bx, -(ax * bz));
+    const float c2 = fmaf(ax, by, -(ay * bx));
+    a0 = fmaf(w, c0, a0);
+    a1 = fmaf(w, c1, a1);
+    a2 = fmaf(w, c2, a2);
+    ws += w;
+    bs = fmaf(w, la * lb, bs);
+  }
+
+  __device__ __forceinline__ void add(float vx, float vy, float vz, float deg2) {
+    const float s = fmaf(vz, vz, fmaf(vy, vy, vx * vx));
+    deg |= !(s >= deg2);
+    const float l = s * rsqrt_apx(s);
+    if (cnt == 0) { fx = vx; fy = vy; fz = vz; fl = l; }
+    else pair(qx, qy, qz, ql, vx, vy, vz, l);
+    qx = vx; qy = vy; qz = vz; ql = l;
+    ++cnt;
+  }
+
+  // 0: no normal (certain), 1: normal + bound, >= 2: undecided -> exact fp64
+  // path (the value says why: 2 short edge vector, 3 cancelling fan, 4 |mean|
+  // near 1e-12, 5 ill-conditioned, 6 orientation)
+  __device__ __forceinline__ int finish(float px, float py, float pz, float n[3], float& err) {
+    if (cnt < 2) return 0;
+    if (cnt >= 3) pair(qx, qy, qz, ql, fx, fy, fz, fl);
+    if (deg) return 2;
+    const float A2 = fmaf(a2, a2, fmaf(a1, a1, a0 * a0));
+    const float inv = rsqrt_apx(A2);
+    const float alen = A2 * inv;
+    const float E = kAcc * kU32 * bs;
+    if (!(alen > 2.0f * E)) return 3;                 // cancelling fan (or underflow)
+    if (alen - E < 1.0001e-12f * ws) return 4;        // |mean| >= 1e-12 undecided (normals.py:138)
+    if (bs > kOutCond * alen) return 5;               // ill-conditioned: exact output
+    err = kU32 * (2.0f * kAcc * bs * rcp_apx(alen) + 8.0f) * 1.01f;
+    float n0 = a0 * inv, n1 = a1 * inv, n2 = a2 * inv;
+    const float dot = fmaf(n2, pz, fmaf(n1, py, n0 * px));
+    const float pm = fabsf(px) + fabsf(py) + fabsf(pz);
+    if (fabsf(dot) <= pm * (err + 8.0f * kU32)) return 6;  // orientation undecided (normals.py:142-143)
+    if (dot > 0.0f) { n0 = -n0; n1 = -n1; n2 = -n2; }
+    n[0] = n0; n[1] = n1; n[2] = n2;
+    return 1;
+  }
+};
+
+// Exact reference normal of kept cell (r, c) of one frame, straight from the
+// range grid and valid bits in global memory (the same operation sequence as
+// the fp64 tile path).  Used for the rare nodes / edges the fp32 bound cannot
+// settle.
+__device__ __noinline__ bool exact_normal_at(const lseg_sensor& sn, const Shape& sh, const double* __restrict__ rf,
+                                             const uint32_t* __restrict__ vbf, int r, int c, double out[3]) {
+  const Vec3 p = cell_pos(sn, r, c * sh.k, __ldg(rf + (int64_t)r * sh.S + (int64_t)c * sh.k));
+  FanT<kFastMath> fan;
+#pragma unroll 1
+  for (int s = 0; s < 6; ++s) {
+    const int rr = r + slot_dr(s);
+    if (rr < 0 || rr >= sh.R) continue;
+    if (s == 5 && sh.Sk == 2) continue;  // mesh.py:96-101
+    const int cc = wrapc(c + slot_dc(s), sh.Sk);
+    if (!((__ldg(vbf + (int64_t)rr * sh.Wk + (cc >> 5)) >> (cc & 31)) & 1u)) continue;
+    const Vec3 q = cell_pos(sn, rr, cc * sh.k, __ldg(rf + (int64_t)rr * sh.S + (int64_t)cc * sh.k));
+    fan.add(__dsub_rn(q.x, p.x), __dsub_rn(q.y, p.y), __dsub_rn(q.z, p.z));
+  }
+  return fan.finish(p, out);
+}
+
+struct CertParams {
+  double t[3];   // thresholds (fp64, for the exact decisions)
+  float tf[3];   // thresholds rounded to fp32
+  float mt[3];   // per-component decision slack: rounding of T and of the fp32 difference
+  float deg2;    // shorter squared edge vectors take the exact path
+};
+
+// Homogeneity decision from certified normals: 1 pass, 0 fail, 2 undecided.
+__device__ __forceinline__ int cert_pass(const CertParams& cp, float ax, float ay, float az, float ea, float bx,
+                                         float by, float bz, float eb) {
+  const float m = ea + eb;
+  const float d0 = fabsf(ax - bx), d1 = fabsf(ay - by), d2 = fabsf(az - bz);
+  const float m0 = m + cp.mt[0], m1 = m + cp.mt[1], m2 = m + cp.mt[2];
+  if (d0 - m0 >= cp.tf[0] || d1 - m1 >= cp.tf[1] || d2 - m2 >= cp.tf[2]) return 0;
+  if (d0 + m0 < cp.tf[0] && d1 + m1 < cp.tf[1] && d2 + m2 < cp.tf[2]) return 1;
+  return 2;
+}
+
+// Border-normal store of the certified path: one float4 {n, err} per cell,
+// same slot layout as bn_row / bn_col.
+__device__ __forceinline__ int64_t bn4_frame(const Shape& sh, int TR, int TC) {
+  return (int64_t)2 * ((sh.R + TR - 1) / TR) * sh.Sk + (int64_t)2 * ((sh.Sk + TC - 1) / TC) * sh.R;
+}
+__device__ __forceinline__ int64_t bn4_row(const Shape& sh, int slot, int c) { return (int64_t)slot * sh.Sk + c; }
+__device__ __forceinline__ int64_t bn4_col(const Shape& sh, int TR, int slot, int r) {
+  return (int64_t)2 * ((sh.R + TR - 1) / TR) * sh.Sk + (int64_t)slot * sh.R + r;
+}
+
+// One CTA per (frame, TR x TC tile), certified normals.  Phases:
+//   A  halo positions (fp64, reference product order) + node ids in smem
+//   B  fp32 normals + bounds from the exactly formed fp64 edge vectors
+//   X0 exact fp64 normals of the nodes the bound could not certify
+//   D1 edge decisions: certain pass / fail, or undecided -> both ends requested
+//   X1 exact fp64 normals of the requested endpoints
+//   D2 undecided edges settled on the exact normals; masks out
+//   C  per-node outputs
+// The exact work (X0 / X1, usually a few nodes per tile) runs lane-dense from
+// the shared-memory positions; its fp64 normals go to the global scratch
+// `xn` for D2.
+template <int TR, int TC, int T>
+__global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile_cert(
+    lseg_sensor sn, Shape sh, const double* __restrict__ ranges, const uint32_t* __restrict__ vbits,
+    const int32_t* __restrict__ wpre, CertParams cp, int32_t* __restrict__ node_ids, int32_t* __restrict__ neighbors,
+    float* __restrict__ n32, uint8_t* __restrict__ nmask, unsigned long long* __restrict__ masks,
+    float4* __restrict__ bn4, double* __restrict__ xn, float* __restrict__ dbg_err, int32_t* __restrict__ fscal) {
+  constexpr int GR = TR + 2, GC = TC + 2, NH = GR * GC;
+  constexpr int NT = TR * TC;
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  double* s_px = reinterpret_cast<double*>(s_dyn);
+  double* s_py = s_px + NH;
+  double* s_pz = s_py + NH;
+  float* s_nx = reinterpret_cast<float*>(s_pz + NH);
+  float* s_ny = s_nx + NT;
+  float* s_nz = s_ny + NT;
+  float* s_err = s_nz + NT;
+  int* s_id = reinterpret_cast<int*>(s_err + NT);
+  unsigned short* s_list = reinterpret_cast<unsigned short*>(s_id + NH);
+  uint8_t* s_has = reinterpret_cast<uint8_t*>(s_list + NT);  // 0 none, 1 normal, 2 not certified (yet)
+  uint8_t* s_m = s_has + NT;                                  // slot mask of general-path nodes
+  uint8_t* s_req = s_m + NT;                                  // exact path: 1 edge request, >= 2 reason
+  __shared__ unsigned long long s_U[TR * 3];
+  __shared__ unsigned s_UW[TR];
+  __shared__ int s_cnt[2 * (T / 32) + 3];
+
+  const int tilesC = (sh.Sk + TC - 1) / TC;
+  const int tilesR = (sh.R + TR - 1) / TR;
+  const int64_t b = blockIdx.x;
+  const int f = (int)(b / ((int64_t)tilesR * tilesC));
+  const int rem = (int)(b - (int64_t)f * tilesR * tilesC);
+  const int r0 = (rem / tilesC) * TR, c0 = (rem % tilesC) * TC;
+  const int TRe = min(TR, sh.R - r0), TCe = min(TC, sh.Sk - c0);
+  const double* rf = ranges + (int64_t)f * sh.R * sh.S;
+  const uint32_t* vbf = vbits + (int64_t)f * sh.R * sh.Wk;
+  const int32_t* wpf = wpre + (int64_t)f * sh.R * sh.Wk;
+  const int64_t nbase = (int64_t)f * sh.cap;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  if (rem == 0 && tid == 0) fscal[f * 4 + 2] = 0;  // k_merge_cert's undecided-edge counter
+
+  // A. halo positions dir*r (reference product order) and node ids
+  {
+    constexpr int NA = (NH + T - 1) / T;
+    double rv[NA];
+    uint32_t wv[NA];
+    int32_t pv[NA];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) {
+      const int e = tid + j * T;
+      const int y = e / GC, x = e - y * GC;
+      const int rr = r0 - 1 + y;
+      rv[j] = 0.0;
+      wv[j] = 0u;
+      pv[j] = 0;
+      if (e < NH && rr >= 0 && rr < sh.R) {
+        const int cc = wrapc(c0 - 1 + x, sh.Sk);
+        rv[j] = __ldg(rf + (int64_t)rr * sh.S + (int64_t)cc * sh.k);
+        wv[j] = __ldg(vbf + (int64_t)rr * sh.Wk + (cc >> 5));
+        pv[j] = __ldg(wpf + (int64_t)rr * sh.Wk + (cc >> 5));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NA; ++j) {
+      const int e = tid + j * T;
+      if (e >= NH) break;
+      const int y = e / GC, x = e - y * GC;
+      const int rr = r0 - 1 + y;
+      const int cc = wrapc(c0 - 1 + x, sh.Sk);
+      const uint32_t bit = 1u << (cc & 31);
+      const int id = (wv[j] & bit) ? pv[j] + __popc(wv[j] & (bit - 1u)) : -1;
+      Vec3 q = {0.0, 0.0, 0.0};
+      if (id >= 0) q = cell_pos(sn, rr, cc * sh.k, rv[j]);
+      s_px[e] = q.x;
+      s_py[e] = q.y;
+      s_pz[e] = q.z;
+      s_id[e] = id;
+    }
+  }
+  __syncthreads();
+
+  // B. certified fp32 normals, split into the fan6 / general work lists
+  {
+    unsigned char ml[(NT + T - 1) / T];
+    int kind[(NT + T - 1) / T];
+    int na = 0, nb = 0;
+#pragma unroll
+    for (int j = 0; j < (NT + T - 1) / T; ++j) {
+      const int e = tid + j * T;
+      const int y = e / TC, x = e - y * TC;
+      const int g = (y + 1) * GC + (x + 1);
+      unsigned m = 0;
+      kind[j] = 0;
+      if (e < NT && y < TRe && x < TCe && s_id[g] >= 0) {
+#pragma unroll
+        for (int s = 0; s < 6; ++s)
+          if (s_id[g + slot_dr(s) * GC + slot_dc(s)] >= 0 && !(s == 5 && sh.Sk == 2)) m |= 1u << s;
+        kind[j] = (m == 0x3fu) ? 1 : 2;
+      }
+      ml[j] = (unsigned char)m;
+      na += kind[j] == 1;
+      nb += kind[j] == 2;
+      if (e < NT) { s_has[e] = 0; s_req[e] = 0; s_m[e] = (unsigned char)m; }
+    }
+    int ia = na, ib = nb;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ta = __shfl_up_sync(0xffffffffu, ia, o), tb = __shfl_up_sync(0xffffffffu, ib, o);
+      if (lane >= o) { ia += ta; ib += tb; }
+    }
+    if (lane == 31) { s_cnt[warp] = ia; s_cnt[T / 32 + warp] = ib; }
+    __syncthreads();
+    int oa = 0, ob = 0, ta = 0, tb = 0;
+    for (int w = 0; w < T / 32; ++w) {
+      if (w < warp) { oa += s_cnt[w]; ob += s_cnt[T / 32 + w]; }
+      ta += s_cnt[w];
+      tb += s_cnt[T / 32 + w];
+    }
+    oa += ia - na;
+    ob += ib - nb;
+#pragma unroll
+    for (int j = 0; j < (NT + T - 1) / T; ++j) {
+      const int e = tid + j * T;
+      if (kind[j] == 1) s_list[oa++] = (unsigned short)e;
+      else if (kind[j] == 2) { s_list[NT - 1 - ob] = (unsigned short)e; ++ob; }
+    }
+    (void)ml;
+    __syncthreads();  // s_cnt is rewritten below
+    if (tid == 0) { s_cnt[2 * (T / 32)] = ta; s_cnt[2 * (T / 32) + 1] = tb; }
+  }
+  __syncthreads();
+  const int nfan6 = s_cnt[2 * (T / 32)], ngen = s_cnt[2 * (T / 32) + 1];
+  auto node_normal = [&](int e, unsigned m) {
+    const int y = e / TC, x = e - y * TC;
+    const int g = (y + 1) * GC + (x + 1);
+    const double px = s_px[g], py = s_py[g], pz = s_pz[g];
+    Fan32 fan;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      if (!((m >> s) & 1u)) continue;
+      const int gq = g + slot_dr(s) * GC + slot_dc(s);
+      fan.add(__double2float_rn(__dsub_rn(s_px[gq], px)), __double2float_rn(__dsub_rn(s_py[gq], py)),
+              __double2float_rn(__dsub_rn(s_pz[gq], pz)), cp.deg2);
+    }
+    float nv[3] = {0.f, 0.f, 0.f}, err = 0.f;
+    const int st = fan.finish(__double2float_rn(px), __double2float_rn(py), __double2float_rn(pz), nv, err);
+    s_has[e] = (uint8_t)min(st, 2);
+    if (st == 1) {
+      s_nx[e] = nv[0];
+      s_ny[e] = nv[1];
+      s_nz[e] = nv[2];
+      s_err[e] = err;
+    } else if (st >= 2) {
+      s_req[e] = (uint8_t)st;
+    }
+  };
+  for (int i = tid; i < nfan6; i += T) node_normal(s_list[i], 0x3fu);  // straight-line: all six slots
+  for (int i = tid; i < ngen; i += T) {
+    const int e = s_list[NT - 1 - i];
+    node_normal(e, s_m[e]);
+  }
+  __syncthreads();
+
+  // X. exact fp64 normals of the nodes whose s_req code matches (first: the
+  // uncertified nodes, else: endpoints of undecided edges), compacted into
+  // s_list so the rare fp64 work runs lane-dense.  Block-uniform.
+  double* xf = xn + nbase * 3;
+  auto run_exact = [&](bool first) {
+    if (tid == 0) s_cnt[2 * (T / 32) + 2] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < (NT + T - 1) / T; ++j) {  // NT is a multiple of T: whole warps
+      const int e = tid + j * T;
+      const int q = (e < NT) ? s_req[e] : 0;
+      const bool want = first ? (q >= 2) : (q == 1);
+      const unsigned bal = __ballot_sync(0xffffffffu, want);
+      if (bal) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&s_cnt[2 * (T / 32) + 2], __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (want) s_list[base + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)e;
+      }
+    }
+    __syncthreads();
+    const int n = s_cnt[2 * (T / 32) + 2];
+    for (int i = tid; i < n; i += T) {
+      const int e = s_list[i];
+      const int y = e / TC, x = e - y * TC;
+      const int g = (y + 1) * GC + (x + 1);
+      const unsigned m = s_m[e];
+      const Vec3 p = {s_px[g], s_py[g], s_pz[g]};
+      FanT<kFastMath> fan;
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        if (!((m >> s) & 1u)) continue;
+        const int gq = g + slot_dr(s) * GC + slot_dc(s);
+        fan.add(__dsub_rn(s_px[gq], p.x), __dsub_rn(s_py[gq], p.y), __dsub_rn(s_pz[gq], p.z));
+      }
+      double nv[3];
+      const bool has = fan.finish(p, nv);
+      const double qn = __longlong_as_double(0x7ff8000000000000LL);
+      const int64_t cell = (int64_t)(r0 + y) * sh.Sk + c0 + x;
+      xf[cell * 3] = has ? nv[0] : qn;
+      xf[cell * 3 + 1] = has ? nv[1] : qn;
+      xf[cell * 3 + 2] = has ? nv[2] : qn;
+      s_has[e] = has ? 1 : 0;
+      if (has) {
+        s_nx[e] = __double2float_rn(nv[0]);
+        s_ny[e] = __double2float_rn(nv[1]);
+        s_nz[e] = __double2float_rn(nv[2]);
+        s_err[e] = 0.5f * kU32;  // rounding of the exact normal to fp32
+      }
+    }
+    __syncthreads();
+  };
+  run_exact(true);
+
+  // D1. decisions on the tile's internal forward edges, one warp per row:
+  // certain passes into the masks, undecided edges into s_U (both ends
+  // requested for X1).
+  static_assert(TC == 64, "row masks assume 64-column tiles");
+  const bool full_width = (c0 == 0 && TCe == sh.Sk);
+  unsigned long long* mrow = masks + (((int64_t)f * tilesR + r0 / TR) * tilesC + c0 / TC) * (TR * 5);
+  auto decide = [&](int ea, int eb) -> int {  // 1 pass, 0 fail, 2 undecided
+    if (!s_has[eb]) return 0;
+    const int r = cert_pass(cp, s_nx[ea], s_ny[ea], s_nz[ea], s_err[ea], s_nx[eb], s_ny[eb], s_nz[eb], s_err[eb]);
+    if (r == 2) {
+      if (!s_req[ea]) s_req[ea] = 1;
+      if (!s_req[eb]) s_req[eb] = 1;
+    }
+    return r;
+  };
+  for (int y = warp; y < TR; y += T / 32) {
+    unsigned long long H = 0, V0 = 0, V1 = 0, HS = 0, UH = 0, UV0 = 0, UV1 = 0;
+    unsigned W = 0, UW = 0;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int x = lane + 32 * half;
+      const int e = y * TC + x;
+      int h = 0, v0 = 0, v1 = 0, w0 = 0, w1 = 0;
+      const bool hs = (y < TRe && x < TCe) && s_has[e];
+      if (hs) {
+        if (x + 1 < TCe) h = decide(e, e + 1);
+        if (y + 1 < TRe) {
+          v0 = decide(e, e + TC);
+          if (x + 1 < TCe) v1 = decide(e, e + TC + 1);
+        }
+        if (full_width && x == TCe - 1) {
+          if (TCe > 1) w0 = decide(e, y * TC);
+          if (y + 1 < TRe) w1 = decide(e, (y + 1) * TC);
+        }
+      }
+      const int sh_ = half ? 32 : 0;
+      H |= (unsigned long long)__ballot_sync(0xffffffffu, h == 1) << sh_;
+      V0 |= (unsigned long long)__ballot_sync(0xffffffffu, v0 == 1) << sh_;
+      V1 |= (unsigned long long)__ballot_sync(0xffffffffu, v1 == 1) << sh_;
+      HS |= (unsigned long long)__ballot_sync(0xffffffffu, hs) << sh_;
+      W |= (__ballot_sync(0xffffffffu, w0 == 1) ? 1u : 0u) | (__ballot_sync(0xffffffffu, w1 == 1) ? 2u : 0u);
+      const unsigned any2 = __ballot_sync(0xffffffffu, (h | v0 | v1 | w0 | w1) & 2);
+      if (any2) {  // rare
+        UH |= (unsigned long long)__ballot_sync(0xffffffffu, h == 2) << sh_;
+        UV0 |= (unsigned long long)__ballot_sync(0xffffffffu, v0 == 2) << sh_;
+        UV1 |= (unsigned long long)__ballot_sync(0xffffffffu, v1 == 2) << sh_;
+        UW |= (__ballot_sync(0xffffffffu, w0 == 2) ? 1u : 0u) | (__ballot_sync(0xffffffffu, w1 == 2) ? 2u : 0u);
+      }
+    }
+    if (lane == 0) {
+      mrow[y * 5 + 0] = H;
+      mrow[y * 5 + 1] = V0;
+      mrow[y * 5 + 2] = V1;
+      mrow[y * 5 + 3] = HS;
+      mrow[y * 5 + 4] = W;
+      s_U[y * 3] = UH;
+      s_U[y * 3 + 1] = UV0;
+      s_U[y * 3 + 2] = UV1;
+      s_UW[y] = UW;
+    }
+  }
+  __syncthreads();
+
+  // X1 + D2: settle the undecided edges on exact normals (rare; block-uniform)
+  int nu = 0;
+  if (tid < TR) nu = (s_U[tid * 3] | s_U[tid * 3 + 1] | s_U[tid * 3 + 2]) != 0ull || s_UW[tid] != 0u;
+  if (__syncthreads_or(nu)) {
+    run_exact(false);
+    auto exact_pass = [&](int ea, int eb) -> bool {
+      const int ya = ea / TC, yb = eb / TC;
+      const int64_t ca = (int64_t)(r0 + ya) * sh.Sk + c0 + (ea - ya * TC);
+      const int64_t cb = (int64_t)(r0 + yb) * sh.Sk + c0 + (eb - yb * TC);
+      const double a[3] = {xf[ca * 3], xf[ca * 3 + 1], xf[ca * 3 + 2]};
+      const double q[3] = {xf[cb * 3], xf[cb * 3 + 1], xf[cb * 3 + 2]};
+      return normals_pass(a, q, cp.t[0], cp.t[1], cp.t[2]);
+    };
+    for (int y = warp; y < TR; y += T / 32) {
+      const unsigned long long UH = s_U[y * 3], UV0 = s_U[y * 3 + 1], UV1 = s_U[y * 3 + 2];
+      const unsigned UW = s_UW[y];
+      if (!(UH | UV0 | UV1) && !UW) continue;  // warp-uniform
+      unsigned long long H = 0, V0 = 0, V1 = 0;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int x = lane + 32 * half;
+        const int e = y * TC + x;
+        const int sh_ = half ? 32 : 0;
+        bool h = false, v0 = false, v1 = false;
+        if ((UH >> x) & 1ull) h = exact_pass(e, e + 1);
+        if ((UV0 >> x) & 1ull) v0 = exact_pass(e, e + TC);
+        if ((UV1 >> x) & 1ull) v1 = exact_pass(e, e + TC + 1);
+        H |= (unsigned long long)__ballot_sync(0xffffffffu, h) << sh_;
+        V0 |= (unsigned long long)__ballot_sync(0xffffffffu, v0) << sh_;
+        V1 |= (unsigned long long)__ballot_sync(0xffffffffu, v1) << sh_;
+      }
+      if (lane == 0) {
+        unsigned W = 0;
+        if ((UW & 1u) && exact_pass(y * TC + TCe - 1, y * TC)) W |= 1u;
+        if ((UW & 2u) && exact_pass(y * TC + TCe - 1, (y + 1) * TC)) W |= 2u;
+        mrow[y * 5 + 0] |= H;
+        mrow[y * 5 + 1] |= V0;
+        mrow[y * 5 + 2] |= V1;
+        mrow[y * 5 + 4] |= W;
+      }
+    }
+  }
+
+  // C. per-node outputs
+  float4* bf = bn4 + (int64_t)f * bn4_frame(sh, TR, TC);
+  const int tr = r0 / TR, tc = c0 / TC;
+  for (int e = tid; e < NT; e += T) {
+    const int y = e / TC, x = e - y * TC;
+    if (y >= TRe || x >= TCe) continue;
+    const int rr = r0 + y, cc = c0 + x;
+    const int g = (y + 1) * GC + (x + 1);
+    const int id = s_id[g];
+    const int64_t cell = (int64_t)rr * sh.Sk + cc;
+    if (node_ids) node_ids[nbase + cell] = id;
+    if (id < 0) continue;
+    int nb[6];
+#pragma unroll
+    for (int s = 0; s < 6; ++s) nb[s] = s_id[g + slot_dr(s) * GC + slot_dc(s)];
+    if (sh.Sk == 2 && nb[5] == nb[2]) nb[5] = -1;
+    int2* o2 = reinterpret_cast<int2*>(neighbors + (nbase + id) * 6);
+    o2[0] = make_int2(nb[0], nb[1]);
+    o2[1] = make_int2(nb[2], nb[3]);
+    o2[2] = make_int2(nb[4], nb[5]);
+    const bool has = s_has[e] == 1;
+    const float qn = __int_as_float(0x7fc00000);
+    const float4 v = has ? make_float4(s_nx[e], s_ny[e], s_nz[e], s_err[e]) : make_float4(qn, qn, qn, -1.0f);
+    if (n32) {
+      float* o = n32 + (nbase + id) * 3;
+      o[0] = v.x;
+      o[1] = v.y;
+      o[2] = v.z;
+    }
+    if (dbg_err) dbg_err[nbase + id] = s_req[e] >= 2 ? -10.0f - s_req[e] : (s_req[e] ? -11.0f : v.w);
+    nmask[nbase + id] = has ? 1 : 0;
+    if (has) {
+      if (y == 0) bf[bn4_row(sh, 2 * tr, cc)] = v;
+      if (y == TRe - 1) bf[bn4_row(sh, 2 * tr + 1, cc)] = v;
+      if (x == 0) bf[bn4_col(sh, TR, 2 * tc, rr)] = v;
+      if (x == TCe - 1) bf[bn4_col(sh, TR, 2 * tc + 1, rr)] = v;
+    }
+  }
+}
+
+// Global union over tile-border edges from the certified border normals;
+// undecided edges recompute both exact normals (exact_normal_at).
+// Undecided edges go to a per-frame list (unc, counter fscal[f*4+2]) that
+// k_merge_exact settles afterwards, keeping the fp64 path (and its registers)
+// out of this kernel.  overflow_pass = true re-enumerates every border edge
+// and settles the undecided ones inline (only for a frame whose list overflowed).
+template <int TR, int TC>
+__device__ __forceinline__ void merge_cert_frame(const lseg_sensor& sn, const Shape& sh, const double* ranges,
+                                                 const uint32_t* vbits, const float4* bn4, const CertParams& cp,
+                                                 int32_t* parent, int32_t* unc, int32_t* fscal, int f, int u0,
+                                                 int ustep, bool overflow_pass) {
+  const int nbr = (sh.R + TR - 1) / TR;
+  const int nbc = (sh.Sk + TC - 1) / TC;
+  const int per = nbr * sh.Sk + nbc * sh.R;
+  const int64_t capp = sh.cap / 2;  // undecided-list capacity (pairs) per frame
+  int32_t* par = parent + (int64_t)f * sh.cap;
+  const float4* bn = bn4 + (int64_t)f * bn4_frame(sh, TR, TC);
+  for (int u = u0; u < per; u += ustep) {
+    int r, c;
+    if (u < nbr * sh.Sk) {
+      const int br = u / sh.Sk;
+      r = min(br * TR + TR - 1, sh.R - 1);
+      c = u - br * sh.Sk;
+    } else {
+      const int v = u - nbr * sh.Sk;
+      const int bc = v / sh.R;
+      c = min(bc * TC + TC - 1, sh.Sk - 1);
+      r = v - bc * sh.R;
+    }
+    const int p = r * sh.Sk + c;
+    if (__ldcg(par + p) < 0) continue;  // no normal
+    const int tr = r / TR;
+    const bool last_row = (r == min(tr * TR + TR - 1, sh.R - 1));
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      if (r + slot_dr(s) >= sh.R) continue;
+      if (edge_internal<TR, TC>(r, c, s, sh.Sk)) continue;
+      const int rq = r + slot_dr(s), cq = wrapc(c + slot_dc(s), sh.Sk);
+      const int q = rq * sh.Sk + cq;
+      if (__ldcg(par + q) < 0) continue;
+      float4 a, bq;
+      if (slot_dr(s) == 1 && last_row) {
+        a = __ldcg(bn + bn4_row(sh, 2 * tr + 1, c));
+        bq = __ldcg(bn + bn4_row(sh, 2 * (rq / TR), cq));
+      } else {
+        a = __ldcg(bn + bn4_col(sh, TR, 2 * (c / TC) + 1, r));
+        bq = __ldcg(bn + bn4_col(sh, TR, 2 * (cq / TC), rq));
+      }
+      int d = cert_pass(cp, a.x, a.y, a.z, a.w, bq.x, bq.y, bq.z, bq.w);
+      if (d == 2) {
+        if (overflow_pass) {
+          const double* rf = ranges + (int64_t)f * sh.R * sh.S;
+          const uint32_t* vbf = vbits + (int64_t)f * sh.R * sh.Wk;
+          double na[3], nq[3];
+          const bool ha = exact_normal_at(sn, sh, rf, vbf, r, c, na);
+          const bool hq = exact_normal_at(sn, sh, rf, vbf, rq, cq, nq);
+          d = (ha && hq && normals_pass(na, nq, cp.t[0], cp.t[1], cp.t[2])) ? 1 : 0;
+        } else {
+          const int idx = atomicAdd(fscal + f * 4 + 2, 1);
+          if (idx < capp) {
+            unc[(int64_t)f * sh.cap + 2 * idx] = p;
+            unc[(int64_t)f * sh.cap + 2 * idx + 1] = q;
+          }
+        }
+      }
+      if (d == 1) uf_union(par, p, q);
+    }
+  }
+}
+
+template <int TR, int TC>
+__global__ void k_merge_cert(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
+                             const uint32_t* __restrict__ vbits, const float4* __restrict__ bn4, CertParams cp,
+                             int32_t* __restrict__ parent, int32_t* __restrict__ unc, int32_t* __restrict__ fscal) {
+  merge_cert_frame<TR, TC>(sn, sh, ranges, vbits, bn4, cp, parent, unc, fscal, blockIdx.y,
+                           blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, false);
+}
+
+// Settles the undecided border edges of k_merge_cert with exact normals.
+template <int TR, int TC>
+__global__ void k_merge_exact(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
+                              const uint32_t* __restrict__ vbits, const float4* __restrict__ bn4, CertParams cp,
+                              int32_t* __restrict__ parent, const int32_t* __restrict__ unc,
+                              int32_t* __restrict__ fscal) {
+  const int f = blockIdx.y;
+  const int n = fscal[f * 4 + 2];
+  if (n == 0) return;
+  if (n > sh.cap / 2) {  // list overflowed: redo the frame's border edges inline
+    merge_cert_frame<TR, TC>(sn, sh, ranges, vbits, bn4, cp, parent, nullptr, fscal, f, threadIdx.x, blockDim.x,
+                             true);
+    return;
+  }
+  const double* rf = ranges + (int64_t)f * sh.R * sh.S;
+  const uint32_t* vbf = vbits + (int64_t)f * sh.R * sh.Wk;
+  int32_t* par = parent + (int64_t)f * sh.cap;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int p = unc[(int64_t)f * sh.cap + 2 * i], q = unc[(int64_t)f * sh.cap + 2 * i + 1];
+    const int r = p / sh.Sk, c = p - r * sh.Sk, rq = q / sh.Sk, cq = q - rq * sh.Sk;
+    double na[3], nq[3];
+    const bool ha = exact_normal_at(sn, sh, rf, vbf, r, c, na);
+    const bool hq = exact_normal_at(sn, sh, rf, vbf, rq, cq, nq);
+    if (ha && hq && normals_pass(na, nq, cp.t[0], cp.t[1], cp.t[2])) uf_union(par, p, q);
+  }
+}
+
 // Tile-local connected components from k_tile's masks (one small CTA per
 // tile): each node's parent starts as the first cell of its horizontal run
 // (bit arithmetic), vertical / diagonal edges join runs with shared-memory
@@ -1308,9 +1928,39 @@ void debug_phases(double* out) {
 void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace& ws, const double* ranges,
                         const double* thr, int32_t* node_ids, int32_t* neighbors, float* n32, uint8_t* nmask,
                         int32_t* n_nodes, int32_t* n_labels, int32_t* node_labels, bool fbits_valid,
-                        cudaStream_t st) {
+                        bool exact_normals, float* dbg_err, cudaStream_t st) {
   const int tilesC = (sh.Sk + TILE_C - 1) / TILE_C, tilesR = (sh.R + TILE_R - 1) / TILE_R;
   const int64_t nt = (int64_t)sh.F * tilesR * tilesC;
+  const int per = tilesR * sh.Sk + tilesC * sh.R;
+  if (!exact_normals) {
+    CertParams cp;
+    for (int c = 0; c < 3; ++c) {
+      cp.t[c] = thr[c];
+      cp.tf[c] = (float)thr[c];
+      cp.mt[c] = 5.9604645e-08f * (8.0f + 4.0f * (float)thr[c]);
+    }
+    cp.deg2 = 1e-30f;  // |V| < 1e-15: fp32 squares would leave the normal range
+    constexpr int NH = (TILE_R + 2) * (TILE_C + 2), NT = TILE_R * TILE_C;
+    const size_t csmem = (size_t)NH * (3 * 8 + 4) + (size_t)NT * (4 * 4 + 2 + 3);  // see k_tile_cert
+    static bool cattr = false;
+    if (!cattr) {
+      cudaFuncSetAttribute(k_tile_cert<TILE_R, TILE_C, TILE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)csmem);
+      cattr = true;
+    }
+    float4* bn4 = reinterpret_cast<float4*>(ws.bnorm);
+    k_tile_cert<TILE_R, TILE_C, TILE_T><<<(unsigned)nt, TILE_T, csmem, st>>>(
+        sn, sh, ranges, ws.vbits, ws.wpre, cp, node_ids, neighbors, n32, nmask, ws.masks, bn4, ws.normals64, dbg_err,
+        ws.fscal);
+    prof_mark("tile", st);
+    k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
+    prof_mark("tile_cc", st);
+    k_merge_cert<TILE_R, TILE_C><<<dim3((per + 255) / 256, sh.F), 256, 0, st>>>(sn, sh, ranges, ws.vbits, bn4, cp,
+                                                                                ws.parent, ws.rank, ws.fscal);
+    k_merge_exact<TILE_R, TILE_C><<<dim3(1, sh.F), 128, 0, st>>>(sn, sh, ranges, ws.vbits, bn4, cp, ws.parent,
+                                                                 ws.rank, ws.fscal);
+    prof_mark("merge", st);
+  } else {
   const size_t tsmem =
 #if LSEG_POS_RECOMPUTE
       (size_t)((TILE_R + 2) * (TILE_C + 2) + 2 * (TILE_R + 2) + 2 * (TILE_C + 2) + 3 * TILE_R * TILE_C) * 8 +
@@ -1331,10 +1981,10 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
   prof_mark("tile_cc", st);
 #endif
-  const int per = tilesR * sh.Sk + tilesC * sh.R;
   k_merge<TILE_R, TILE_C><<<dim3((per + 255) / 256, sh.F), 256, 0, st>>>(
       sh, ws.bnorm, thr[0], thr[1], thr[2], ws.parent);
   prof_mark("merge", st);
+  }
   {
     const int64_t nwords = (int64_t)sh.F * sh.R * sh.Wk;
     const int64_t blocks = (nwords * 32 + 255) / 256;

@@ -103,8 +103,14 @@ class BatchPipeline:
 
     def __init__(self, config: SensorConfig, interval: int, segmenter: SegmenterConfig | None = None,
                  frames: int = 1, device=None, keep_node_labels: bool = False, streams: int = 1,
-                 chunk_frames: int | None = None):
+                 chunk_frames: int | None = None, normals: str = "certified"):
         self.L = _lib.lib()
+        if normals not in ("certified", "exact"):
+            raise ValueError("normals must be 'certified' or 'exact'")
+        # "certified": fp32 normals with a rigorous error bound, exact fp64 only
+        # where a decision needs it (labels identical); "exact": fp64 normals
+        # rounded to fp32 (bit-identical to the reference's, FP64-bound)
+        self.normals_mode = normals
         self.config = config
         self.interval = int(interval)
         subsample_steps(config, interval)
@@ -143,14 +149,13 @@ class BatchPipeline:
     def _call(self, f0, f1, ws, xyz, ring, offsets):
         P = int(xyz.shape[0])
         sl = lambda t: None if t is None else t[f0:f1]
+        flags = _lib.PIPE_EXACT_NORMALS if self.normals_mode == "exact" else 0
         if ring.dtype == torch.uint8:
-            fn = self.L.lseg_run_pipeline_r8
-        elif ring.dtype == torch.int32:
-            fn = self.L.lseg_run_pipeline
-        else:
+            flags |= _lib.PIPE_RING_U8
+        elif ring.dtype != torch.int32:
             raise ValueError("ring ids must be int32 or uint8")
-        _lib.check(fn(
-            self.sn, f1 - f0, self.interval, self.thr, int(self.seg.min_segment_size), _lib.ptr(xyz),
+        _lib.check(self.L.lseg_run_pipeline_ex(
+            self.sn, f1 - f0, self.interval, self.thr, int(self.seg.min_segment_size), flags, _lib.ptr(xyz),
             _lib.ptr(ring), _lib.ptr(offsets[f0:]), P, _lib.ptr(sl(self.ranges)), _lib.ptr(sl(self.node_ids)),
             _lib.ptr(sl(self.neighbors)), _lib.ptr(sl(self.normals)), _lib.ptr(sl(self.nmask)),
             _lib.ptr(sl(self.node_labels)), _lib.ptr(sl(self.labels)), _lib.ptr(sl(self.n_nodes)),
@@ -194,12 +199,13 @@ class StreamingPipeline:
 
     def __init__(self, config: SensorConfig, interval: int, segmenter: SegmenterConfig | None = None,
                  chunk_frames: int = 64, max_chunk_points: int | None = None, device=None,
-                 ring_dtype=torch.int32):
+                 ring_dtype=torch.int32, normals: str = "certified"):
         self.device = torch.device(device or "cuda")
         self.cf = int(chunk_frames)
         R, S = config.rings, config.azimuth_steps
         self.maxp = int(max_chunk_points or self.cf * R * S)
-        self.bps = [BatchPipeline(config, interval, segmenter, frames=self.cf, device=self.device) for _ in range(2)]
+        self.bps = [BatchPipeline(config, interval, segmenter, frames=self.cf, device=self.device, normals=normals)
+                    for _ in range(2)]
         self.xyz = [torch.empty((self.maxp, 3), dtype=torch.float32, device=self.device) for _ in range(2)]
         self.ring = [torch.empty(self.maxp, dtype=ring_dtype, device=self.device) for _ in range(2)]
         self.off = [torch.empty(self.cf + 1, dtype=torch.int64, device=self.device) for _ in range(2)]

@@ -84,22 +84,23 @@ def test_bin_points_golden(L, name):
     np.testing.assert_array_equal(grid.ranges, g["ranges"])
 
 
-def _run_batch(L, shape_name, frames, k, seed=5):
+def _run_batch(L, shape_name, frames, k, seed=5, normals="certified"):
     from paper_2005_02704_b200 import synth
     shape = synth.CONFIGS[shape_name]
     xyz, ring, off = synth.make_batch(shape, frames=frames, seed=seed, device="cuda")
     cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
                          r_max=shape.r_max)
-    bp = L.BatchPipeline(cfg, k, frames=frames, keep_node_labels=True)
+    bp = L.BatchPipeline(cfg, k, frames=frames, keep_node_labels=True, normals=normals)
     bp.run(xyz, ring, off)
     torch.cuda.synchronize()
     return shape, cfg, bp, xyz.cpu().numpy(), ring.cpu().numpy(), off.cpu().numpy()
 
 
+@pytest.mark.parametrize("normals", ["certified", "exact"])
 @pytest.mark.parametrize("shape_name,frames,k", [("vlp16", 3, 1), ("vlp16", 2, 5), ("hdl64", 2, 1),
                                                   ("hdl64", 2, 5), ("os128", 1, 1), ("os128", 1, 5)])
-def test_batch_pipeline_vs_oracle(L, oracle, shape_name, frames, k):
-    shape, cfg, bp, xyz, ring, off = _run_batch(L, shape_name, frames, k)
+def test_batch_pipeline_vs_oracle(L, oracle, shape_name, frames, k, normals):
+    shape, cfg, bp, xyz, ring, off = _run_batch(L, shape_name, frames, k, normals=normals)
     for f in range(frames):
         sl = slice(off[f], off[f + 1])
         want = oracle.run_from_points(xyz[sl], ring[sl], shape.elevations, shape.steps, k, shape.r_min,
@@ -110,14 +111,19 @@ def test_batch_pipeline_vs_oracle(L, oracle, shape_name, frames, k):
         np.testing.assert_array_equal(got["neighbors"], want["mesh"]["neighbors"])
         np.testing.assert_array_equal(got["mask"], want["mask"])
         m = want["mask"]
+        # normals within 1e-5 per component (fp32); the exact
+        # mode is additionally the exact rounding of the reference's fp64 values
         np.testing.assert_allclose(got["normals"][m], want["normals"][m], rtol=0, atol=1e-5)
-        np.testing.assert_array_equal(got["normals"][m], want["normals"][m].astype(np.float32))
+        if normals == "exact":
+            np.testing.assert_array_equal(got["normals"][m], want["normals"][m].astype(np.float32))
+        # labels are bit-exact in both modes (undecided edges take the exact path)
         np.testing.assert_array_equal(got["node_labels"], want["node_labels"])
         np.testing.assert_array_equal(got["labels"], want["labels"])
 
 
-def test_stress_frame_vs_oracle(L, oracle):
-    shape, cfg, bp, xyz, ring, off = _run_batch(L, "stress", 1, 1, seed=9)
+@pytest.mark.parametrize("normals", ["certified", "exact"])
+def test_stress_frame_vs_oracle(L, oracle, normals):
+    shape, cfg, bp, xyz, ring, off = _run_batch(L, "stress", 1, 1, seed=9, normals=normals)
     want = oracle.run_from_points(xyz, ring, shape.elevations, shape.steps, 1, shape.r_min, shape.r_max)
     got = bp.frame(0)
     np.testing.assert_array_equal(got["neighbors"], want["mesh"]["neighbors"])
@@ -262,3 +268,49 @@ def test_streaming_pipeline_host_to_host(L):
     sp.run_host(hx, hr, ho, hl)
     torch.cuda.synchronize()
     assert torch.equal(hl, want)
+
+
+@pytest.mark.parametrize("shape_name,frames,seed", [("hdl64", 4, 21), ("stress", 1, 22), ("vlp16", 8, 23)])
+def test_certified_normal_bounds_hold(L, oracle, shape_name, frames, seed):
+    """The certified fp32 normals obey their per-node error bound against the
+    reference's exact fp64 normals (the bound is what makes the fp32 edge
+    decisions safe), and stay within the 1e-5 output tolerance."""
+    import ctypes as C
+    from paper_2005_02704_b200 import _lib, synth
+    shape = synth.CONFIGS[shape_name]
+    xyz, ring, off = synth.make_batch(shape, frames=frames, seed=seed, device="cuda")
+    cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
+                         r_max=shape.r_max)
+    bp = L.BatchPipeline(cfg, 1, frames=frames)
+    err = torch.full((frames, bp.cap), -2.0, dtype=torch.float32, device="cuda")
+    lib = _lib.lib()
+    lib.lseg_debug_cert_err.argtypes = [C.c_void_p]
+    lib.lseg_debug_cert_err(_lib.ptr(err))
+    bp.run(xyz, ring, off)
+    torch.cuda.synchronize()
+    xyz_h, ring_h, off_h = xyz.cpu().numpy(), ring.cpu().numpy(), off.cpu().numpy()
+    n_exact = n_tot = 0
+    worst = 0.0
+    reasons = {}
+    for f in range(frames):
+        sl = slice(off_h[f], off_h[f + 1])
+        want = oracle.run_from_points(xyz_h[sl], ring_h[sl], shape.elevations, shape.steps, 1, shape.r_min,
+                                      shape.r_max)
+        got = bp.frame(f)
+        m = want["mask"]
+        e = err[f, :m.size].cpu().numpy()
+        d = np.abs(got["normals"][m].astype(np.float64) - want["normals"][m]).max(axis=1)
+        em = e[m]
+        assert (em != -1).all() and (em != -2).all()
+        cert = em > 0
+        assert (d[cert] <= em[cert]).all(), "certified bound violated"
+        # nodes that took the exact path carry the exact fp32 rounding
+        assert (d[~cert] <= 6e-8).all()
+        assert d.max() <= 1e-5
+        worst = max(worst, float((d[cert] / em[cert]).max()) if cert.any() else 0.0)
+        n_exact += int((~cert).sum())
+        n_tot += int(m.sum())
+        for code in range(1, 7):
+            reasons[code] = reasons.get(code, 0) + int((em == -10.0 - code).sum())
+    print(f"certified: worst error/bound {worst:.3g}, exact fallbacks {n_exact}/{n_tot}, by reason {reasons}")
+    assert n_exact < 0.05 * n_tot, f"exact fallbacks {n_exact}/{n_tot}"
