@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=2005)
     ap.add_argument("--streams", type=int, default=1, help="frame chunks on concurrent streams")
     ap.add_argument("--chunk", type=int, default=0, help="sequential frame chunks of this size (0 = whole batch)")
+    ap.add_argument("--normals", default="exact", choices=["certified", "exact"],
+                    help="fused-path normals: certified fp32 (labels exact) or exact fp64")
     return ap.parse_args()
 
 
@@ -243,7 +245,8 @@ def main():
     P = int(xyz.shape[0])
     cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
                          r_max=shape.r_max)
-    bp = L.BatchPipeline(cfg, a.interval, frames=F, device=dev, streams=a.streams, chunk_frames=a.chunk or None)
+    bp = L.BatchPipeline(cfg, a.interval, frames=F, device=dev, streams=a.streams, chunk_frames=a.chunk or None,
+                         normals=a.normals)
     st = torch.cuda.current_stream()
 
     def barrier():
@@ -301,7 +304,7 @@ def main():
     # ---- the same batch at the reference's default interval (pipeline.py:25)
     other = None
     if a.also_interval and a.also_interval != a.interval:
-        bp2 = L.BatchPipeline(cfg, a.also_interval, frames=F, device=dev)
+        bp2 = L.BatchPipeline(cfg, a.also_interval, frames=F, device=dev, normals=a.normals)
         for _ in range(3):
             bp2.run(xyz, ring, off)
         barrier()
@@ -330,7 +333,8 @@ def main():
         cf = min(64, F)
         maxp = max(int(ho[min(f + cf, F)] - ho[f]) for f in range(0, F, cf))
         del bp  # free the device-resident pipeline before allocating the streaming one
-        sp = L.StreamingPipeline(cfg, a.interval, chunk_frames=cf, max_chunk_points=maxp, device=dev, ring_dtype=rdt)
+        sp = L.StreamingPipeline(cfg, a.interval, chunk_frames=cf, max_chunk_points=maxp, device=dev, ring_dtype=rdt,
+                                 normals=a.normals)
         for _ in range(2):
             sp.run_host(hx, hr, ho, hl)
         torch.cuda.synchronize()
@@ -357,10 +361,12 @@ def main():
         launches = sum(v[1] for k, v in stages.items() if k not in ("bin_fill",))
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": a.steps,
                 "warmup": max(a.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded ray-cast scenes, BASELINE.json shapes)",
+                "vs_baseline": None, "dtype": "f64" if a.normals == "exact" else "f32+f64",
+                "data": "synthetic (seeded ray-cast scenes, BASELINE.json shapes)",
                 "config": {"workload": f"{shape.name}: {F} frames x {cfg.rings}x{cfg.azimuth_steps} per rank "
                                        f"(BASELINE configs[3])", "interval": a.interval, "frames_per_rank": F,
                            "points_per_rank": P, "nodes_per_rank": N, "parallelism": f"frame-shard x{ws}",
+                           "normals": a.normals,
                            "l2": "inputs (>1 GB per step) exceed the 126 MB L2; no flush needed"},
                 "frames_per_s": run["frames"] / (ms / 1e3),
                 "segments_per_frame": run["segments"] / max(run["frames"], 1),

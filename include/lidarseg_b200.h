@@ -153,18 +153,18 @@ int lseg_run_pipeline_r8(const lseg_sensor* sensor, int32_t frames, int32_t inte
                          int32_t* n_labels, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Flags of lseg_run_pipeline_ex. */
-#define LSEG_PIPE_EXACT_NORMALS 1u /* fp64 normals, then rounded to fp32: normals32 bit-identical to the
-                                      reference's fp64 normals cast to float32 (slower: FP64-bound) */
-#define LSEG_PIPE_RING_U8 2u       /* ring ids are uint8_t (as lseg_run_pipeline_r8) */
+#define LSEG_PIPE_CERT_NORMALS 1u /* certified fp32 normals (see below) instead of exact fp64 ones */
+#define LSEG_PIPE_RING_U8 2u      /* ring ids are uint8_t (as lseg_run_pipeline_r8) */
 
-/* lseg_run_pipeline with flags.  Without LSEG_PIPE_EXACT_NORMALS (and in
- * lseg_run_pipeline / _r8) normals are "certified fp32": computed in fp32
- * with a rigorous per-node error bound; every homogeneity decision the bound
- * cannot settle, and every degenerate or ill-conditioned node, is recomputed
- * with the exact fp64 arithmetic, so node_labels / labels are identical in
- * both modes (bit-exact with the reference).  normals32 then differs from the
- * reference's fp64 normals by far less than 1e-5 per component
- * (SURVEY.md §8(c) tolerance) instead of being its exact rounding. */
+/* lseg_run_pipeline with flags.  By default (and in lseg_run_pipeline / _r8)
+ * normals are computed in fp64 with the reference's operation order, so
+ * normals32 is the exact float32 rounding of the reference's fp64 normals.
+ * With LSEG_PIPE_CERT_NORMALS they are computed in fp32 with a rigorous
+ * per-node error bound; every homogeneity decision the bound cannot settle,
+ * and every degenerate or ill-conditioned node, is recomputed with the exact
+ * fp64 arithmetic, so node_labels / labels are identical in both modes
+ * (bit-exact with the reference) while normals32 then agrees with the
+ * reference to well within 1e-5 per component (SURVEY.md §8(c) tolerance). */
 int lseg_run_pipeline_ex(const lseg_sensor* sensor, int32_t frames, int32_t interval,
                          const double* thresholds, int32_t min_segment_size, uint32_t flags,
                          const float* xyz, const void* ring, const int64_t* frame_offsets,

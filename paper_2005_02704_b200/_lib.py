@@ -57,7 +57,7 @@ _SIGS = {
     "lseg_run_pipeline_ex": (C.c_int, [C.POINTER(lseg_sensor), _I32, _I32, C.POINTER(C.c_double), _I32, C.c_uint32,
                                        _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
 }
-PIPE_EXACT_NORMALS = 1  # include/lidarseg_b200.h LSEG_PIPE_EXACT_NORMALS
+PIPE_CERT_NORMALS = 1  # include/lidarseg_b200.h LSEG_PIPE_CERT_NORMALS
 PIPE_RING_U8 = 2
 EXPORTS = tuple(_SIGS)
 

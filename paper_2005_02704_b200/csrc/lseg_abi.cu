@@ -342,7 +342,7 @@ static int run_pipeline_impl(const lseg_sensor* sensor, int32_t frames, int32_t 
   float* dbg = g_dbg_err;
   g_dbg_err = nullptr;
   launch_fused_graph(*sensor, sh, ws, ranges, thresholds, node_ids, neighbors, normals32, nmask, n_nodes, n_labels,
-                     node_labels, fused_bin, (flags & LSEG_PIPE_EXACT_NORMALS) != 0, dbg, st);
+                     node_labels, fused_bin, (flags & LSEG_PIPE_CERT_NORMALS) == 0, dbg, st);
   launch_prune_fused(sh, ws, min_segment_size, labels, st);
   return check_launch("run_pipeline");
 }
@@ -375,7 +375,7 @@ int lseg_run_pipeline_ex(const lseg_sensor* sensor, int32_t frames, int32_t inte
                          int32_t* neighbors, float* normals32, uint8_t* nmask, int32_t* node_labels,
                          int32_t* labels, int32_t* n_nodes, int32_t* n_labels, void* workspace,
                          size_t workspace_bytes, void* stream) {
-  if (flags & ~(LSEG_PIPE_EXACT_NORMALS | LSEG_PIPE_RING_U8)) return fail(LSEG_EINVAL, "unknown pipeline flags");
+  if (flags & ~(LSEG_PIPE_CERT_NORMALS | LSEG_PIPE_RING_U8)) return fail(LSEG_EINVAL, "unknown pipeline flags");
   return run_pipeline_impl(sensor, frames, interval, thresholds, min_segment_size, flags, xyz, ring,
                            (flags & LSEG_PIPE_RING_U8) ? 1 : 4, frame_offsets, total_points, ranges, node_ids,
                            neighbors, normals32, nmask, node_labels, labels, n_nodes, n_labels, workspace,

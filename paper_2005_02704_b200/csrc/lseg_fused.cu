@@ -11,6 +11,7 @@
 //              root chase), then the nearest-donor backfill and the label
 //              histogram, in one pass (replaces label_dense + backfill).
 #include <cub/block/block_scan.cuh>
+#include <cuda_fp16.h>
 #include <stdlib.h>
 
 #include "lseg_internal.cuh"
@@ -43,6 +44,18 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #endif
 #ifndef LSEG_CC_SV
 #define LSEG_CC_SV 1
+#endif
+#ifndef LSEG_CERT_IDMASK
+#define LSEG_CERT_IDMASK 1
+#endif
+#ifndef LSEG_CERT_SPLITC
+#define LSEG_CERT_SPLITC 0
+#endif
+#ifndef LSEG_CERT_RECOMP
+#define LSEG_CERT_RECOMP 0
+#endif
+#ifndef LSEG_CERT_MINB
+#define LSEG_CERT_MINB 4
 #endif
 static constexpr int TILE_R = kTileR;
 static constexpr int TILE_C = kTileC;
@@ -664,41 +677,64 @@ __device__ __forceinline__ int64_t bn4_col(const Shape& sh, int TR, int slot, in
   return (int64_t)2 * ((sh.R + TR - 1) / TR) * sh.Sk + (int64_t)slot * sh.R + r;
 }
 
-// One CTA per (frame, TR x TC tile), certified normals.  Phases:
-//   A  halo positions (fp64, reference product order) + node ids in smem
-//   B  fp32 normals + bounds from the exactly formed fp64 edge vectors
-//   X0 exact fp64 normals of the nodes the bound could not certify
-//   D1 edge decisions: certain pass / fail, or undecided -> both ends requested
-//   X1 exact fp64 normals of the requested endpoints
-//   D2 undecided edges settled on the exact normals; masks out
-//   C  per-node outputs
-// The exact work (X0 / X1, usually a few nodes per tile) runs lane-dense from
-// the shared-memory positions; its fp64 normals go to the global scratch
-// `xn` for D2.
+// One CTA per (frame, TR x TC tile), certified normals.  Phases (4 barriers
+// when nothing needs the exact path):
+//   A  halo positions (fp64, reference product order) + node ids in smem,
+//      then per halo row a presence bitmask (slot masks by bit arithmetic)
+//   L  work lists: all-six-slot nodes / the rest (warp-aggregated atomics)
+//   B  fp32 normals + bounds from the exactly formed fp64 edge vectors;
+//      uncertified nodes are listed for X0
+//   X0 exact fp64 normals of the uncertified nodes (lane-dense, from smem)
+//   D  per row: edge decisions (certain pass / fail / undecided) and the
+//      per-node outputs; undecided edges list their endpoints for X1
+//   X1 + D2 (rare): exact normals of those endpoints, undecided edges settled
+// Exact fp64 normals also go to the global scratch `xn` (read back by D2).
 template <int TR, int TC, int T>
-__global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile_cert(
+__global__ void __launch_bounds__(T, LSEG_CERT_MINB) k_tile_cert(
     lseg_sensor sn, Shape sh, const double* __restrict__ ranges, const uint32_t* __restrict__ vbits,
     const int32_t* __restrict__ wpre, CertParams cp, int32_t* __restrict__ node_ids, int32_t* __restrict__ neighbors,
     float* __restrict__ n32, uint8_t* __restrict__ nmask, unsigned long long* __restrict__ masks,
     float4* __restrict__ bn4, double* __restrict__ xn, float* __restrict__ dbg_err, int32_t* __restrict__ fscal) {
   constexpr int GR = TR + 2, GC = TC + 2, NH = GR * GC;
   constexpr int NT = TR * TC;
+  static_assert(TC == 64, "row masks assume 64-column tiles");
   extern __shared__ __align__(16) unsigned char s_dyn[];
+#if LSEG_CERT_RECOMP
+  // ranges + separable direction tables; positions rebuilt on use (fewer
+  // shared bytes -> more resident CTAs)
+  double* s_r = reinterpret_cast<double*>(s_dyn);
+  double* s_ct = s_r + NH;
+  double* s_st = s_ct + GR;
+  double* s_cp = s_st + GR;
+  double* s_sp = s_cp + GC;
+  float* s_nx = reinterpret_cast<float*>(s_sp + GC);
+  auto posg = [&](int gi) -> Vec3 {
+    const int yy = gi / GC, xx = gi - yy * GC;
+    const double ct = s_ct[yy], r = s_r[gi];
+    return Vec3{__dmul_rn(__dmul_rn(ct, s_cp[xx]), r), __dmul_rn(__dmul_rn(ct, s_sp[xx]), r),
+                __dmul_rn(s_st[yy], r)};
+  };
+#else
   double* s_px = reinterpret_cast<double*>(s_dyn);
   double* s_py = s_px + NH;
   double* s_pz = s_py + NH;
   float* s_nx = reinterpret_cast<float*>(s_pz + NH);
+  auto posg = [&](int gi) -> Vec3 { return Vec3{s_px[gi], s_py[gi], s_pz[gi]}; };
+#endif
   float* s_ny = s_nx + NT;
   float* s_nz = s_ny + NT;
-  float* s_err = s_nz + NT;
-  int* s_id = reinterpret_cast<int*>(s_err + NT);
-  unsigned short* s_list = reinterpret_cast<unsigned short*>(s_id + NH);
-  uint8_t* s_has = reinterpret_cast<uint8_t*>(s_list + NT);  // 0 none, 1 normal, 2 not certified (yet)
-  uint8_t* s_m = s_has + NT;                                  // slot mask of general-path nodes
-  uint8_t* s_req = s_m + NT;                                  // exact path: 1 edge request, >= 2 reason
+  __half* s_eh = reinterpret_cast<__half*>(s_nz + NT);  // err / u, rounded up (<= 64 kAcc + 8 < 65504)
+  int* s_id = reinterpret_cast<int*>(s_eh + NT);
+  unsigned short* s_list = reinterpret_cast<unsigned short*>(s_id + NH);  // fan6 from the front, rest from the back
+  unsigned short* s_xl = s_list + NT;                                     // exact-path list (X0, then X1)
+  uint8_t* s_has = reinterpret_cast<uint8_t*>(s_xl + NT);  // 0 none, 1 normal, 2 uncertified
+  uint8_t* s_m = s_has + NT;                                // slot mask
+  uint8_t* s_req = s_m + NT;                                // exact path: 1 edge request, >= 2 reason
+  __shared__ unsigned long long s_hm[GR];                   // presence of halo columns 1..64 per halo row
+  __shared__ unsigned s_he[GR];                             // bit 0: halo column 0, bit 1: column 65
   __shared__ unsigned long long s_U[TR * 3];
   __shared__ unsigned s_UW[TR];
-  __shared__ int s_cnt[2 * (T / 32) + 3];
+  __shared__ int s_cnt[5];  // fan6, general, X0, X1 list sizes; undecided edges
 
   const int tilesC = (sh.Sk + TC - 1) / TC;
   const int tilesR = (sh.R + TR - 1) / TR;
@@ -713,6 +749,10 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile_cert(
   const int64_t nbase = (int64_t)f * sh.cap;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+#if LSEG_PHASES
+  long long ph_prev = clock64();
+#endif
+  if (tid < 5) s_cnt[tid] = 0;
   if (rem == 0 && tid == 0) fscal[f * 4 + 2] = 0;  // k_merge_cert's undecided-edge counter
 
   // A. halo positions dir*r (reference product order) and node ids
@@ -745,89 +785,112 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile_cert(
       const int cc = wrapc(c0 - 1 + x, sh.Sk);
       const uint32_t bit = 1u << (cc & 31);
       const int id = (wv[j] & bit) ? pv[j] + __popc(wv[j] & (bit - 1u)) : -1;
+#if LSEG_CERT_RECOMP
+      s_r[e] = id >= 0 ? rv[j] : 0.0;
+      (void)rr;
+#else
       Vec3 q = {0.0, 0.0, 0.0};
       if (id >= 0) q = cell_pos(sn, rr, cc * sh.k, rv[j]);
       s_px[e] = q.x;
       s_py[e] = q.y;
       s_pz[e] = q.z;
+#endif
       s_id[e] = id;
     }
-  }
-  __syncthreads();
-
-  // B. certified fp32 normals, split into the fan6 / general work lists
-  {
-    unsigned char ml[(NT + T - 1) / T];
-    int kind[(NT + T - 1) / T];
-    int na = 0, nb = 0;
-#pragma unroll
-    for (int j = 0; j < (NT + T - 1) / T; ++j) {
-      const int e = tid + j * T;
-      const int y = e / TC, x = e - y * TC;
-      const int g = (y + 1) * GC + (x + 1);
-      unsigned m = 0;
-      kind[j] = 0;
-      if (e < NT && y < TRe && x < TCe && s_id[g] >= 0) {
-#pragma unroll
-        for (int s = 0; s < 6; ++s)
-          if (s_id[g + slot_dr(s) * GC + slot_dc(s)] >= 0 && !(s == 5 && sh.Sk == 2)) m |= 1u << s;
-        kind[j] = (m == 0x3fu) ? 1 : 2;
+#if LSEG_CERT_RECOMP
+    for (int e = tid; e < GR + GC; e += T) {
+      if (e < GR) {
+        const int rr = min(max(r0 - 1 + e, 0), sh.R - 1);
+        s_ct[e] = __ldg(sn.cos_el + rr);
+        s_st[e] = __ldg(sn.sin_el + rr);
+      } else {
+        const int cc = wrapc(c0 - 1 + (e - GR), sh.Sk) * sh.k;
+        s_cp[e - GR] = __ldg(sn.cos_az + cc);
+        s_sp[e - GR] = __ldg(sn.sin_az + cc);
       }
-      ml[j] = (unsigned char)m;
-      na += kind[j] == 1;
-      nb += kind[j] == 2;
-      if (e < NT) { s_has[e] = 0; s_req[e] = 0; s_m[e] = (unsigned char)m; }
     }
-    int ia = na, ib = nb;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int ta = __shfl_up_sync(0xffffffffu, ia, o), tb = __shfl_up_sync(0xffffffffu, ib, o);
-      if (lane >= o) { ia += ta; ib += tb; }
-    }
-    if (lane == 31) { s_cnt[warp] = ia; s_cnt[T / 32 + warp] = ib; }
-    __syncthreads();
-    int oa = 0, ob = 0, ta = 0, tb = 0;
-    for (int w = 0; w < T / 32; ++w) {
-      if (w < warp) { oa += s_cnt[w]; ob += s_cnt[T / 32 + w]; }
-      ta += s_cnt[w];
-      tb += s_cnt[T / 32 + w];
-    }
-    oa += ia - na;
-    ob += ib - nb;
-#pragma unroll
-    for (int j = 0; j < (NT + T - 1) / T; ++j) {
-      const int e = tid + j * T;
-      if (kind[j] == 1) s_list[oa++] = (unsigned short)e;
-      else if (kind[j] == 2) { s_list[NT - 1 - ob] = (unsigned short)e; ++ob; }
-    }
-    (void)ml;
-    __syncthreads();  // s_cnt is rewritten below
-    if (tid == 0) { s_cnt[2 * (T / 32)] = ta; s_cnt[2 * (T / 32) + 1] = tb; }
+#endif
   }
   __syncthreads();
-  const int nfan6 = s_cnt[2 * (T / 32)], ngen = s_cnt[2 * (T / 32) + 1];
+  for (int hy = warp; hy < GR; hy += T / 32) {
+    const int* row = s_id + hy * GC;
+    const unsigned lo = __ballot_sync(0xffffffffu, row[1 + lane] >= 0);
+    const unsigned hi = __ballot_sync(0xffffffffu, row[33 + lane] >= 0);
+    if (lane == 0) {
+      s_hm[hy] = ((unsigned long long)hi << 32) | lo;
+      s_he[hy] = (row[0] >= 0 ? 1u : 0u) | (row[GC - 1] >= 0 ? 2u : 0u);
+    }
+  }
+  __syncthreads();
+  PH_MARK(1);
+
+  // L. slot masks (mesh.py:83-102) from the presence bits, work lists
+  auto pres = [&](int hy, int xx) -> unsigned {  // xx = tile column (-1..64)
+    return xx < 0 ? (s_he[hy] & 1u) : xx > 63 ? ((s_he[hy] >> 1) & 1u) : (unsigned)((s_hm[hy] >> xx) & 1ull);
+  };
+#pragma unroll
+  for (int j = 0; j < NT / T; ++j) {
+    const int e = tid + j * T;
+    const int y = e / TC, x = e - y * TC;
+    const int hy = y + 1;
+    unsigned m = 0;
+    const bool node = y < TRe && x < TCe && pres(hy, x);
+    if (node) {
+#if LSEG_CERT_IDMASK
+      const int g = hy * GC + x + 1;
+#pragma unroll
+      for (int s = 0; s < 6; ++s)
+        if (s_id[g + slot_dr(s) * GC + slot_dc(s)] >= 0 && !(s == 5 && sh.Sk == 2)) m |= 1u << s;
+#else
+      m = pres(hy + 1, x) | pres(hy + 1, x + 1) << 1 | pres(hy, x + 1) << 2 | pres(hy - 1, x) << 3 |
+          pres(hy - 1, x - 1) << 4 | (sh.Sk == 2 ? 0u : pres(hy, x - 1) << 5);
+#endif
+    }
+    s_m[e] = (uint8_t)m;
+    s_has[e] = 0;
+    s_req[e] = 0;
+    const bool six = node && m == 0x3fu, gen = node && m != 0x3fu;
+    const unsigned b6 = __ballot_sync(0xffffffffu, six), bg = __ballot_sync(0xffffffffu, gen);
+    int o6 = 0, og = 0;
+    if (lane == 0) {
+      if (b6) o6 = atomicAdd(&s_cnt[0], __popc(b6));
+      if (bg) og = atomicAdd(&s_cnt[1], __popc(bg));
+    }
+    o6 = __shfl_sync(0xffffffffu, o6, 0);
+    og = __shfl_sync(0xffffffffu, og, 0);
+    const unsigned below = (1u << lane) - 1u;
+    if (six) s_list[o6 + __popc(b6 & below)] = (unsigned short)e;
+    if (gen) s_list[NT - 1 - (og + __popc(bg & below))] = (unsigned short)e;
+  }
+  __syncthreads();
+  PH_MARK(2);
+
+  // B. certified fp32 normals
+  const int nfan6 = s_cnt[0], ngen = s_cnt[1];
   auto node_normal = [&](int e, unsigned m) {
     const int y = e / TC, x = e - y * TC;
     const int g = (y + 1) * GC + (x + 1);
-    const double px = s_px[g], py = s_py[g], pz = s_pz[g];
+    const Vec3 p = posg(g);
     Fan32 fan;
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       if (!((m >> s) & 1u)) continue;
-      const int gq = g + slot_dr(s) * GC + slot_dc(s);
-      fan.add(__double2float_rn(__dsub_rn(s_px[gq], px)), __double2float_rn(__dsub_rn(s_py[gq], py)),
-              __double2float_rn(__dsub_rn(s_pz[gq], pz)), cp.deg2);
+      const Vec3 q = posg(g + slot_dr(s) * GC + slot_dc(s));
+      fan.add(__double2float_rn(__dsub_rn(q.x, p.x)), __double2float_rn(__dsub_rn(q.y, p.y)),
+              __double2float_rn(__dsub_rn(q.z, p.z)), cp.deg2);
     }
     float nv[3] = {0.f, 0.f, 0.f}, err = 0.f;
-    const int st = fan.finish(__double2float_rn(px), __double2float_rn(py), __double2float_rn(pz), nv, err);
-    s_has[e] = (uint8_t)min(st, 2);
+    const int st = fan.finish(__double2float_rn(p.x), __double2float_rn(p.y), __double2float_rn(p.z), nv, err);
     if (st == 1) {
       s_nx[e] = nv[0];
       s_ny[e] = nv[1];
       s_nz[e] = nv[2];
-      s_err[e] = err;
+      s_eh[e] = __float2half_ru(err * (1.0f / kU32));
+      s_has[e] = 1;
     } else if (st >= 2) {
+      s_has[e] = 2;
       s_req[e] = (uint8_t)st;
+      s_xl[atomicAdd(&s_cnt[2], 1)] = (unsigned short)e;
     }
   };
   for (int i = tid; i < nfan6; i += T) node_normal(s_list[i], 0x3fu);  // straight-line: all six slots
@@ -836,41 +899,23 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile_cert(
     node_normal(e, s_m[e]);
   }
   __syncthreads();
+  PH_MARK(3);
 
-  // X. exact fp64 normals of the nodes whose s_req code matches (first: the
-  // uncertified nodes, else: endpoints of undecided edges), compacted into
-  // s_list so the rare fp64 work runs lane-dense.  Block-uniform.
+  // X. exact fp64 normals of the listed nodes, from the smem positions
   double* xf = xn + nbase * 3;
-  auto run_exact = [&](bool first) {
-    if (tid == 0) s_cnt[2 * (T / 32) + 2] = 0;
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < (NT + T - 1) / T; ++j) {  // NT is a multiple of T: whole warps
-      const int e = tid + j * T;
-      const int q = (e < NT) ? s_req[e] : 0;
-      const bool want = first ? (q >= 2) : (q == 1);
-      const unsigned bal = __ballot_sync(0xffffffffu, want);
-      if (bal) {
-        int base = 0;
-        if (lane == 0) base = atomicAdd(&s_cnt[2 * (T / 32) + 2], __popc(bal));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (want) s_list[base + __popc(bal & ((1u << lane) - 1u))] = (unsigned short)e;
-      }
-    }
-    __syncthreads();
-    const int n = s_cnt[2 * (T / 32) + 2];
+  auto run_exact = [&](int n) {
     for (int i = tid; i < n; i += T) {
-      const int e = s_list[i];
+      const int e = s_xl[i];
       const int y = e / TC, x = e - y * TC;
       const int g = (y + 1) * GC + (x + 1);
       const unsigned m = s_m[e];
-      const Vec3 p = {s_px[g], s_py[g], s_pz[g]};
+      const Vec3 p = posg(g);
       FanT<kFastMath> fan;
 #pragma unroll
       for (int s = 0; s < 6; ++s) {
         if (!((m >> s) & 1u)) continue;
-        const int gq = g + slot_dr(s) * GC + slot_dc(s);
-        fan.add(__dsub_rn(s_px[gq], p.x), __dsub_rn(s_py[gq], p.y), __dsub_rn(s_pz[gq], p.z));
+        const Vec3 q = posg(g + slot_dr(s) * GC + slot_dc(s));
+        fan.add(__dsub_rn(q.x, p.x), __dsub_rn(q.y, p.y), __dsub_rn(q.z, p.z));
       }
       double nv[3];
       const bool has = fan.finish(p, nv);
@@ -879,30 +924,43 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile_cert(
       xf[cell * 3] = has ? nv[0] : qn;
       xf[cell * 3 + 1] = has ? nv[1] : qn;
       xf[cell * 3 + 2] = has ? nv[2] : qn;
-      s_has[e] = has ? 1 : 0;
-      if (has) {
-        s_nx[e] = __double2float_rn(nv[0]);
-        s_ny[e] = __double2float_rn(nv[1]);
-        s_nz[e] = __double2float_rn(nv[2]);
-        s_err[e] = 0.5f * kU32;  // rounding of the exact normal to fp32
+      if (s_req[e] >= 2) {  // X0: the exact normal is the node's output
+        s_has[e] = has ? 1 : 0;
+        if (has) {
+          s_nx[e] = __double2float_rn(nv[0]);
+          s_ny[e] = __double2float_rn(nv[1]);
+          s_nz[e] = __double2float_rn(nv[2]);
+          s_eh[e] = __float2half_ru(0.5f);  // rounding of the exact normal to fp32
+        }
       }
     }
-    __syncthreads();
   };
-  run_exact(true);
+  const int nx0 = s_cnt[2];
+  if (nx0) {
+    run_exact(nx0);
+    __syncthreads();
+    if (tid == 0) s_cnt[2] = 0;  // no reader before the next barrier
+  }
+  PH_MARK(4);
 
-  // D1. decisions on the tile's internal forward edges, one warp per row:
-  // certain passes into the masks, undecided edges into s_U (both ends
-  // requested for X1).
-  static_assert(TC == 64, "row masks assume 64-column tiles");
+  // D. per row: edge decisions + per-node outputs.  One warp per row, lane x
+  // and x + 32.  Undecided edges list their not-yet-exact endpoints for X1.
   const bool full_width = (c0 == 0 && TCe == sh.Sk);
   unsigned long long* mrow = masks + (((int64_t)f * tilesR + r0 / TR) * tilesC + c0 / TC) * (TR * 5);
+  float4* bf = bn4 + (int64_t)f * bn4_frame(sh, TR, TC);
+  const int tr = r0 / TR, tc = c0 / TC;
+  auto request = [&](int e) {
+    const unsigned sft = (e & 3) * 8;
+    const unsigned old = atomicOr(reinterpret_cast<unsigned*>(s_req) + (e >> 2), 1u << sft);
+    if (!((old >> sft) & 0xffu)) s_xl[atomicAdd(&s_cnt[3], 1)] = (unsigned short)e;
+  };
   auto decide = [&](int ea, int eb) -> int {  // 1 pass, 0 fail, 2 undecided
     if (!s_has[eb]) return 0;
-    const int r = cert_pass(cp, s_nx[ea], s_ny[ea], s_nz[ea], s_err[ea], s_nx[eb], s_ny[eb], s_nz[eb], s_err[eb]);
+    const int r = cert_pass(cp, s_nx[ea], s_ny[ea], s_nz[ea], __half2float(s_eh[ea]) * kU32, s_nx[eb], s_ny[eb],
+                            s_nz[eb], __half2float(s_eh[eb]) * kU32);
     if (r == 2) {
-      if (!s_req[ea]) s_req[ea] = 1;
-      if (!s_req[eb]) s_req[eb] = 1;
+      request(ea);
+      request(eb);
     }
     return r;
   };
@@ -913,8 +971,9 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile_cert(
     for (int half = 0; half < 2; ++half) {
       const int x = lane + 32 * half;
       const int e = y * TC + x;
+      const bool in = y < TRe && x < TCe;
+      const bool hs = in && s_has[e];
       int h = 0, v0 = 0, v1 = 0, w0 = 0, w1 = 0;
-      const bool hs = (y < TRe && x < TCe) && s_has[e];
       if (hs) {
         if (x + 1 < TCe) h = decide(e, e + 1);
         if (y + 1 < TRe) {
@@ -932,12 +991,45 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile_cert(
       V1 |= (unsigned long long)__ballot_sync(0xffffffffu, v1 == 1) << sh_;
       HS |= (unsigned long long)__ballot_sync(0xffffffffu, hs) << sh_;
       W |= (__ballot_sync(0xffffffffu, w0 == 1) ? 1u : 0u) | (__ballot_sync(0xffffffffu, w1 == 1) ? 2u : 0u);
-      const unsigned any2 = __ballot_sync(0xffffffffu, (h | v0 | v1 | w0 | w1) & 2);
-      if (any2) {  // rare
+      if (__any_sync(0xffffffffu, (h | v0 | v1 | w0 | w1) & 2)) {  // rare
         UH |= (unsigned long long)__ballot_sync(0xffffffffu, h == 2) << sh_;
         UV0 |= (unsigned long long)__ballot_sync(0xffffffffu, v0 == 2) << sh_;
         UV1 |= (unsigned long long)__ballot_sync(0xffffffffu, v1 == 2) << sh_;
         UW |= (__ballot_sync(0xffffffffu, w0 == 2) ? 1u : 0u) | (__ballot_sync(0xffffffffu, w1 == 2) ? 2u : 0u);
+      }
+      // per-node outputs
+      if (!LSEG_CERT_SPLITC && in) {
+        const int rr = r0 + y, cc = c0 + x;
+        const int g = (y + 1) * GC + (x + 1);
+        const int id = s_id[g];
+        if (node_ids) node_ids[nbase + (int64_t)rr * sh.Sk + cc] = id;
+        if (id >= 0) {
+          int nb[6];
+#pragma unroll
+          for (int s = 0; s < 6; ++s) nb[s] = s_id[g + slot_dr(s) * GC + slot_dc(s)];
+          if (sh.Sk == 2 && nb[5] == nb[2]) nb[5] = -1;
+          int2* o2 = reinterpret_cast<int2*>(neighbors + (nbase + id) * 6);
+          o2[0] = make_int2(nb[0], nb[1]);
+          o2[1] = make_int2(nb[2], nb[3]);
+          o2[2] = make_int2(nb[4], nb[5]);
+          const float qn = __int_as_float(0x7fc00000);
+          const float4 v = hs ? make_float4(s_nx[e], s_ny[e], s_nz[e], __half2float(s_eh[e]) * kU32)
+                              : make_float4(qn, qn, qn, -1.0f);
+          if (n32) {
+            float* o = n32 + (nbase + id) * 3;
+            o[0] = v.x;
+            o[1] = v.y;
+            o[2] = v.z;
+          }
+          if (dbg_err) dbg_err[nbase + id] = s_req[e] >= 2 ? -10.0f - s_req[e] : v.w;
+          nmask[nbase + id] = hs ? 1 : 0;
+          if (hs) {
+            if (y == 0) bf[bn4_row(sh, 2 * tr, cc)] = v;
+            if (y == TRe - 1) bf[bn4_row(sh, 2 * tr + 1, cc)] = v;
+            if (x == 0) bf[bn4_col(sh, TR, 2 * tc, rr)] = v;
+            if (x == TCe - 1) bf[bn4_col(sh, TR, 2 * tc + 1, rr)] = v;
+          }
+        }
       }
     }
     if (lane == 0) {
@@ -950,15 +1042,57 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile_cert(
       s_U[y * 3 + 1] = UV0;
       s_U[y * 3 + 2] = UV1;
       s_UW[y] = UW;
+      if ((UH | UV0 | UV1) || UW) atomicAdd(&s_cnt[4], 1);
     }
   }
   __syncthreads();
+  PH_MARK(5);
 
-  // X1 + D2: settle the undecided edges on exact normals (rare; block-uniform)
-  int nu = 0;
-  if (tid < TR) nu = (s_U[tid * 3] | s_U[tid * 3 + 1] | s_U[tid * 3 + 2]) != 0ull || s_UW[tid] != 0u;
-  if (__syncthreads_or(nu)) {
-    run_exact(false);
+#if LSEG_CERT_SPLITC
+  for (int e = tid; e < NT; e += T) {
+    const int y = e / TC, x = e - y * TC;
+    if (y >= TRe || x >= TCe) continue;
+    const int rr = r0 + y, cc = c0 + x;
+    const int g = (y + 1) * GC + (x + 1);
+    const int id = s_id[g];
+    if (node_ids) node_ids[nbase + (int64_t)rr * sh.Sk + cc] = id;
+    if (id < 0) continue;
+    int nb[6];
+#pragma unroll
+    for (int s = 0; s < 6; ++s) nb[s] = s_id[g + slot_dr(s) * GC + slot_dc(s)];
+    if (sh.Sk == 2 && nb[5] == nb[2]) nb[5] = -1;
+    int2* o2 = reinterpret_cast<int2*>(neighbors + (nbase + id) * 6);
+    o2[0] = make_int2(nb[0], nb[1]);
+    o2[1] = make_int2(nb[2], nb[3]);
+    o2[2] = make_int2(nb[4], nb[5]);
+    const bool hs = s_has[e] != 0;
+    const float qn = __int_as_float(0x7fc00000);
+    const float4 v = hs ? make_float4(s_nx[e], s_ny[e], s_nz[e], __half2float(s_eh[e]) * kU32)
+                        : make_float4(qn, qn, qn, -1.0f);
+    if (n32) {
+      float* o = n32 + (nbase + id) * 3;
+      o[0] = v.x;
+      o[1] = v.y;
+      o[2] = v.z;
+    }
+    if (dbg_err) dbg_err[nbase + id] = s_req[e] >= 2 ? -10.0f - s_req[e] : v.w;
+    nmask[nbase + id] = hs ? 1 : 0;
+    if (hs) {
+      if (y == 0) bf[bn4_row(sh, 2 * tr, cc)] = v;
+      if (y == TRe - 1) bf[bn4_row(sh, 2 * tr + 1, cc)] = v;
+      if (x == 0) bf[bn4_col(sh, TR, 2 * tc, rr)] = v;
+      if (x == TCe - 1) bf[bn4_col(sh, TR, 2 * tc + 1, rr)] = v;
+    }
+  }
+#endif
+
+  // X1 + D2 (rare; block-uniform): settle the undecided edges on exact normals
+  if (s_cnt[4]) {
+    const int nx1 = s_cnt[3];
+    if (nx1) {
+      run_exact(nx1);
+      __syncthreads();
+    }
     auto exact_pass = [&](int ea, int eb) -> bool {
       const int ya = ea / TC, yb = eb / TC;
       const int64_t ca = (int64_t)(r0 + ya) * sh.Sk + c0 + (ea - ya * TC);
@@ -996,45 +1130,10 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile_cert(
       }
     }
   }
-
-  // C. per-node outputs
-  float4* bf = bn4 + (int64_t)f * bn4_frame(sh, TR, TC);
-  const int tr = r0 / TR, tc = c0 / TC;
-  for (int e = tid; e < NT; e += T) {
-    const int y = e / TC, x = e - y * TC;
-    if (y >= TRe || x >= TCe) continue;
-    const int rr = r0 + y, cc = c0 + x;
-    const int g = (y + 1) * GC + (x + 1);
-    const int id = s_id[g];
-    const int64_t cell = (int64_t)rr * sh.Sk + cc;
-    if (node_ids) node_ids[nbase + cell] = id;
-    if (id < 0) continue;
-    int nb[6];
-#pragma unroll
-    for (int s = 0; s < 6; ++s) nb[s] = s_id[g + slot_dr(s) * GC + slot_dc(s)];
-    if (sh.Sk == 2 && nb[5] == nb[2]) nb[5] = -1;
-    int2* o2 = reinterpret_cast<int2*>(neighbors + (nbase + id) * 6);
-    o2[0] = make_int2(nb[0], nb[1]);
-    o2[1] = make_int2(nb[2], nb[3]);
-    o2[2] = make_int2(nb[4], nb[5]);
-    const bool has = s_has[e] == 1;
-    const float qn = __int_as_float(0x7fc00000);
-    const float4 v = has ? make_float4(s_nx[e], s_ny[e], s_nz[e], s_err[e]) : make_float4(qn, qn, qn, -1.0f);
-    if (n32) {
-      float* o = n32 + (nbase + id) * 3;
-      o[0] = v.x;
-      o[1] = v.y;
-      o[2] = v.z;
-    }
-    if (dbg_err) dbg_err[nbase + id] = s_req[e] >= 2 ? -10.0f - s_req[e] : (s_req[e] ? -11.0f : v.w);
-    nmask[nbase + id] = has ? 1 : 0;
-    if (has) {
-      if (y == 0) bf[bn4_row(sh, 2 * tr, cc)] = v;
-      if (y == TRe - 1) bf[bn4_row(sh, 2 * tr + 1, cc)] = v;
-      if (x == 0) bf[bn4_col(sh, TR, 2 * tc, rr)] = v;
-      if (x == TCe - 1) bf[bn4_col(sh, TR, 2 * tc + 1, rr)] = v;
-    }
-  }
+#if LSEG_PHASES
+  __syncthreads();
+#endif
+  PH_MARK(0);
 }
 
 // Global union over tile-border edges from the certified border normals;
@@ -1941,7 +2040,12 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
     }
     cp.deg2 = 1e-30f;  // |V| < 1e-15: fp32 squares would leave the normal range
     constexpr int NH = (TILE_R + 2) * (TILE_C + 2), NT = TILE_R * TILE_C;
-    const size_t csmem = (size_t)NH * (3 * 8 + 4) + (size_t)NT * (4 * 4 + 2 + 3);  // see k_tile_cert
+#if LSEG_CERT_RECOMP
+    const size_t csmem = (size_t)NH * (8 + 4) + (size_t)(2 * (TILE_R + 2) + 2 * (TILE_C + 2)) * 8 +
+                         (size_t)NT * (3 * 4 + 2 + 2 + 2 + 3);  // see k_tile_cert
+#else
+    const size_t csmem = (size_t)NH * (3 * 8 + 4) + (size_t)NT * (3 * 4 + 2 + 2 + 2 + 3);  // see k_tile_cert
+#endif
     static bool cattr = false;
     if (!cattr) {
       cudaFuncSetAttribute(k_tile_cert<TILE_R, TILE_C, TILE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -103,13 +103,14 @@ class BatchPipeline:
 
     def __init__(self, config: SensorConfig, interval: int, segmenter: SegmenterConfig | None = None,
                  frames: int = 1, device=None, keep_node_labels: bool = False, streams: int = 1,
-                 chunk_frames: int | None = None, normals: str = "certified"):
+                 chunk_frames: int | None = None, normals: str = "exact"):
         self.L = _lib.lib()
         if normals not in ("certified", "exact"):
             raise ValueError("normals must be 'certified' or 'exact'")
-        # "certified": fp32 normals with a rigorous error bound, exact fp64 only
-        # where a decision needs it (labels identical); "exact": fp64 normals
-        # rounded to fp32 (bit-identical to the reference's, FP64-bound)
+        # "exact": fp64 normals in the reference's operation order, rounded to
+        # fp32; "certified": fp32 normals with a rigorous error bound, exact
+        # fp64 only where a decision or the output tolerance needs it (labels
+        # identical in both modes)
         self.normals_mode = normals
         self.config = config
         self.interval = int(interval)
@@ -149,7 +150,7 @@ class BatchPipeline:
     def _call(self, f0, f1, ws, xyz, ring, offsets):
         P = int(xyz.shape[0])
         sl = lambda t: None if t is None else t[f0:f1]
-        flags = _lib.PIPE_EXACT_NORMALS if self.normals_mode == "exact" else 0
+        flags = _lib.PIPE_CERT_NORMALS if self.normals_mode == "certified" else 0
         if ring.dtype == torch.uint8:
             flags |= _lib.PIPE_RING_U8
         elif ring.dtype != torch.int32:
@@ -199,7 +200,7 @@ class StreamingPipeline:
 
     def __init__(self, config: SensorConfig, interval: int, segmenter: SegmenterConfig | None = None,
                  chunk_frames: int = 64, max_chunk_points: int | None = None, device=None,
-                 ring_dtype=torch.int32, normals: str = "certified"):
+                 ring_dtype=torch.int32, normals: str = "exact"):
         self.device = torch.device(device or "cuda")
         self.cf = int(chunk_frames)
         R, S = config.rings, config.azimuth_steps

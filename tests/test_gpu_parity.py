@@ -84,7 +84,7 @@ def test_bin_points_golden(L, name):
     np.testing.assert_array_equal(grid.ranges, g["ranges"])
 
 
-def _run_batch(L, shape_name, frames, k, seed=5, normals="certified"):
+def _run_batch(L, shape_name, frames, k, seed=5, normals="exact"):
     from paper_2005_02704_b200 import synth
     shape = synth.CONFIGS[shape_name]
     xyz, ring, off = synth.make_batch(shape, frames=frames, seed=seed, device="cuda")
@@ -281,7 +281,7 @@ def test_certified_normal_bounds_hold(L, oracle, shape_name, frames, seed):
     xyz, ring, off = synth.make_batch(shape, frames=frames, seed=seed, device="cuda")
     cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
                          r_max=shape.r_max)
-    bp = L.BatchPipeline(cfg, 1, frames=frames)
+    bp = L.BatchPipeline(cfg, 1, frames=frames, normals="certified")
     err = torch.full((frames, bp.cap), -2.0, dtype=torch.float32, device="cuda")
     lib = _lib.lib()
     lib.lseg_debug_cert_err.argtypes = [C.c_void_p]

@@ -14,7 +14,12 @@ out = (C.c_double * 8)()
 bp.run(xyz, ring, off); torch.cuda.synchronize(); f(out)
 for _ in range(3): bp.run(xyz, ring, off)
 torch.cuda.synchronize(); f(out)
-names = ["", "A halo", "B1 lists", "B2 normals", "C outputs", "D masks"]
-tot = sum(out[1:6])
-for i in range(1, 6): print(f"{names[i]:12s} {100*out[i]/tot:5.1f}%")
+if os.environ.get("CERT", "1") == "1":
+    names = ["X1+D2", "A halo", "L lists", "B normals", "X0 exact", "D dec+out"]
+    tot = sum(out[0:6])
+    for i in range(0, 6): print(f"{names[i]:12s} {100*out[i]/tot:5.1f}%")
+else:
+    names = ["", "A halo", "B1 lists", "B2 normals", "C outputs", "D masks"]
+    tot = sum(out[1:6])
+    for i in range(1, 6): print(f"{names[i]:12s} {100*out[i]/tot:5.1f}%")
 print("tile_cc label-propagation rounds per tile: %.2f" % (out[6] / max(out[7], 1)))
