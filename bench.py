@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-latency", action="store_true", help="skip the single-scan latency (CUDA graph) lines")
     ap.add_argument("--also-interval", type=int, default=5,
                     help="also time this interval (reference default 5); 0 disables")
     ap.add_argument("--seed", type=int, default=2005)
@@ -223,6 +224,38 @@ def run_reference(a, shape):
     print(json.dumps(line), flush=True)
 
 
+def single_scan_latency(dev, normals="exact", reps=200):
+    """single scans of configs 1-3 are launch-bound, so they
+    are reported as latency -- device time per frame of one scan, eager
+    (every kernel launched from the host) and as one replayed CUDA graph."""
+    import paper_2005_02704_b200 as L
+    from paper_2005_02704_b200 import synth
+    out = {}
+    for name in ("vlp16", "hdl64", "os128"):
+        shape = synth.CONFIGS[name]
+        xyz, ring, off = synth.make_batch(shape, frames=1, seed=77, device=dev)
+        cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
+                             r_max=shape.r_max)
+        bp = L.BatchPipeline(cfg, 1, frames=1, device=dev, normals=normals)
+        g = bp.capture(xyz, ring, off)
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        res = {}
+        for mode in ("eager", "graph"):
+            for _ in range(10):
+                g.replay() if mode == "graph" else bp.run(xyz, ring, off)
+            torch.cuda.synchronize()
+            e0.record(st)
+            for _ in range(reps):
+                g.replay() if mode == "graph" else bp.run(xyz, ring, off)
+            e1.record(st)
+            torch.cuda.synchronize()
+            res[mode + "_us_per_frame"] = e0.elapsed_time(e1) * 1e3 / reps
+        res["points"] = int(xyz.shape[0])
+        out[name] = res
+    return out
+
+
 def main():
     a = parse()
     from paper_2005_02704_b200 import synth
@@ -373,6 +406,8 @@ def main():
                 "roofline": roof, "pipeline_roofline": pipe_roof, "stage_ms": stage_ms,
                 "at_interval_%d" % a.also_interval if other else "at_other_interval": other,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk}
+        if not a.no_latency:
+            line["single_scan_latency"] = single_scan_latency(dev, a.normals)
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
