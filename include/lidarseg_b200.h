@@ -194,6 +194,35 @@ int lseg_dilate_chebyshev(int32_t frames, int32_t rings, int32_t steps, const ui
                           int32_t radius, uint8_t* out, void* workspace, size_t workspace_bytes,
                           void* stream);
 
+/* ---- scan simulator (reference simulate.py:59-448).
+ * A scene is n_prims packed records of LSEG_PRIM_STRIDE doubles (layout in
+ * csrc/lseg_sim.cu, built by simulate.py:_pack); ties between primitives keep
+ * the earlier one, as cast_grid does. */
+#define LSEG_PRIM_STRIDE 24
+
+/* Replaces cast_grid (simulate.py:383-401), batched: frames x (rings, steps)
+ * beams, t_out = nearest hit (+inf if none), ids_out = surface id (0 if none).
+ * poses (frames, 12) = row-major rotation of the beam directions then the
+ * sensor origin, or NULL for the reference's origin-centred scan. */
+int lseg_cast_grid(const lseg_sensor* sensor, int32_t frames, const double* prims, int32_t n_prims,
+                   const double* poses, double* t_out, int32_t* ids_out, void* stream);
+
+/* Replaces ray_intersect (simulate.py:364-380) for n_rays arbitrary rays
+ * (origins, unit directions: (n_rays, 3) each). */
+int lseg_cast_rays(const double* prims, int32_t n_prims, int64_t n_rays, const double* origins,
+                   const double* dirs, double* t_out, int32_t* ids_out, void* stream);
+
+/* scan_scene's noise + range window (simulate.py:404-421): ranges = t
+ * (+ noise where the beam hit; noise may be NULL), NaN + label 0 outside
+ * [r_min, r_max]. */
+int lseg_apply_scan(int64_t n_cells, double r_min, double r_max, const double* t, const int32_t* ids,
+                    const double* noise, double* ranges, int32_t* labels, void* stream);
+
+/* Replaces scene_normals (simulate.py:424-448): (rings, steps, 3) f64,
+ * oriented toward the sensor, NaN where labels == 0. */
+int lseg_scene_normals(const lseg_sensor* sensor, const double* prims, int32_t n_prims,
+                       const double* ranges, const int32_t* labels, double* normals, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

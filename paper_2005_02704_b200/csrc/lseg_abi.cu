@@ -422,4 +422,53 @@ int lseg_dilate_chebyshev(int32_t frames, int32_t rings, int32_t steps, const ui
   return eval_dilate(frames, rings, steps, mask, radius, out, workspace, (cudaStream_t)stream);
 }
 
+
+// ---------------------------------------------------------------- simulator (F3)
+static int check_prims(const double* prims, int32_t n_prims) {
+  if (n_prims < 0) return fail(LSEG_EINVAL, "n_prims must be >= 0");
+  if (n_prims > 0 && !prims) return fail(LSEG_EINVAL, "prims is NULL");
+  return LSEG_OK;
+}
+
+int lseg_cast_grid(const lseg_sensor* sensor, int32_t frames, const double* prims, int32_t n_prims,
+                   const double* poses, double* t_out, int32_t* ids_out, void* stream) {
+  if (!sensor || !sensor->cos_el || !sensor->sin_el || !sensor->cos_az || !sensor->sin_az)
+    return fail(LSEG_EINVAL, "sensor angle tables must be device pointers");
+  if (frames < 0 || sensor->rings < 1 || sensor->steps < 1) return fail(LSEG_EINVAL, "bad shape");
+  if (int e = check_prims(prims, n_prims)) return e;
+  if (frames == 0) return LSEG_OK;
+  if (!t_out || !ids_out) return fail(LSEG_EINVAL, "NULL buffer");
+  launch_cast_grid(*sensor, frames, prims, n_prims, poses, t_out, ids_out, (cudaStream_t)stream);
+  return check_launch("cast_grid");
+}
+
+int lseg_cast_rays(const double* prims, int32_t n_prims, int64_t n_rays, const double* origins, const double* dirs,
+                   double* t_out, int32_t* ids_out, void* stream) {
+  if (n_rays < 0) return fail(LSEG_EINVAL, "n_rays must be >= 0");
+  if (int e = check_prims(prims, n_prims)) return e;
+  if (n_rays == 0) return LSEG_OK;
+  if (!origins || !dirs || !t_out || !ids_out) return fail(LSEG_EINVAL, "NULL buffer");
+  launch_cast_rays(prims, n_prims, n_rays, origins, dirs, t_out, ids_out, (cudaStream_t)stream);
+  return check_launch("cast_rays");
+}
+
+int lseg_apply_scan(int64_t n_cells, double r_min, double r_max, const double* t, const int32_t* ids,
+                    const double* noise, double* ranges, int32_t* labels, void* stream) {
+  if (n_cells < 0) return fail(LSEG_EINVAL, "n_cells must be >= 0");
+  if (n_cells == 0) return LSEG_OK;
+  if (!t || !ids || !ranges || !labels) return fail(LSEG_EINVAL, "NULL buffer");
+  launch_apply_scan(n_cells, r_min, r_max, t, ids, noise, ranges, labels, (cudaStream_t)stream);
+  return check_launch("apply_scan");
+}
+
+int lseg_scene_normals(const lseg_sensor* sensor, const double* prims, int32_t n_prims, const double* ranges,
+                       const int32_t* labels, double* normals, void* stream) {
+  if (!sensor || !sensor->cos_el || !sensor->sin_el || !sensor->cos_az || !sensor->sin_az)
+    return fail(LSEG_EINVAL, "sensor angle tables must be device pointers");
+  if (int e = check_prims(prims, n_prims)) return e;
+  if (!ranges || !labels || !normals) return fail(LSEG_EINVAL, "NULL buffer");
+  launch_scene_normals(*sensor, prims, n_prims, ranges, labels, normals, (cudaStream_t)stream);
+  return check_launch("scene_normals");
+}
+
 }  // extern "C"

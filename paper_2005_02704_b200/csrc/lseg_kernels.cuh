@@ -41,5 +41,13 @@ int eval_counts(int F, int R, int S, const int32_t* pred, const int32_t* truth, 
                 cudaStream_t st);
 int eval_extract(int F, int R, int S, const int32_t* labels, uint8_t* out, void* ws, cudaStream_t st);
 int eval_dilate(int F, int R, int S, const uint8_t* mask, int r, uint8_t* out, void* ws, cudaStream_t st);
+void launch_cast_grid(const lseg_sensor& sn, int F, const double* prims, int n_prims, const double* poses,
+                      double* t, int32_t* id, cudaStream_t st);
+void launch_cast_rays(const double* prims, int n_prims, int64_t n, const double* origins, const double* dirs,
+                      double* t, int32_t* id, cudaStream_t st);
+void launch_apply_scan(int64_t n, double r_min, double r_max, const double* t, const int32_t* id,
+                       const double* noise, double* ranges, int32_t* labels, cudaStream_t st);
+void launch_scene_normals(const lseg_sensor& sn, const double* prims, int n_prims, const double* ranges,
+                          const int32_t* labels, double* out, cudaStream_t st);
 void launch_selftest_math(int64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t st);
 }  // namespace lseg

@@ -1,0 +1,263 @@
+"""Scan simulator against the reference simulator.
+
+Golden files (tests/golden/sim*.npz, made by make_golden_sim.py from the
+reference) hold generated scenes, the reference's cast_grid, scan_scene and
+scene_normals.  Scene generation is host numpy and must reproduce the
+reference's records exactly.  The reference evaluates its dot products with
+BLAS (summation order / FMA depend on the host CPU), so ray-cast ranges are
+compared with rtol 1e-12 and surface ids must agree on all but near-tie
+cells (two primitives within 1e-9 relative of each other, or a grazing
+boundary), at most 1 in 10^4 cells.  The other tests restate the reference's
+own simulator tests (pkg/tests/test_simulate.py).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_names, load_golden
+
+SIM = golden_names("sim")
+
+
+@pytest.fixture(scope="module")
+def L():
+    import paper_2005_02704_b200 as L
+    return L
+
+
+def _scene_from_golden(L, g):
+    sc = L.generate_scene(int(g["seed"]), crowding=float(g["crowding"]))
+    if len(g["records"]) > len(sc.primitives):  # sim3 adds a ramp and an overhead patch
+        extra = (L.Plane(point=(6.0, -4.0, -1.0), normal=(0.0, 0.3, 1.0), surface_id=900, extent=(3.0, 2.0)),
+                 L.Plane(point=(0.0, 0.0, 4.0), normal=(0.0, 0.0, -1.0), surface_id=901, extent=(5.0, 5.0)))
+        sc = L.Scene(primitives=sc.primitives + extra, seed=sc.seed)
+    return sc
+
+
+def _config(L, g):
+    return L.SensorConfig.uniform(rings=int(g["rings"]), top_deg=float(g["top"]), bottom_deg=float(g["bottom"]),
+                                  azimuth_steps=int(g["steps"]), r_min=0.5, r_max=100.0,
+                                  noise_sigma=float(g["sigma"]))
+
+
+@pytest.mark.parametrize("name", SIM)
+def test_scene_generation_matches_reference(name):
+    import paper_2005_02704_b200 as L
+    from paper_2005_02704_b200.simulate import _record
+    g = load_golden(name)
+    sc = _scene_from_golden(L, g)
+    got = np.stack([_record(p) for p in sc.primitives])
+    np.testing.assert_array_equal(got, g["records"])
+    np.testing.assert_array_equal(_config(L, g).ring_elevations, g["elev"])
+
+
+def _ids_agree(got_t, got_id, want_t, want_id):
+    same_inf = np.isinf(got_t) == np.isinf(want_t)
+    fin = np.isfinite(got_t) & np.isfinite(want_t)
+    np.testing.assert_allclose(got_t[fin], want_t[fin], rtol=1e-12, atol=0)
+    bad = (got_id != want_id) | ~same_inf
+    assert bad.sum() <= max(1, got_t.size // 10000), f"{bad.sum()} cells disagree"
+    return bad
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", SIM)
+def test_cast_grid_vs_reference(L, name):
+    g = load_golden(name)
+    sc, cfg = _scene_from_golden(L, g), _config(L, g)
+    t, ids = L.cast_grid(sc, cfg)
+    _ids_agree(t, ids, g["t"], g["ids"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", SIM)
+def test_scan_scene_and_normals_vs_reference(L, name):
+    g = load_golden(name)
+    sc, cfg = _scene_from_golden(L, g), _config(L, g)
+    grid = L.scan_scene(sc, cfg)
+    r, wr = grid.ranges, g["ranges"]
+    both = np.isfinite(r) & np.isfinite(wr)
+    np.testing.assert_allclose(r[both], wr[both], rtol=1e-12, atol=0)
+    bad = (np.isfinite(r) != np.isfinite(wr)) | (grid.truth_labels != g["labels"])
+    assert bad.sum() <= max(1, r.size // 10000)
+    n = L.scene_normals(sc, grid)
+    ok = (grid.truth_labels == g["labels"]) & (grid.truth_labels > 0)
+    np.testing.assert_allclose(n[ok], g["normals"][ok], rtol=0, atol=1e-12)
+    assert np.isnan(n[grid.truth_labels == 0]).all()
+
+
+# ---- restated reference unit tests (pkg/tests/test_simulate.py)
+
+def _cfg(L, rings=4, steps=8, r_min=0.5, r_max=100.0, top_deg=10.0, bottom_deg=-30.0, noise_sigma=0.0):
+    return L.SensorConfig.uniform(rings=rings, top_deg=top_deg, bottom_deg=bottom_deg, azimuth_steps=steps,
+                                  r_min=r_min, r_max=r_max, noise_sigma=noise_sigma)
+
+
+def _ground(L):
+    return L.Scene(primitives=(L.Plane(point=(0.0, 0.0, -1.0), normal=(0.0, 0.0, 1.0), surface_id=1),), seed=7)
+
+
+@pytest.mark.gpu
+def test_ray_intersect_closed_forms(L):
+    s = L.Sphere(center=(5.0, 0.0, 0.0), radius=1.0, surface_id=1)
+    t, sid = L.ray_intersect(s, (0.0, 0.0, 0.0), (1.0, 0.0, 0.0))
+    assert np.isclose(t, 4.0) and sid == 1
+    assert L.ray_intersect(L.Sphere(center=(-5.0, 0.0, 0.0), radius=1.0, surface_id=1), (0, 0, 0), (1, 0, 0)) is None
+    with pytest.raises(ValueError):
+        L.ray_intersect(s, (0.0, 0.0, 0.0), (2.0, 0.0, 0.0))
+    p = L.Plane(point=(0.0, 0.0, 0.0), normal=(0.0, 0.0, 1.0), surface_id=2)
+    d = np.array([1.0, 0.0, -1.0]) / np.sqrt(2.0)
+    t, sid = L.ray_intersect(p, (0.0, 0.0, 1.0), d)
+    assert np.isclose(t, np.sqrt(2.0)) and sid == 2
+    b = L.Box(center=(3.0, 0.0, 0.0), half_extents=(1.0, 1.0, 1.0), surface_ids=(10, 11, 12, 13, 14, 15))
+    t, sid = L.ray_intersect(b, (0.0, 0.0, 0.0), (1.0, 0.0, 0.0))
+    assert np.isclose(t, 2.0) and sid == 11  # -x face looks at the sensor
+    c = L.Cylinder(base=(5.0, 0.0, -2.0), axis=(0.0, 0.0, 1.0), radius=1.0, height=4.0, surface_ids=(1, 2, 3))
+    assert L.ray_intersect(c, (0.0, 0.0, 0.0), (1.0, 0.0, 0.0)) == pytest.approx((4.0, 1))
+    assert L.ray_intersect(c, (5.0, 0.0, 10.0), (0.0, 0.0, -1.0)) == pytest.approx((8.0, 3))
+    assert L.ray_intersect(c, (5.0, 0.0, -10.0), (0.0, 0.0, 1.0)) == pytest.approx((8.0, 2))
+    k = L.Cone(apex=(5.0, 0.0, 2.0), axis=(0.0, 0.0, -1.0), half_angle=np.pi / 4, height=2.0, surface_ids=(8, 9))
+    assert L.ray_intersect(k, (0.0, 0.0, 1.0), (1.0, 0.0, 0.0)) == pytest.approx((4.0, 8))
+    assert L.ray_intersect(k, (5.5, 0.0, -5.0), (0.0, 0.0, 1.0)) == pytest.approx((5.0, 9))
+
+
+def _inside_fn(L, prim):
+    if isinstance(prim, L.Sphere):
+        return lambda p: np.linalg.norm(p - prim.center) - prim.radius
+    if isinstance(prim, L.Box):
+        return lambda p: np.max(np.abs(prim.rotation.T @ (p - prim.center)) - prim.half_extents)
+    if isinstance(prim, L.Cylinder):
+        def f(p):
+            rel = p - prim.base
+            s = rel @ prim.axis
+            return max(np.linalg.norm(rel - s * prim.axis) - prim.radius, -s, s - prim.height)
+        return f
+
+    def g(p):
+        rel = p - prim.apex
+        s = rel @ prim.axis
+        return max(np.linalg.norm(rel - s * prim.axis) - abs(s) * np.tan(prim.half_angle), -s, s - prim.height)
+    return g
+
+
+def _march(f, d, t_max=30.0, coarse=2e-3):
+    """Independent oracle: first sign change of the implicit function along
+    the ray, refined by bisection."""
+    ts = np.arange(coarse, t_max, coarse)
+    vals = np.array([f(t * d) for t in ts])
+    hit = np.nonzero(vals <= 0.0)[0]
+    if hit.size == 0:
+        return None
+    hi = ts[hit[0]]
+    lo = hi - coarse
+    for _ in range(60):
+        mid = 0.5 * (lo + hi)
+        if f(mid * d) <= 0.0:
+            hi = mid
+        else:
+            lo = mid
+    return 0.5 * (lo + hi)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(2))
+def test_solids_match_march_oracle(L, seed):
+    rng = np.random.default_rng(seed)
+    prims = [L.Sphere(center=(6.0, 1.0, -0.5), radius=1.8, surface_id=1),
+             L.Box(center=(5.0, -3.0, 0.0), half_extents=(1.5, 1.0, 2.0), rotation=L.rotation_rpy(yaw=0.4, pitch=0.2),
+                   surface_ids=range(2, 8)),
+             L.Cylinder(base=(4.0, 4.0, -2.0), axis=np.array((0.1, 0.0, 1.0)) / np.linalg.norm((0.1, 0.0, 1.0)),
+                        radius=1.2, height=3.5, surface_ids=(8, 9, 10)),
+             L.Cone(apex=(7.0, 0.0, 3.0), axis=(0.0, 0.0, -1.0), half_angle=0.5, height=3.0, surface_ids=(11, 12))]
+    for prim in prims:
+        f = _inside_fn(L, prim)
+        target = getattr(prim, "center", None)
+        if target is None:
+            target = getattr(prim, "base", getattr(prim, "apex", np.zeros(3)))
+        for _ in range(6):
+            aim = target + rng.normal(scale=1.5, size=3)
+            d = aim / np.linalg.norm(aim)
+            hit = L.ray_intersect(prim, (0.0, 0.0, 0.0), d)
+            oracle = _march(f, d)
+            if oracle is None:
+                assert hit is None or hit[0] > 29.0
+            else:
+                assert hit is not None and np.isclose(hit[0], oracle, atol=1e-6)
+
+
+@pytest.mark.gpu
+def test_scan_scene_properties(L):
+    assert L.scan_scene(L.Scene(primitives=(), seed=0), _cfg(L, 4, 12)).valid_mask.sum() == 0
+    ground = _ground(L)
+    cfg = _cfg(L, rings=8, steps=24, bottom_deg=-40.0)
+    grid = L.scan_scene(ground, cfg)
+    for ring, theta in enumerate(cfg.ring_elevations):  # closed form 1/sin(-theta)
+        expected = 1.0 / np.sin(-theta) if theta < 0 else np.inf
+        if np.isfinite(expected) and cfg.r_min <= expected <= cfg.r_max:
+            assert np.allclose(grid.ranges[ring], expected, rtol=1e-12)
+            assert np.all(grid.truth_labels[ring] == 1)
+        else:
+            assert not grid.valid_mask[ring].any() and np.all(grid.truth_labels[ring] == 0)
+    noisy = _cfg(L, rings=6, steps=30, noise_sigma=0.1, bottom_deg=-40.0)
+    a, b = L.scan_scene(ground, noisy), L.scan_scene(ground, noisy)
+    np.testing.assert_array_equal(a.ranges, b.ranges)
+    assert not np.array_equal(a.ranges, L.scan_scene(ground, noisy, seed=99).ranges)
+    base = L.scan_scene(ground, _cfg(L, rings=10, steps=60, bottom_deg=-40.0))
+    occ = L.Sphere(center=(3.0, 0.0, -0.5), radius=1.0, surface_id=5)
+    both = L.scan_scene(L.Scene(primitives=ground.primitives + (occ,), seed=7), _cfg(L, rings=10, steps=60,
+                                                                                    bottom_deg=-40.0))
+    m = base.valid_mask & both.valid_mask
+    assert np.all(both.ranges[m] <= base.ranges[m] + 1e-12)
+    # noise statistics over >= 1e5 ground cells
+    cn = _cfg(L, rings=64, steps=2000, top_deg=-5.0, bottom_deg=-45.0, noise_sigma=0.1)
+    c0 = _cfg(L, rings=64, steps=2000, top_deg=-5.0, bottom_deg=-45.0)
+    gn, g0 = L.scan_scene(ground, cn), L.scan_scene(ground, c0)
+    mk = gn.valid_mask & g0.valid_mask
+    assert mk.sum() >= 100_000
+    delta = (gn.ranges - g0.ranges)[mk]
+    assert abs(delta.mean()) <= 0.01 and 0.09 <= delta.std() <= 0.11
+    # dropped returns lose their labels
+    cd = _cfg(L, rings=4, steps=400, top_deg=-9.0, bottom_deg=-11.0, r_max=1.0 / np.sin(np.radians(10.0)) + 0.05,
+              noise_sigma=0.2)
+    gd = L.scan_scene(L.Scene(primitives=(L.Plane(point=(0, 0, -1.0), normal=(0, 0, 1), surface_id=1),), seed=11),
+                      cd)
+    assert gd.valid_mask.any() and np.all((gd.truth_labels > 0) == gd.valid_mask)
+    assert (~gd.valid_mask & (gd.truth_labels == 0)).any()
+
+
+@pytest.mark.gpu
+def test_box_faces_and_normals(L):
+    cfg = _cfg(L, rings=24, steps=240, top_deg=20.0, bottom_deg=-30.0)
+    box = L.Box(center=(4.0, 0.0, 0.5), half_extents=(1.0, 1.0, 1.0), rotation=L.rotation_rpy(yaw=0.5),
+                surface_ids=(2, 3, 4, 5, 6, 7))
+    seen = set(np.unique(L.scan_scene(L.Scene(primitives=(box,), seed=0), cfg).truth_labels)) - {0}
+    assert len(seen) >= 2 and seen <= {2, 3, 4, 5, 6, 7}
+    ground = _ground(L)
+    gs = L.scan_scene(ground, _cfg(L, rings=8, steps=24, bottom_deg=-40.0))
+    n = L.scene_normals(ground, gs)
+    assert np.allclose(n[gs.valid_mask], [0.0, 0.0, 1.0], atol=1e-12)
+    cs = _cfg(L, rings=24, steps=240, top_deg=20.0, bottom_deg=-20.0)
+    sph = L.Sphere(center=(6.0, 0.0, 0.0), radius=2.0, surface_id=3)
+    sc = L.Scene(primitives=(sph,), seed=0)
+    grid = L.scan_scene(sc, cs)
+    n = L.scene_normals(sc, grid)
+    pts, m = grid.points(), grid.valid_mask
+    radial = pts[m] - sph.center
+    radial /= np.linalg.norm(radial, axis=1, keepdims=True)
+    assert np.allclose(n[m], radial, atol=1e-9)
+    assert np.all(np.einsum("ij,ij->i", n[m], pts[m]) <= 0.0)
+
+
+def test_scene_validation():
+    import paper_2005_02704_b200 as L
+    with pytest.raises(ValueError):
+        L.Scene(primitives=(L.Sphere(center=(1, 0, 0), radius=1, surface_id=1),
+                            L.Sphere(center=(4, 0, 0), radius=1, surface_id=1)), seed=0)
+    with pytest.raises(ValueError):
+        L.Sphere(center=(0, 0, 0), radius=-1.0, surface_id=1)
+    with pytest.raises(ValueError):
+        L.Cylinder(base=(0, 0, 0), axis=(0, 0, 0), radius=1, height=1, surface_ids=(1, 2, 3))
+    with pytest.raises(ValueError):
+        L.Cone(apex=(0, 0, 0), axis=(0, 0, 1), half_angle=2.0, height=1, surface_ids=(1, 2))
+    with pytest.raises(ValueError):
+        L.Box(center=(0, 0, 0), half_extents=(1, 0, 1), surface_ids=range(1, 7))
