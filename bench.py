@@ -256,6 +256,24 @@ def single_scan_latency(dev, normals="exact", reps=200):
     return out
 
 
+def suite_accuracy(dev, normals="exact", n_scenes=64):
+    """SURVEY.md §8(f) F1 + F3 at batch scale: the paper's edge P/R/F1 of the
+    pipeline's labels against simulator truth, over a generated suite of
+    scenes (reference scenes.generate_suite) scanned by the GPU simulator at the
+    HDL-64 shape; mean over scenes per interval."""
+    import paper_2005_02704_b200 as L
+    sensor = L.SensorConfig(ring_elevations=np.radians(np.linspace(2.0, -24.9, 64)), azimuth_steps=2048,
+                            r_min=0.5, r_max=120.0, noise_sigma=0.02)
+    cfg = L.PipelineConfig(sensor=sensor, intervals=(1, 5))
+    scenes = L.generate_suite(2005, n_scenes)
+    rows = L.run_suite(scenes, cfg, normals=normals, device=dev)
+    out = {"scenes": n_scenes, "generator": "generate_suite(2005, n) on HDL-64 shape, noise 0.02 m"}
+    for k in cfg.intervals:
+        rr = [r for r in rows if r["interval"] == k]
+        out[f"interval_{k}"] = {m: float(np.mean([r[m] for r in rr])) for m in ("precision", "recall", "f1")}
+    return out
+
+
 def main():
     a = parse()
     from paper_2005_02704_b200 import synth
@@ -408,6 +426,7 @@ def main():
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk}
         if not a.no_latency:
             line["single_scan_latency"] = single_scan_latency(dev, a.normals)
+            line["accuracy_vs_truth"] = suite_accuracy(dev, a.normals)
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()

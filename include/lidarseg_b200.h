@@ -173,6 +173,16 @@ int lseg_run_pipeline_ex(const lseg_sensor* sensor, int32_t frames, int32_t inte
                          int32_t* n_nodes, int32_t* n_labels, void* workspace, size_t workspace_bytes,
                          void* stream);
 
+/* Batched run_pipeline on range grids (reference run_pipeline(scan, cfg),
+ * pipeline.py:47-70, over F frames): ranges (F, R, S) f64 with NaN = INVALID
+ * as input instead of points; outputs and flags (LSEG_PIPE_CERT_NORMALS) as
+ * in lseg_run_pipeline_ex. */
+int lseg_run_pipeline_grid(const lseg_sensor* sensor, int32_t frames, int32_t interval,
+                           const double* thresholds, int32_t min_segment_size, uint32_t flags,
+                           const double* ranges, int32_t* node_ids, int32_t* neighbors, float* normals32,
+                           uint8_t* nmask, int32_t* node_labels, int32_t* labels, int32_t* n_nodes,
+                           int32_t* n_labels, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- edge-based evaluation (reference evaluate.py:40-94).
  * Label grids (F,R,S) i32, 0 = unlabelled.  Scratch sized by
  * lseg_eval_workspace_bytes. */

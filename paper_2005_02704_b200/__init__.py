@@ -18,6 +18,7 @@ from .pipeline import BatchPipeline, PipelineConfig, PipelineResult, StreamingPi
 from .scan import (INVALID, GridIndex, Point3, ScanGrid, SensorConfig, polar_to_cartesian, subsample_steps,
                    valid_point)
 from .scenes import generate_scene, generate_suite
+from .suite import run_suite, scan_scenes
 from .segment import SegmenterConfig, backfill, prune_small, segment
 from .simulate import (Box, Cone, Cylinder, Plane, Scene, Sphere, cast_grid, cast_grid_batch, ray_intersect,
                        rotation_rpy, scan_scene, scene_normals)

@@ -20,6 +20,7 @@ from . import _lib
 from .mesh import Mesh, build_mesh
 from .normals import NormalMap, estimate_normals_device
 from .scan import ScanGrid, SensorConfig, device_tables, subsample_steps
+from .evaluate import EvalConfig
 from .segment import SegmenterConfig, backfill_device, prune_small_device, segment_device
 
 
@@ -29,7 +30,7 @@ class PipelineConfig:
     interval: int = 5
     intervals: tuple = (5, 10, 15)
     segmenter: SegmenterConfig = field(default_factory=SegmenterConfig)
-    eval: object = None       # reference EvalConfig (out of scope here)
+    eval: EvalConfig = field(default_factory=EvalConfig)
     baseline: object = None   # reference BaselineConfig (out of scope here)
 
     def __post_init__(self):
@@ -175,6 +176,28 @@ class BatchPipeline:
         for st in self.streams:
             cur.wait_stream(st)
         return self.labels
+
+    def run_grid(self, ranges: torch.Tensor) -> torch.Tensor:
+        """The batch from range grids (F, R, S) f64 (NaN = INVALID) instead of
+        points -- the batched form of the reference's run_pipeline(scan)
+        (lseg_run_pipeline_grid).  ``self.ranges`` is not touched."""
+        F = int(ranges.shape[0])
+        if F > self.frames or tuple(ranges.shape[1:]) != (self.config.rings, self.config.azimuth_steps):
+            raise ValueError("ranges must be (frames <= capacity, rings, azimuth_steps)")
+        ranges = ranges.to(device=self.device, dtype=torch.float64).contiguous()
+        flags = _lib.PIPE_CERT_NORMALS if self.normals_mode == "certified" else 0
+        for (f0, f1), ws in zip(self.chunks, self.ws):  # one workspace per chunk, sequential
+            f1 = min(f1, F)
+            if f0 >= f1:
+                break
+            sl = lambda t: None if t is None else t[f0:f1]
+            _lib.check(self.L.lseg_run_pipeline_grid(
+                self.sn, f1 - f0, self.interval, self.thr, int(self.seg.min_segment_size), flags,
+                _lib.ptr(ranges[f0:f1]), _lib.ptr(sl(self.node_ids)), _lib.ptr(sl(self.neighbors)),
+                _lib.ptr(sl(self.normals)), _lib.ptr(sl(self.nmask)), _lib.ptr(sl(self.node_labels)),
+                _lib.ptr(sl(self.labels)), _lib.ptr(sl(self.n_nodes)), _lib.ptr(sl(self.n_labels)), _lib.ptr(ws),
+                self.ws_bytes, _lib.stream_ptr()))
+        return self.labels[:F]
 
     def capture(self, xyz, ring, offsets) -> "torch.cuda.CUDAGraph":
         """Capture ``run`` on these (fixed) input buffers as one CUDA graph --

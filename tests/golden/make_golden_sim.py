@@ -74,10 +74,20 @@ def main(ref_src="/root/reference/pkg/src"):
         t, ids = L.cast_grid(scene, cfg)
         grid = L.scan_scene(scene, cfg)
         nrm = L.scene_normals(scene, grid)
+        # suite: the pipeline on the reference's own scan + edge P/R/F1 vs truth
+        pcfg = L.PipelineConfig(sensor=cfg, intervals=(1, 5))
+        suite = {}
+        prf = []
+        for k in (1, 5):
+            res = L.run_pipeline(grid, pcfg, interval=k)
+            rep = L.edge_prf(res.labels, grid.truth_labels, pcfg.eval)
+            suite[f"suite_labels_k{k}"] = res.labels
+            prf.append([rep.precision, rep.recall, rep.f1])
         np.savez_compressed(os.path.join(HERE, f"sim{i}.npz"), seed=seed, crowding=crowd, rings=R, steps=S,
                             top=top, bottom=bot, sigma=sigma, elev=cfg.ring_elevations,
                             records=np.stack([pack_reference(p) for p in scene.primitives]),
-                            t=t, ids=ids, ranges=grid.ranges, labels=grid.truth_labels, normals=nrm)
+                            t=t, ids=ids, ranges=grid.ranges, labels=grid.truth_labels, normals=nrm,
+                            suite_prf=np.array(prf), **suite)
     print(f"wrote {len(cases)} simulator golden files to {HERE}")
 
 

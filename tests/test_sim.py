@@ -261,3 +261,36 @@ def test_scene_validation():
         L.Cone(apex=(0, 0, 0), axis=(0, 0, 1), half_angle=2.0, height=1, surface_ids=(1, 2))
     with pytest.raises(ValueError):
         L.Box(center=(0, 0, 0), half_extents=(1, 0, 1), surface_ids=range(1, 7))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", SIM)
+def test_pipeline_grid_and_suite_metrics_vs_reference(L, name):
+    """Batched run_pipeline on the reference's own scan (BatchPipeline.run_grid)
+    gives the reference's labels bit-for-bit at k = 1 and 5, hence the same
+    edge P/R/F1 vs the truth labels (reference cli `suite` numbers)."""
+    import torch
+    g = load_golden(name)
+    cfg = _config(L, g)
+    ranges = torch.from_numpy(g["ranges"][None]).cuda()
+    truth = torch.from_numpy(g["labels"][None].astype(np.int32)).cuda()
+    for j, k in enumerate((1, 5)):
+        for normals in ("exact", "certified"):
+            bp = L.BatchPipeline(cfg, k, frames=1, normals=normals)
+            labels = bp.run_grid(ranges)
+            np.testing.assert_array_equal(labels[0].cpu().numpy(), g[f"suite_labels_k{k}"])
+            prf = L.edge_prf_batch(labels, truth, 2).cpu().numpy()[0]
+            np.testing.assert_allclose(prf, g["suite_prf"][j], rtol=0, atol=1e-15)
+
+
+@pytest.mark.gpu
+def test_run_suite_end_to_end(L):
+    """Scan (GPU simulator) -> batched pipeline -> batched edge P/R/F1 over a
+    small suite; agrees with the reference's numbers on the same scenes up to
+    the simulator's last-ulp differences."""
+    gs = [load_golden(n) for n in SIM if int(load_golden(n)["rings"]) == 16]
+    g = gs[0]
+    cfg = L.PipelineConfig(sensor=_config(L, g), intervals=(1, 5))
+    rows = L.run_suite([_scene_from_golden(L, g)], cfg)
+    got = np.array([[r["precision"], r["recall"], r["f1"]] for r in rows])
+    np.testing.assert_allclose(got, g["suite_prf"], rtol=0, atol=2e-3)
