@@ -233,6 +233,16 @@ int lseg_apply_scan(int64_t n_cells, double r_min, double r_max, const double* t
 int lseg_scene_normals(const lseg_sensor* sensor, const double* prims, int32_t n_prims,
                        const double* ranges, const int32_t* labels, double* normals, void* stream);
 
+/* ---- text formats (reference io.py).  Host-side, no
+ * device needed.  Formats n_rows rows of n_cols values (row-major doubles):
+ * col_kind[c] = 0 -> Python repr(float) text (io.py:42-47, shortest
+ * round-trip), 1 -> integer; cells joined by ' ', rows ended by '\n'.
+ * out = NULL returns an upper bound of the bytes needed; otherwise returns the
+ * bytes written (-2 if capacity is too small, -1 on bad arguments).
+ * threads <= 0: all hardware threads. */
+int64_t lseg_format_rows(int64_t n_rows, int32_t n_cols, const double* values, const uint8_t* col_kind,
+                         char* out, int64_t capacity, int32_t threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,7 +15,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC]
-SOURCES = ["lseg_kernels.cu", "lseg_fused.cu", "lseg_eval.cu", "lseg_sim.cu", "lseg_abi.cu"]
+SOURCES = ["lseg_kernels.cu", "lseg_fused.cu", "lseg_eval.cu", "lseg_sim.cu", "lseg_format.cpp", "lseg_abi.cu"]
 
 
 def _deps():
@@ -39,7 +39,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     os.makedirs(objdir, exist_ok=True)
 
     def compile_one(src):
-        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        obj = os.path.join(objdir, src.rsplit(".", 1)[0] + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, *["-D" + d for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:

@@ -25,13 +25,34 @@ from .segment import SegmenterConfig, backfill_device, prune_small_device, segme
 
 
 @dataclass(frozen=True)
+class BaselineConfig:
+    """Parameters of the reference's region-growing comparison baseline
+    (reference baseline.py:21-35).  Only the configuration is mirrored (it is
+    part of the LSEGCFG1 format); the baseline algorithm itself is off the
+    hot path and not built."""
+
+    k_neighbors: int = 30
+    angle_threshold: float = float(np.radians(3.0))
+    curvature_threshold: float = 0.05
+    min_cluster_size: int = 50
+
+    def __post_init__(self):
+        if self.k_neighbors < 3:
+            raise ValueError("k_neighbors must be >= 3")
+        if not (0.0 < self.angle_threshold < np.pi / 2):
+            raise ValueError("angle_threshold must be in (0, pi/2) radians")
+        if self.min_cluster_size < 0:
+            raise ValueError("min_cluster_size must be >= 0")
+
+
+@dataclass(frozen=True)
 class PipelineConfig:
     sensor: SensorConfig = field(default_factory=SensorConfig.default)
     interval: int = 5
     intervals: tuple = (5, 10, 15)
     segmenter: SegmenterConfig = field(default_factory=SegmenterConfig)
     eval: EvalConfig = field(default_factory=EvalConfig)
-    baseline: object = None   # reference BaselineConfig (out of scope here)
+    baseline: BaselineConfig = field(default_factory=BaselineConfig)
 
     def __post_init__(self):
         if self.interval < 1:
