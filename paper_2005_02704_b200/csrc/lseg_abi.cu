@@ -15,6 +15,7 @@
 #include "lseg_kernels.cuh"
 
 namespace lseg {
+void debug_tile_cc(int n, const unsigned long long* masks, int32_t* parent, uint32_t* lroots);
 
 static thread_local std::string g_last_error;
 
@@ -412,6 +413,10 @@ int lseg_run_pipeline_grid(const lseg_sensor* sensor, int32_t frames, int32_t in
 }
 
 void lseg_debug_cert_err(float* per_node_err) { g_dbg_err = per_node_err; }
+
+void lseg_debug_tile_cc(int n, const unsigned long long* masks, int32_t* parent, uint32_t* lroots) {
+  lseg::debug_tile_cc(n, masks, parent, lroots);
+}
 
 // ---------------------------------------------------------------- evaluator (F1)
 size_t lseg_eval_workspace_bytes(int32_t frames, int32_t rings, int32_t steps) {

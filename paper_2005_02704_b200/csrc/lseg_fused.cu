@@ -12,6 +12,7 @@
 //              histogram, in one pass (replaces label_dense + backfill).
 #include <cub/block/block_scan.cuh>
 #include <cuda_fp16.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "lseg_internal.cuh"
@@ -44,6 +45,9 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #endif
 #ifndef LSEG_CC_SV
 #define LSEG_CC_SV 1
+#endif
+#ifndef LSEG_CC_MINB
+#define LSEG_CC_MINB 8
 #endif
 #ifndef LSEG_CERT_IDMASK
 #define LSEG_CERT_IDMASK 1
@@ -1280,61 +1284,69 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
 #if LSEG_CC_SV
   // Run-level label propagation (Shiloach-Vishkin style, every thread doing
   // the same work -- the serial union-find chains of divergent lanes were the
-  // cost here): labels live at run starts, L[start] <= start.  Hook: for every
-  // kept vertical edge link the larger of the two current labels to the
-  // smaller (atomicMin); shortcut: L[a] = L[L[a]].  Repeat until nothing
-  // changes; then every run's label is its component's minimum run start.
+  // cost here): labels live at run starts, L[start] <= start, and every other
+  // cell keeps s_par = its run start throughout.  Hook: for every kept
+  // vertical edge link the larger of the two current labels to the smaller
+  // (atomicMin); shortcut (run starts only): L[a] = L[L[a]].  Repeat until
+  // nothing changes; then every run's label is its component's minimum run
+  // start.  A thread's edges live in registers, packed as
+  // a | b0 << 10 | b1 << 20 | valid bits << 30 (10-bit tile cell indices).
+  static_assert(NT <= 1024, "10-bit cell indices");
   constexpr int NJ = (NT + T - 1) / T;
-  int ea[2 * NJ + 2], eb[2 * NJ + 2];
-  int ne = 0;
+  unsigned pk[NJ];
+  unsigned starts = 0;  // which of this thread's cells are run starts
+  int any = 0;
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
     const int e = threadIdx.x + j * T;
     const int y = e / TC, x = e - y * TC;
+    pk[j] = 0;
     if (e < NT) {
-      const unsigned long long Zs = ~s_m[y * 5] & ((1ull << x) - 1ull);
-      const int a = y * TC + (Zs ? 64 - __clzll((long long)Zs) : 0);
-      if ((s_U[2 * y] >> x) & 1ull) {
-        const int t = e + TC;
-        const unsigned long long Zt = ~s_m[(y + 1) * 5] & ((1ull << x) - 1ull);
-        ea[ne] = a; eb[ne] = (y + 1) * TC + (Zt ? 64 - __clzll((long long)Zt) : 0); ++ne;
-        (void)t;
-      }
-      if ((s_U[2 * y + 1] >> x) & 1ull) {
-        const int xt = x + 1;
-        const unsigned long long Zt = ~s_m[(y + 1) * 5] & ((1ull << xt) - 1ull);
-        ea[ne] = a; eb[ne] = (y + 1) * TC + (Zt ? 64 - __clzll((long long)Zt) : 0); ++ne;
-      }
+      const int a = s_par[e];
+      if (a == e) starts |= 1u << j;
+      const bool u0 = (s_U[2 * y] >> x) & 1ull, u1 = (s_U[2 * y + 1] >> x) & 1ull;
+      const unsigned b0 = u0 ? (unsigned)s_par[e + TC] : 0u, b1 = u1 ? (unsigned)s_par[e + TC + 1] : 0u;
+      pk[j] = (unsigned)a | b0 << 10 | b1 << 20 | (u0 ? 1u << 30 : 0u) | (u1 ? 2u << 30 : 0u);
+      any |= u0 | u1;
     }
   }
+  unsigned pw = 0;
   if (threadIdx.x < TRe) {  // full-width column wrap (x = S'-1 -> 0)
     const int y = threadIdx.x;
     const unsigned W = (unsigned)s_m[y * 5 + 4];
-    const int x = TCe - 1;
-    const unsigned long long Zs = ~s_m[y * 5] & ((1ull << x) - 1ull);
-    const int a = y * TC + (Zs ? 64 - __clzll((long long)Zs) : 0);
-    if (W & 1u) { ea[ne] = a; eb[ne] = y * TC; ++ne; }
-    if (W & 2u) { ea[ne] = a; eb[ne] = (y + 1) * TC; ++ne; }
+    const unsigned a = (unsigned)s_par[y * TC + TCe - 1];
+    const bool w0 = W & 1u, w1 = (W & 2u) && (y + 1 < TRe);
+    // (y + 1) * TC is 1024 on the last row: only packed when that edge exists
+    pw = a | (unsigned)(y * TC) << 10 | (w1 ? (unsigned)((y + 1) * TC) << 20 : 0u) | (w0 ? 1u << 30 : 0u) |
+         (w1 ? 2u << 30 : 0u);
+    any |= w0 | w1;
   }
-  while (true) {
-    int changed = 0;
-    for (int k = 0; k < ne; ++k) {
-      const int la = s_par[ea[k]], lb = s_par[eb[k]];
-      if (la != lb) {
-        const int hi = max(la, lb), lo = min(la, lb);
-        changed |= atomicMin(s_par + hi, lo) > lo;
-      }
-    }
-    __syncthreads();
+  auto hook = [&](unsigned ia, unsigned ib) -> int {
+    const int la = s_par[ia], lb = s_par[ib];
+    if (la == lb) return 0;
+    const int hi = max(la, lb), lo = min(la, lb);
+    return atomicMin(s_par + hi, lo) > lo;
+  };
+  if (__syncthreads_or(any)) {
+    while (true) {
+      int changed = 0;
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) {  // shortcut
-      const int e = threadIdx.x + j * T;
-      if (e >= NT) break;
-      const int l = s_par[e];
-      const int ll = s_par[l];
-      if (ll != l) { s_par[e] = ll; changed = 1; }
+      for (int j = 0; j <= NJ; ++j) {
+        const unsigned v = j < NJ ? pk[j] : pw;
+        if (v & (1u << 30)) changed |= hook(v & 1023u, (v >> 10) & 1023u);
+        if (v & (2u << 30)) changed |= hook(v & 1023u, (v >> 20) & 1023u);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {  // shortcut at run starts
+        if (!((starts >> j) & 1u)) continue;
+        const int e = threadIdx.x + j * T;
+        const int l = s_par[e];
+        const int ll = s_par[l];
+        if (ll != l) { s_par[e] = ll; changed = 1; }
+      }
+      if (!__syncthreads_or(changed)) break;
     }
-    if (!__syncthreads_or(changed)) break;
   }
 #else
   for (int e = threadIdx.x; e < NT; e += T) {
@@ -1365,8 +1377,12 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
     const bool in = (y < TRe && x < TCe);
     int pc = -1;
     if (in && ((s_m[y * 5 + 3] >> x) & 1ull)) {
+#if LSEG_CC_SV
+      const int lr = s_par[s_par[e]];  // run start -> its label
+#else
       const unsigned long long Z = ~s_m[y * 5] & ((1ull << x) - 1ull);
       const int lr = s_par[y * TC + (Z ? 64 - __clzll((long long)Z) : 0)];
+#endif
       pc = (r0 + lr / TC) * sh.Sk + c0 + lr % TC;
     }
     const int cell = (r0 + y) * sh.Sk + c0 + x;
@@ -1377,8 +1393,26 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
   }
 }
 
+// Test hook (lseg_debug_tile_cc): the tile CC body on given pass masks, one
+// 16 x 64 tile per "frame" (tests/test_gpu_math.py checks it against a CPU
+// union-find over the same edges).
 template <int TR, int TC, int T>
-__global__ void __launch_bounds__(T) k_tile_cc(Shape sh, const unsigned long long* __restrict__ masks,
+__global__ void k_tile_cc_dbg(Shape sh, const unsigned long long* __restrict__ masks, int32_t* parent,
+                              uint32_t* lroots) {
+  __shared__ int s_par[TR * TC];
+  __shared__ unsigned long long s_m[TR * 5];
+  const int f = blockIdx.x;
+  for (int j = threadIdx.x; j < TR * 5; j += T) s_m[j] = masks[(int64_t)f * TR * 5 + j];
+  __syncthreads();
+  tile_cc_body<TR, TC, T>(sh, f, 0, 0, TR, TC, s_m, s_par, parent, lroots);
+}
+void debug_tile_cc(int n, const unsigned long long* masks, int32_t* parent, uint32_t* lroots) {
+  const Shape sh = make_shape(n, TILE_R, TILE_C, 1);
+  k_tile_cc_dbg<TILE_R, TILE_C, 256><<<n, 256>>>(sh, masks, parent, lroots);
+}
+
+template <int TR, int TC, int T>
+__global__ void __launch_bounds__(T, LSEG_CC_MINB) k_tile_cc(Shape sh, const unsigned long long* __restrict__ masks,
                                                int32_t* __restrict__ parent, uint32_t* __restrict__ lroots) {
   __shared__ int s_par[TR * TC];
   __shared__ unsigned long long s_m[TR * 5];

@@ -21,3 +21,61 @@ def test_fast_sqrt_rcp_bit_exact():
         _lib.check(fn(1 << 30, seed, C.c_void_p(bad.data_ptr()), _lib.stream_ptr()))
         torch.cuda.synchronize()
         assert bad.tolist() == [0, 0], f"sqrt / rcp mismatches: {bad.tolist()}"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(3))
+def test_tile_cc_matches_union_find(seed):
+    """The tile-local connected components (k_tile_cc's body, run-level label
+    propagation on the 64-bit pass masks) against a plain CPU union-find over
+    the same horizontal / vertical / diagonal edges: every cell with a normal
+    gets the minimum cell of its component, the rest -1."""
+    import ctypes as C
+    import numpy as np
+    import torch
+    from paper_2005_02704_b200 import _lib
+    lib = _lib.load()
+    fn = lib.lseg_debug_tile_cc
+    fn.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+    rng = np.random.default_rng(seed)
+    n, TR, TC = 256, 16, 64
+    m = np.zeros((n, TR, 5), dtype=np.uint64)
+    pack = lambda b: (b.astype(np.uint64) << np.arange(64, dtype=np.uint64)).sum(axis=1, dtype=np.uint64)
+    want = np.empty((n, TR * TC), dtype=np.int64)
+    for t in range(n):
+        dens = rng.uniform(0.2, 1.0)
+        hs = rng.random((TR, TC)) < rng.uniform(0.6, 1.0)
+        H = (rng.random((TR, TC)) < dens) & hs & np.roll(hs, -1, axis=1)
+        H[:, -1] = False
+        V0 = np.zeros((TR, TC), bool)
+        V1 = np.zeros((TR, TC), bool)
+        V0[:-1] = (rng.random((TR - 1, TC)) < dens) & hs[:-1] & hs[1:]
+        V1[:-1, :-1] = (rng.random((TR - 1, TC - 1)) < dens) & hs[:-1, :-1] & hs[1:, 1:]
+        m[t, :, 0], m[t, :, 1], m[t, :, 2], m[t, :, 3] = pack(H), pack(V0), pack(V1), pack(hs)
+        par = np.arange(TR * TC)
+
+        def find(a):
+            while par[a] != a:
+                par[a] = par[par[a]]
+                a = par[a]
+            return a
+
+        def union(a, b):
+            ra, rb = find(a), find(b)
+            if ra != rb:
+                par[max(ra, rb)] = min(ra, rb)
+
+        for y, x in zip(*np.nonzero(H)):
+            union(y * TC + x, y * TC + x + 1)
+        for y, x in zip(*np.nonzero(V0)):
+            union(y * TC + x, (y + 1) * TC + x)
+        for y, x in zip(*np.nonzero(V1)):
+            union(y * TC + x, (y + 1) * TC + x + 1)
+        roots = np.array([find(i) for i in range(TR * TC)])
+        want[t] = np.where(hs.reshape(-1), roots, -1)
+    mt = torch.from_numpy(m.view(np.int64)).cuda()
+    parent = torch.empty((n, TR * TC), dtype=torch.int32, device="cuda")
+    lroots = torch.empty((n, TR * 2), dtype=torch.int32, device="cuda")
+    fn(n, mt.data_ptr(), parent.data_ptr(), lroots.data_ptr())
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(parent.cpu().numpy(), want)
