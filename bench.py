@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-latency", action="store_true", help="skip the single-scan latency (CUDA graph) lines")
+    ap.add_argument("--e2e-chunk", type=int, default=64, help="frames per streamed chunk in the e2e run")
+    ap.add_argument("--e2e-rings", default="segments", choices=["segments", "u8", "i32"],
+                    help="ring input form of the e2e run: per-frame segment table, or a ring id per point")
     ap.add_argument("--also-interval", type=int, default=5,
                     help="also time this interval (reference default 5); 0 disables")
     ap.add_argument("--seed", type=int, default=2005)
@@ -376,12 +379,18 @@ def main():
     e2e = None
     if not a.no_e2e:
         hx = xyz.cpu().pin_memory()
-        # ring ids travel as one byte each (<= 256 rings): 13 B instead of 16 B per point
-        rdt = torch.uint8 if cfg.rings <= 256 else torch.int32
-        hr = ring.to(rdt).cpu().pin_memory()
         ho = off.cpu()
+        if a.e2e_rings == "segments":
+            # ring-major points carry their rings as a per-frame (R+1) offset
+            # table (LSEG_PIPE_RING_SEGMENTS): 12 B per point on the wire
+            rdt = "segments"
+            hr = L.ring_segments(ring, off, cfg.rings).cpu().pin_memory()
+        else:
+            # one byte per ring id (<= 256 rings): 13 B instead of 16 B per point
+            rdt = torch.uint8 if (a.e2e_rings == "u8" and cfg.rings <= 256) else torch.int32
+            hr = ring.to(rdt).cpu().pin_memory()
         hl = torch.empty(bp.labels.shape, dtype=torch.int32).pin_memory()
-        cf = min(64, F)
+        cf = min(a.e2e_chunk, F)
         maxp = max(int(ho[min(f + cf, F)] - ho[f]) for f in range(0, F, cf))
         del bp  # free the device-resident pipeline before allocating the streaming one
         sp = L.StreamingPipeline(cfg, a.interval, chunk_frames=cf, max_chunk_points=maxp, device=dev, ring_dtype=rdt,
@@ -399,9 +408,38 @@ def main():
         if ws > 1:
             torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
         h2d = hx.numel() * hx.element_size() + hr.numel() * hr.element_size() + ho.numel() * ho.element_size()
+        # the PCIe ceiling of the same traffic: copy-only time of h2d bytes up
+        # and the label bytes down, concurrently on two streams
+        del sp
+        up_h = torch.empty(int(h2d), dtype=torch.uint8).pin_memory()
+        up_d = torch.empty(int(h2d), dtype=torch.uint8, device=dev)
+        dn_d = torch.empty(hl.numel() * 4, dtype=torch.uint8, device=dev)
+        dn_h = torch.empty(hl.numel() * 4, dtype=torch.uint8).pin_memory()
+        s_up, s_dn = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+        def copies():
+            s_up.wait_stream(st)
+            s_dn.wait_stream(st)
+            with torch.cuda.stream(s_up):
+                up_d.copy_(up_h, non_blocking=True)
+            with torch.cuda.stream(s_dn):
+                dn_h.copy_(dn_d, non_blocking=True)
+            st.wait_stream(s_up)
+            st.wait_stream(s_dn)
+
+        copies()
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(3):
+            copies()
+        e1.record(st)
+        torch.cuda.synchronize()
+        copy_ms = e0.elapsed_time(e1) / 3
+        del up_h, up_d, dn_d, dn_h
         e2e = {"value": float(tot_pts.item()) * a.steps / (float(te.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(hl.numel() * 4),
-               "ms_per_step": float(te.item()) / a.steps, "chunk_frames": cf, "ring_dtype": str(rdt).replace("torch.", "")}
+               "copy_only_ms_per_step": copy_ms, "frac_of_copy_bound": copy_ms / (float(te.item()) / a.steps),
+               "ms_per_step": float(te.item()) / a.steps, "chunk_frames": cf, "ring_input": str(rdt).replace("torch.", "")}
 
     cpu = None
     if rank == 0 and ws == 1 and not a.no_cpu_baseline:

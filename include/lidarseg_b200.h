@@ -155,6 +155,10 @@ int lseg_run_pipeline_r8(const lseg_sensor* sensor, int32_t frames, int32_t inte
 /* Flags of lseg_run_pipeline_ex. */
 #define LSEG_PIPE_CERT_NORMALS 1u /* certified fp32 normals (see below) instead of exact fp64 ones */
 #define LSEG_PIPE_RING_U8 2u      /* ring ids are uint8_t (as lseg_run_pipeline_r8) */
+#define LSEG_PIPE_RING_SEGMENTS 4u /* points are ring-major and `ring` is an int64_t (frames, rings + 1)
+                                      table of absolute point offsets (ring i of frame f = points
+                                      [seg[f][i], seg[f][i+1])) instead of a ring id per point:
+                                      12 instead of 13 or 16 input bytes per point */
 
 /* lseg_run_pipeline with flags.  By default (and in lseg_run_pipeline / _r8)
  * normals are computed in fp64 with the reference's operation order, so

@@ -14,7 +14,7 @@ from .evaluate import (EvalConfig, EvalReport, StageStats, bench, dilate_chebysh
                        extract_edges, time_total)
 from .mesh import Mesh, MeshBuilder, build_mesh, mesh_triangles
 from .normals import NormalMap, estimate_normals, node_positions, normal_from_neighbors, normals_to_grid, point_normal
-from .pipeline import BaselineConfig, BatchPipeline, PipelineConfig, PipelineResult, StreamingPipeline, bin_points, run_pipeline
+from .pipeline import BaselineConfig, BatchPipeline, PipelineConfig, PipelineResult, StreamingPipeline, bin_points, ring_segments, run_pipeline
 from .scan import (INVALID, GridIndex, Point3, ScanGrid, SensorConfig, polar_to_cartesian, subsample_steps,
                    valid_point)
 from .scenes import generate_scene, generate_suite

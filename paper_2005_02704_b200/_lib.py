@@ -66,6 +66,7 @@ _SIGS = {
 }
 PIPE_CERT_NORMALS = 1  # include/lidarseg_b200.h LSEG_PIPE_CERT_NORMALS
 PIPE_RING_U8 = 2
+PIPE_RING_SEGMENTS = 4
 EXPORTS = tuple(_SIGS)
 
 _lib = None

@@ -332,7 +332,9 @@ static int run_pipeline_impl(const lseg_sensor* sensor, int32_t frames, int32_t 
   cudaStream_t st = (cudaStream_t)stream;
   prof_mark(nullptr, st);
   const bool fused_bin = sensor->steps <= 8192;
-  if (!fused_bin && ring_bytes != 4) return fail(LSEG_EINVAL, "byte ring ids need azimuth_steps <= 8192");
+  if (!fused_bin && ring_bytes != 4)
+    return fail(LSEG_EINVAL, "byte ring ids / ring segments need azimuth_steps <= 8192");
+  if (ring_bytes == 0 && !ring) return fail(LSEG_EINVAL, "ring segment table is NULL");
   if (fused_bin) {
     launch_bin_fused(*sensor, sh, xyz, ring, ring_bytes, frame_offsets, ws, ranges, n_nodes, st);
   } else {
@@ -376,9 +378,13 @@ int lseg_run_pipeline_ex(const lseg_sensor* sensor, int32_t frames, int32_t inte
                          int32_t* neighbors, float* normals32, uint8_t* nmask, int32_t* node_labels,
                          int32_t* labels, int32_t* n_nodes, int32_t* n_labels, void* workspace,
                          size_t workspace_bytes, void* stream) {
-  if (flags & ~(LSEG_PIPE_CERT_NORMALS | LSEG_PIPE_RING_U8)) return fail(LSEG_EINVAL, "unknown pipeline flags");
+  if (flags & ~(LSEG_PIPE_CERT_NORMALS | LSEG_PIPE_RING_U8 | LSEG_PIPE_RING_SEGMENTS))
+    return fail(LSEG_EINVAL, "unknown pipeline flags");
+  if ((flags & LSEG_PIPE_RING_U8) && (flags & LSEG_PIPE_RING_SEGMENTS))
+    return fail(LSEG_EINVAL, "LSEG_PIPE_RING_U8 and LSEG_PIPE_RING_SEGMENTS are exclusive");
+  const int ring_bytes = (flags & LSEG_PIPE_RING_SEGMENTS) ? 0 : (flags & LSEG_PIPE_RING_U8) ? 1 : 4;
   return run_pipeline_impl(sensor, frames, interval, thresholds, min_segment_size, flags, xyz, ring,
-                           (flags & LSEG_PIPE_RING_U8) ? 1 : 4, frame_offsets, total_points, ranges, node_ids,
+                           ring_bytes, frame_offsets, total_points, ranges, node_ids,
                            neighbors, normals32, nmask, node_labels, labels, n_nodes, n_labels, workspace,
                            workspace_bytes, stream);
 }

@@ -1744,7 +1744,7 @@ __device__ __forceinline__ bool bin_one(const lseg_sensor& sn, const float* __re
 // (no memset, no global atomics).  The CTA verifies that its binary-searched
 // segment really holds only its ring (and ring 0 / R-1 check the prefix /
 // suffix), so any other input order flips the frame to the generic path.
-template <int T, typename RT>
+template <int T, typename RT, bool RINGS = true>
 __global__ void __launch_bounds__(T) k_bin_rows(lseg_sensor sn, Shape sh, const float* __restrict__ xyz,
                                                 const RT* __restrict__ ring, const int64_t* __restrict__ off,
                                                 const int64_t* __restrict__ seg, double* __restrict__ ranges,
@@ -1756,7 +1756,9 @@ __global__ void __launch_bounds__(T) k_bin_rows(lseg_sensor sn, Shape sh, const 
   const int f = (int)(row / sh.R), i = (int)(row - (int64_t)f * sh.R);
   const int S = sh.S;
   const int64_t p0 = __ldg(off + f), p1 = __ldg(off + f + 1);
-  const int64_t lo = __ldg(seg + f * (sh.R + 1) + i), hi = __ldg(seg + f * (sh.R + 1) + i + 1);
+  const int64_t lo = __ldg(seg + f * (sh.R + 1) + i);
+  int64_t hi = __ldg(seg + f * (sh.R + 1) + i + 1);
+  if (!RINGS) hi = max(hi, lo);  // caller-given segments: nothing to verify against
   for (int s = threadIdx.x; s < S; s += T) s_cell[s] = ~0ull;
   if (threadIdx.x == 0) s_bad = (hi < lo) ? 1 : 0;
   __syncthreads();
@@ -1772,7 +1774,7 @@ __global__ void __launch_bounds__(T) k_bin_rows(lseg_sensor sn, Shape sh, const 
       pr[j] = i;
       px[j] = py[j] = pz[j] = 0.0f;
       if (p < hi) {
-        pr[j] = (int)__ldg(ring + p);
+        if (RINGS) pr[j] = (int)__ldg(ring + p);
         px[j] = __ldg(xyz + 3 * p);
         py[j] = __ldg(xyz + 3 * p + 1);
         pz[j] = __ldg(xyz + 3 * p + 2);
@@ -1788,9 +1790,9 @@ __global__ void __launch_bounds__(T) k_bin_rows(lseg_sensor sn, Shape sh, const 
       if (bin_xyz(sn, px[j], py[j], pz[j], r, st)) atomicMin(s_cell + st, (unsigned long long)__double_as_longlong(r));
     }
   }
-  if (i == 0)
+  if (RINGS && i == 0)
     for (int64_t p = p0 + threadIdx.x; p < lo; p += T) bad |= ((int)__ldg(ring + p) >= 0) ? 1 : 0;
-  if (i == sh.R - 1)
+  if (RINGS && i == sh.R - 1)
     for (int64_t p = hi + threadIdx.x; p < p1; p += T) bad |= ((int)__ldg(ring + p) < sh.R) ? 1 : 0;
   if (bad) s_bad = 1;
   __syncthreads();
@@ -1884,9 +1886,23 @@ static void bin_fused_t(const lseg_sensor& sn, const Shape& sh, const float* xyz
   prof_mark("bin_fallback", st);
 }
 
+// Ring-major points whose per-frame ring segments the caller passes
+// ((F, R+1) absolute point offsets) instead of a ring id per point: no bounds
+// search, no verification, no generic path.
+static void bin_fused_seg(const lseg_sensor& sn, const Shape& sh, const float* xyz, const int64_t* segs,
+                          const int64_t* off, const Workspace& ws, double* ranges, cudaStream_t st) {
+  const size_t smem = sizeof(unsigned long long) * sh.S;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_bin_rows<256, uint8_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_bin_rows<256, uint8_t, false><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, xyz, nullptr, off, segs, ranges, ws.vbits,
+                                                                  ws.fbits, ws.fallback);
+  prof_mark("bin_rows", st);
+}
+
 void launch_bin_fused(const lseg_sensor& sn, const Shape& sh, const float* xyz, const void* ring, int ring_bytes,
                       const int64_t* off, const Workspace& ws, double* ranges, int32_t* n_nodes, cudaStream_t st) {
-  if (ring_bytes == 1) bin_fused_t(sn, sh, xyz, static_cast<const uint8_t*>(ring), off, ws, ranges, st);
+  if (ring_bytes == 0) bin_fused_seg(sn, sh, xyz, static_cast<const int64_t*>(ring), off, ws, ranges, st);
+  else if (ring_bytes == 1) bin_fused_t(sn, sh, xyz, static_cast<const uint8_t*>(ring), off, ws, ranges, st);
   else bin_fused_t(sn, sh, xyz, static_cast<const int32_t*>(ring), off, ws, ranges, st);
   launch_frame_scan(sh, ws, n_nodes, st);
 }

@@ -175,8 +175,13 @@ class BatchPipeline:
         flags = _lib.PIPE_CERT_NORMALS if self.normals_mode == "certified" else 0
         if ring.dtype == torch.uint8:
             flags |= _lib.PIPE_RING_U8
+        elif ring.dtype == torch.int64 and ring.dim() == 2:
+            if tuple(ring.shape) != (self.frames, self.config.rings + 1) or not ring.is_contiguous():
+                raise ValueError("ring segment table must be (frames, rings + 1) int64, contiguous")
+            flags |= _lib.PIPE_RING_SEGMENTS
+            ring = ring[f0:]
         elif ring.dtype != torch.int32:
-            raise ValueError("ring ids must be int32 or uint8")
+            raise ValueError("ring ids must be int32 / uint8, or an int64 (frames, rings + 1) segment table")
         _lib.check(self.L.lseg_run_pipeline_ex(
             self.sn, f1 - f0, self.interval, self.thr, int(self.seg.min_segment_size), flags, _lib.ptr(xyz),
             _lib.ptr(ring), _lib.ptr(offsets[f0:]), P, _lib.ptr(sl(self.ranges)), _lib.ptr(sl(self.node_ids)),
@@ -244,6 +249,22 @@ class BatchPipeline:
         return out
 
 
+def ring_segments(ring, offsets, rings: int):
+    """(F, rings + 1) int64 table of absolute point offsets of each ring of
+    ring-major frames (the LSEG_PIPE_RING_SEGMENTS input form): ring i of
+    frame f holds points [seg[f, i], seg[f, i + 1])."""
+    r = torch.as_tensor(ring)
+    off = torch.as_tensor(offsets, dtype=torch.int64, device=r.device)
+    F = int(off.numel()) - 1
+    out = torch.empty((F, rings + 1), dtype=torch.int64, device=r.device)
+    q = torch.arange(rings + 1, dtype=r.dtype if r.dtype != torch.uint8 else torch.int32, device=r.device)
+    for f in range(F):
+        p0, p1 = int(off[f]), int(off[f + 1])
+        rf = r[p0:p1].to(q.dtype)
+        out[f] = torch.searchsorted(rf, q) + p0
+    return out
+
+
 class StreamingPipeline:
     """Host-to-host batched hot path with copy/compute overlap.
 
@@ -264,7 +285,10 @@ class StreamingPipeline:
         self.bps = [BatchPipeline(config, interval, segmenter, frames=self.cf, device=self.device, normals=normals)
                     for _ in range(2)]
         self.xyz = [torch.empty((self.maxp, 3), dtype=torch.float32, device=self.device) for _ in range(2)]
-        self.ring = [torch.empty(self.maxp, dtype=ring_dtype, device=self.device) for _ in range(2)]
+        self.segments = ring_dtype == "segments"  # ring-major points + (F, R+1) ring segment table
+        self.R = R
+        self.ring = [torch.empty((self.cf, R + 1), dtype=torch.int64, device=self.device) if self.segments
+                     else torch.empty(self.maxp, dtype=ring_dtype, device=self.device) for _ in range(2)]
         self.off = [torch.empty(self.cf + 1, dtype=torch.int64, device=self.device) for _ in range(2)]
         self.s_in, self.s_run, self.s_out = (torch.cuda.Stream(self.device) for _ in range(3))
         self.freed = [torch.cuda.Event() for _ in range(2)]     # d2h of the chunk that used buffer b done
@@ -272,8 +296,9 @@ class StreamingPipeline:
         self.computed = [torch.cuda.Event() for _ in range(2)]
 
     def run_host(self, xyz_h, ring_h, offsets_h, labels_h):
-        """xyz_h (P,3) f32, ring_h (P,) i32, offsets_h (F+1,) i64 host tensors
-        (pinned); labels_h (F,R,S) i32 pinned output.  Enqueues everything and
+        """xyz_h (P,3) f32, ring_h (P,) i32 / u8 (or, with ring_dtype="segments",
+        the (F, R+1) i64 table of ``ring_segments``), offsets_h (F+1,) i64 host
+        tensors (pinned); labels_h (F,R,S) i32 pinned output.  Enqueues everything and
         returns; synchronise on the current stream to wait."""
         F = offsets_h.numel() - 1
         offs = offsets_h.tolist()
@@ -294,8 +319,14 @@ class StreamingPipeline:
                 if ci >= 2:
                     self.s_in.wait_event(self.freed[b])
                 self.xyz[b][: p1 - p0].copy_(xyz_h[p0:p1], non_blocking=True)
-                self.ring[b][: p1 - p0].copy_(ring_h[p0:p1], non_blocking=True)
                 loc = offsets_h[f0:f1 + 1] - p0
+                if self.segments:  # chunk-relative segment table, empty frames as padding
+                    seg = ring_h[f0:f1] - p0
+                    if nf < self.cf:
+                        seg = torch.cat([seg, seg.new_full((self.cf - nf, self.R + 1), int(loc[-1]))])
+                    self.ring[b].copy_(seg, non_blocking=True)
+                else:
+                    self.ring[b][: p1 - p0].copy_(ring_h[p0:p1], non_blocking=True)
                 if nf < self.cf:  # pad the last chunk with empty frames
                     loc = torch.cat([loc, loc[-1:].expand(self.cf - nf)])
                 self.off[b].copy_(loc, non_blocking=True)

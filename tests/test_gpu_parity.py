@@ -254,6 +254,27 @@ def test_byte_ring_ids_match_int32(L):
             assert torch.equal(a.neighbors[f, :n], b.neighbors[f, :n])
 
 
+def test_ring_segment_input_matches_ring_ids(L):
+    """Ring-major points + per-frame ring segment table
+    (LSEG_PIPE_RING_SEGMENTS) == per-point ring ids, incl. an empty frame."""
+    from paper_2005_02704_b200 import synth
+    for name, k in (("vlp16", 1), ("hdl64", 5)):
+        shape = synth.CONFIGS[name]
+        xyz, ring, off = synth.make_batch(shape, frames=2, seed=14, device="cuda")
+        n0 = int(off[1])
+        off3 = torch.tensor([0, n0, n0, int(off[2])], dtype=torch.int64, device="cuda")
+        cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
+                             r_max=shape.r_max)
+        a = L.BatchPipeline(cfg, k, frames=3)
+        b = L.BatchPipeline(cfg, k, frames=3)
+        la = a.run(xyz, ring, off3).clone()
+        seg = L.ring_segments(ring, off3, shape.rings)
+        lb = b.run(xyz, seg, off3).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(la, lb)
+        assert torch.equal(a.n_nodes, b.n_nodes)
+
+
 def test_streaming_pipeline_host_to_host(L):
     from paper_2005_02704_b200 import synth
     shape = synth.CONFIGS["hdl64"]
@@ -268,6 +289,13 @@ def test_streaming_pipeline_host_to_host(L):
     sp.run_host(hx, hr, ho, hl)
     torch.cuda.synchronize()
     assert torch.equal(hl, want)
+    # ring-segment input form
+    hs = L.ring_segments(ring.cpu(), ho, shape.rings).pin_memory()
+    hl2 = torch.zeros_like(hl).pin_memory()
+    sp2 = L.StreamingPipeline(cfg, 1, chunk_frames=2, device="cuda", ring_dtype="segments")
+    sp2.run_host(hx, hs, ho, hl2)
+    torch.cuda.synchronize()
+    assert torch.equal(hl2, want)
 
 
 @pytest.mark.parametrize("shape_name,frames,seed", [("hdl64", 4, 21), ("stress", 1, 22), ("vlp16", 8, 23)])
