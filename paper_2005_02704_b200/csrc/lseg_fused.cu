@@ -1496,7 +1496,8 @@ __device__ __forceinline__ int root_of(const int32_t* __restrict__ par, int x) {
 // roots with a bit per kept cell (k_frame_scan over these gives label ranks)
 // and zero each root's histogram slot (labels are root cell + 1 until pruning).
 __global__ void k_root_flatten(Shape sh, int32_t* __restrict__ parent, const uint32_t* __restrict__ lroots,
-                               uint32_t* __restrict__ rbits, int32_t* __restrict__ hist, int64_t K) {
+                               uint32_t* __restrict__ rbits, int32_t* __restrict__ hist, int64_t K,
+                               int32_t* __restrict__ fscal) {
   // after k_merge: point every tile-local root straight at its final root
   // (the only cells whose chains can be long; every other cell points at its
   // tile-local root, so its final root is parent[parent[cell]]), mark final
@@ -1507,6 +1508,7 @@ __global__ void k_root_flatten(Shape sh, int32_t* __restrict__ parent, const uin
   const int lane = threadIdx.x & 31;
   int32_t* par = parent + (int64_t)f * sh.cap;
   int32_t* hf = hist + (int64_t)f * K;
+  if (i == 0 && threadIdx.x == 0) fscal[f * 4] = 0;  // k_survivor_rows' any-small flag
   for (int w = threadIdx.x >> 5; w < sh.Wk; w += blockDim.x >> 5) {
     const uint32_t lr = __ldg(lroots + (int64_t)row * sh.Wk + w);
     bool root = false;
@@ -1907,91 +1909,68 @@ void launch_bin_fused(const lseg_sensor& sn, const Shape& sh, const float* xyz, 
   launch_frame_scan(sh, ws, n_nodes, st);
 }
 
-// Pruning plan over roots: a root survives unless its (post-backfill) count is
-// below min_size; survivor bits -> k_frame_scan gives the compaction ranks.
-// fscal[f*4] = 1 when some label of frame f is small (reference
-// segment.py:136-140: otherwise labels stay as they are).
-__global__ void k_survivors(Shape sh, const uint32_t* __restrict__ rbits, const int32_t* __restrict__ hist, int64_t K,
-                            int32_t min_size, uint32_t* __restrict__ sbits, int32_t* __restrict__ fscal) {
-  const int row = blockIdx.x;  // one CTA per ring row, one warp per word
-  const int f = row / sh.R, i = row - f * sh.R;
-  const int lane = threadIdx.x & 31;
-  const int32_t* hf = hist + (int64_t)f * K;
-  bool any = false;
-  for (int w = threadIdx.x >> 5; w < sh.Wk; w += blockDim.x >> 5) {
-    const uint32_t rb = __ldg(rbits + (int64_t)row * sh.Wk + w);
-    bool surv = false, small = false;
-    if ((rb >> lane) & 1u) {
-      const int cnt = __ldg(hf + i * sh.Sk + w * 32 + lane + 1);
-      small = (min_size > 0) && (cnt < min_size);
-      surv = !small;
-    }
-    const uint32_t b = __ballot_sync(0xffffffffu, surv);
-    any |= __any_sync(0xffffffffu, small);
-    if (lane == 0) sbits[(int64_t)row * sh.Wk + w] = b;
-  }
-  if (lane == 0 && any) atomicOr(fscal + f * 4, 1);
-}
-
-// Survivor bits + their per-frame exclusive word prefix in one pass (one CTA
-// per frame): replaces k_survivors + k_frame_scan.
-template <int T, int ITEMS>
-__global__ void __launch_bounds__(T) k_survivor_scan(Shape sh, const uint32_t* __restrict__ rbits,
+// Pruning plan over roots, one CTA per ring row (all rows in parallel): a
+// root survives unless its post-backfill count is below min_size (reference
+// segment.py:136-140); survivor bits, their row-local exclusive word prefix
+// and the row's survivor count.  k_prune_rows turns the per-row counts into
+// row bases.  fscal[f*4] = 1 when some label of frame f is small (zeroed by
+// k_root_flatten).  One warp per 32-cell word: the histogram reads of a word
+// are one coalesced load.
+template <int T>
+__global__ void __launch_bounds__(T) k_survivor_rows(Shape sh, const uint32_t* __restrict__ rbits,
                                                      const int32_t* __restrict__ hist, int64_t K, int32_t min_size,
                                                      uint32_t* __restrict__ sbits, int32_t* __restrict__ spre,
-                                                     int32_t* __restrict__ fscal, int32_t* __restrict__ nsurv) {
-  using Scan = cub::BlockScan<int, T>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ int carry, s_any;
-  const int f = blockIdx.x;
-  const int n = sh.R * sh.Wk;
-  const uint32_t* rb = rbits + (int64_t)f * n;
-  uint32_t* sb = sbits + (int64_t)f * n;
-  int32_t* sp = spre + (int64_t)f * n;
-  const int32_t* hf = hist + (int64_t)f * K;
-  if (threadIdx.x == 0) { carry = 0; s_any = 0; }
-  __syncthreads();
-  int any = 0;
-  for (int base = 0; base < n; base += T * ITEMS) {
-    uint32_t w[ITEMS];
-    int cnt[ITEMS];
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-      const int idx = base + threadIdx.x * ITEMS + j;
-      w[j] = idx < n ? __ldg(rb + idx) : 0u;
+                                                     int32_t* __restrict__ rcnt, int32_t* __restrict__ fscal) {
+  constexpr int NW = T / 32;
+  extern __shared__ int s_wc[];  // per-word survivor counts of the row
+  __shared__ int s_part[NW];
+  const int row = blockIdx.x;
+  const int f = row / sh.R, i = row - f * sh.R;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int32_t* hf = hist + (int64_t)f * K + (int64_t)i * sh.Sk + 1;
+  bool small = false;
+  for (int w = warp; w < sh.Wk; w += NW) {
+    const uint32_t rb = __ldg(rbits + (int64_t)row * sh.Wk + w);
+    bool surv = false;
+    if ((rb >> lane) & 1u) {
+      const bool sm = (min_size > 0) && (__ldg(hf + w * 32 + lane) < min_size);
+      small |= sm;
+      surv = !sm;
     }
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-      const int idx = base + threadIdx.x * ITEMS + j;
-      uint32_t surv = w[j];
-      if (min_size > 0 && w[j]) {
-        const int row = idx / sh.Wk;
-        const int cell0 = row * sh.Sk + (idx - row * sh.Wk) * 32 + 1;  // hist slot of the word's first cell
-        for (uint32_t m = w[j]; m; m &= m - 1) {
-          const int b = __ffs(m) - 1;
-          if (__ldg(hf + cell0 + b) < min_size) { surv &= ~(1u << b); any = 1; }
-        }
-      }
-      w[j] = surv;
-      cnt[j] = __popc(surv);
+    const uint32_t b = __ballot_sync(0xffffffffu, surv);
+    if (lane == 0) {
+      sbits[(int64_t)row * sh.Wk + w] = b;
+      s_wc[w] = __popc(b);
     }
-    int x[ITEMS], total;
-    Scan(tmp).ExclusiveSum(cnt, x, total);
-    const int c0 = carry;
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-      const int idx = base + threadIdx.x * ITEMS + j;
-      if (idx < n) { sb[idx] = w[j]; sp[idx] = c0 + x[j]; }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) carry = c0 + total;
-    __syncthreads();
   }
-  if (any) s_any = 1;
+  if (__any_sync(0xffffffffu, small) && lane == 0) atomicOr(fscal + f * 4, 1);
   __syncthreads();
+  // row-local exclusive prefix over the words: each warp scans a contiguous
+  // block of words, then the block totals are offset
+  const int per = (sh.Wk + NW - 1) / NW;
+  const int w0 = warp * per, w1 = min(sh.Wk, w0 + per);
+  int carry = 0;
+  for (int c = w0; c < w1; c += 32) {
+    const int w = c + lane;
+    const int v = (w < w1) ? s_wc[w] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    if (w < w1) s_wc[w] = carry + x - v;  // exclusive within the warp's block
+    carry += __shfl_sync(0xffffffffu, x, 31);
+  }
+  if (lane == 0) s_part[warp] = carry;
+  __syncthreads();
+  int base = 0;
+  for (int q = 0; q < warp; ++q) base += s_part[q];
+  for (int w = w0 + lane; w < w1; w += 32) spre[(int64_t)row * sh.Wk + w] = base + s_wc[w];
   if (threadIdx.x == 0) {
-    fscal[f * 4] = s_any;
-    nsurv[f] = carry;
+    int tot = 0;
+    for (int q = 0; q < NW; ++q) tot += s_part[q];
+    rcnt[row] = tot;
   }
 }
 
@@ -2003,11 +1982,12 @@ __global__ void __launch_bounds__(T) k_prune_rows(Shape sh, const int32_t* __res
                                                   int64_t K, int32_t min_size, const int32_t* __restrict__ fscal,
                                                   const uint32_t* __restrict__ rbits, const int32_t* __restrict__ rpre,
                                                   const uint32_t* __restrict__ sbits,
-                                                  const int32_t* __restrict__ spre) {
+                                                  const int32_t* __restrict__ spre, const int32_t* __restrict__ rcnt) {
   extern __shared__ int s_dynrow[];
   const int S = sh.S, nw = (S + 31) / 32;
   int* s_val = s_dynrow;
   uint32_t* s_dm = reinterpret_cast<uint32_t*>(s_dynrow + nw * 32);
+  int* s_base = reinterpret_cast<int*>(s_dm + nw);  // survivor rank of each ring row's first root
   __shared__ int s_any;
   const int row = blockIdx.x;
   const int f = row / sh.R;
@@ -2017,6 +1997,21 @@ __global__ void __launch_bounds__(T) k_prune_rows(Shape sh, const int32_t* __res
   const int32_t* bp = (any_small ? spre : rpre) + (int64_t)f * sh.R * sh.Wk;
   const int64_t rb = (int64_t)row * S;
   if (threadIdx.x == 0) s_any = 0;
+  if (any_small && threadIdx.x < 32) {  // row bases: exclusive scan of the frame's row counts
+    const int lane = threadIdx.x;
+    int carry = 0;
+    for (int c = 0; c < sh.R; c += 32) {
+      const int v = (c + lane < sh.R) ? __ldg(rcnt + (int64_t)f * sh.R + c + lane) : 0;
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += t;
+      }
+      if (c + lane < sh.R) s_base[c + lane] = carry + x - v;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+  }
   __syncthreads();
   bool any = false;
   constexpr int PF = 8;
@@ -2045,20 +2040,26 @@ __global__ void __launch_bounds__(T) k_prune_rows(Shape sh, const int32_t* __res
   const bool rany = s_any != 0;
   for (int s = threadIdx.x; s < S; s += T) {
     const int v = fill_one(s_val, s_dm, nw, S, s, rany);
-    out[rb + s] = v > 0 ? rank_label(bb, bp, sh.Wk, sh.Sk, v - 1, sh.inv_Sk) : 0;
+    int o = 0;
+    if (v > 0) {
+      const int rc = v - 1;
+      const int rr = fdiv(rc, sh.Sk, sh.inv_Sk), cc = rc - rr * sh.Sk;
+      o = 1 + (any_small ? s_base[rr] : 0) + node_id_at(bb + (int64_t)rr * sh.Wk, bp + (int64_t)rr * sh.Wk, cc);
+    }
+    out[rb + s] = o;
   }
 }
 
 void launch_prune_fused(const Shape& sh, const Workspace& ws, int32_t min_size, int32_t* labels, cudaStream_t st) {
-  k_survivor_scan<512, 4><<<sh.F, 512, 0, st>>>(sh, ws.rbits, ws.hist, ws.K, min_size, ws.sbits, ws.spre, ws.fscal,
-                                                 ws.fscal_cnt);
+  k_survivor_rows<256><<<sh.F * sh.R, 256, sizeof(int) * (size_t)sh.Wk, st>>>(
+      sh, ws.rbits, ws.hist, ws.K, min_size, ws.sbits, ws.spre, ws.rcnt, ws.fscal);
   prof_mark("prune_plan", st);
   const int nwr = (sh.S + 31) / 32;
-  const size_t smem = sizeof(int) * (size_t)nwr * 33;
+  const size_t smem = sizeof(int) * ((size_t)nwr * 33 + (size_t)sh.R);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_prune_rows<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_prune_rows<256><<<sh.F * sh.R, 256, smem, st>>>(sh, ws.lab_tmp, labels, ws.hist, ws.K, min_size, ws.fscal, ws.rbits,
-                                                    ws.rpre, ws.sbits, ws.spre);
+                                                    ws.rpre, ws.sbits, ws.spre, ws.rcnt);
   prof_mark("prune_apply", st);
 }
 
@@ -2144,7 +2145,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
     const int64_t blocks = (nwords * 32 + 255) / 256;
     (void)blocks;
     const int thr = sh.Wk >= 8 ? 256 : 32 * sh.Wk;
-    k_root_flatten<<<sh.F * sh.R, thr, 0, st>>>(sh, ws.parent, ws.lroots, ws.rbits, ws.hist, ws.K);
+    k_root_flatten<<<sh.F * sh.R, thr, 0, st>>>(sh, ws.parent, ws.lroots, ws.rbits, ws.hist, ws.K, ws.fscal);
     prof_mark("root_flatten", st);
     launch_scan_bits(sh, ws.rbits, ws.rpre, n_labels, nullptr, 0, st);
     prof_mark("root_scan", st);
