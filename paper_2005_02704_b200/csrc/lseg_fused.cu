@@ -46,6 +46,12 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_CC_SV
 #define LSEG_CC_SV 1
 #endif
+#ifndef LSEG_ROW_MINB
+#define LSEG_ROW_MINB 8
+#endif
+#ifndef LSEG_BIN_MINB
+#define LSEG_BIN_MINB 8
+#endif
 #ifndef LSEG_CC_MINB
 #define LSEG_CC_MINB 8
 #endif
@@ -1587,7 +1593,7 @@ __device__ __forceinline__ void hist_add(int32_t* hw, int lab) {
 // label ids are root cell + 1 (ascending root cell == ascending reference
 // label, so the compaction in k_prune_rows reproduces the reference ids).
 template <int T>
-__global__ void __launch_bounds__(T) k_labels_backfill(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
+__global__ void __launch_bounds__(T, LSEG_ROW_MINB) k_labels_backfill(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
                                                        const uint32_t* __restrict__ vbits,
                                                        const uint32_t* __restrict__ fbits,
                                                        const int32_t* __restrict__ parent,
@@ -1747,7 +1753,7 @@ __device__ __forceinline__ bool bin_one(const lseg_sensor& sn, const float* __re
 // segment really holds only its ring (and ring 0 / R-1 check the prefix /
 // suffix), so any other input order flips the frame to the generic path.
 template <int T, typename RT, bool RINGS = true>
-__global__ void __launch_bounds__(T) k_bin_rows(lseg_sensor sn, Shape sh, const float* __restrict__ xyz,
+__global__ void __launch_bounds__(T, LSEG_BIN_MINB) k_bin_rows(lseg_sensor sn, Shape sh, const float* __restrict__ xyz,
                                                 const RT* __restrict__ ring, const int64_t* __restrict__ off,
                                                 const int64_t* __restrict__ seg, double* __restrict__ ranges,
                                                 uint32_t* __restrict__ vbits, uint32_t* __restrict__ fbits,
@@ -1977,7 +1983,7 @@ __global__ void __launch_bounds__(T) k_survivor_rows(Shape sh, const uint32_t* _
 // Dissolve small segments into the nearest surviving ring donor (reference
 // segment.py:141-154) and write the final compacted ids, one CTA per ring row.
 template <int T>
-__global__ void __launch_bounds__(T) k_prune_rows(Shape sh, const int32_t* __restrict__ lab_in,
+__global__ void __launch_bounds__(T, LSEG_ROW_MINB) k_prune_rows(Shape sh, const int32_t* __restrict__ lab_in,
                                                   int32_t* __restrict__ out, const int32_t* __restrict__ hist,
                                                   int64_t K, int32_t min_size, const int32_t* __restrict__ fscal,
                                                   const uint32_t* __restrict__ rbits, const int32_t* __restrict__ rpre,
