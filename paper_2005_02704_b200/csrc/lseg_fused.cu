@@ -69,7 +69,10 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #endif
 static constexpr int TILE_R = kTileR;
 static constexpr int TILE_C = kTileC;
-static constexpr int TILE_T = 256;
+#ifndef LSEG_TILE_T
+#define LSEG_TILE_T 256
+#endif
+static constexpr int TILE_T = LSEG_TILE_T;
 
 __device__ __forceinline__ int wrapc(int c, int Sk) { return c < 0 ? c + Sk : (c >= Sk ? c - Sk : c); }
 

@@ -342,3 +342,51 @@ def test_certified_normal_bounds_hold(L, oracle, shape_name, frames, seed):
             reasons[code] = reasons.get(code, 0) + int((em == -10.0 - code).sum())
     print(f"certified: worst error/bound {worst:.3g}, exact fallbacks {n_exact}/{n_tot}, by reason {reasons}")
     assert n_exact < 0.05 * n_tot, f"exact fallbacks {n_exact}/{n_tot}"
+
+
+def _grid_points(rng, R, S, top, bottom, base=5.0, noise=0.3, keep=0.9, planar=True):
+    """Ring-major f32 points of a random smooth range grid (plus dropouts)."""
+    elev = np.radians(np.linspace(top, bottom, R))
+    az = 2.0 * np.pi * np.arange(S) / S
+    if planar:
+        rr = base + noise * np.sin(az)[None, :] * np.cos(elev)[:, None] + rng.uniform(-0.02, 0.02, size=(R, S))
+    else:
+        rr = base + rng.uniform(-noise, noise, size=(R, S))
+    valid = rng.random((R, S)) < keep
+    dirs = np.stack([np.cos(elev)[:, None] * np.cos(az)[None, :], np.cos(elev)[:, None] * np.sin(az)[None, :],
+                     np.broadcast_to(np.sin(elev)[:, None], (R, S))], axis=-1)
+    pts = (dirs * rr[:, :, None])[valid].astype(np.float32)
+    ring = np.nonzero(valid)[0].astype(np.int32)
+    return elev, pts, ring
+
+
+@pytest.mark.parametrize("R,S,k,mseg,keep", [
+    (2, 16, 1, 0, 1.0),        # minimum rings, tiny grid
+    (3, 10, 9, 2, 0.9),        # k = S - 1: S' = 2, slot N5 dropped (mesh.py:96-101)
+    (5, 40, 7, 3, 0.8),        # S mod k != 0 (wrap gap)
+    (4, 9000, 1, 10, 0.95),    # S > 8192: generic binning path (no fused rows)
+    (6, 64, 1, 10 ** 6, 0.9),  # everything small: all labels dissolve to 0
+    (7, 130, 2, 1, 0.0),       # no valid point at all
+    (16, 1800, 3, 5, 0.5),     # sparse, fragmented
+])
+def test_edge_shapes_vs_oracle(L, oracle, R, S, k, mseg, keep):
+    """Edge cases of the batched path (the reference's own tests cover them
+    for the single-scan API): tiny / degenerate grids, S' = 2, wrap gaps,
+    the generic binning path, total pruning, empty frames, fragmentation."""
+    rng = np.random.default_rng(R * 1000 + S + k)
+    elev, pts, ring = _grid_points(rng, R, S, 10.0, -20.0, keep=keep, planar=(R % 2 == 0))
+    off = np.array([0, pts.shape[0]], dtype=np.int64)
+    cfg = L.SensorConfig(ring_elevations=elev, azimuth_steps=S, r_min=0.5, r_max=100.0)
+    for normals in ("exact", "certified"):
+        bp = L.BatchPipeline(cfg, k, L.SegmenterConfig(min_segment_size=mseg), frames=1, keep_node_labels=True,
+                             normals=normals)
+        bp.run(torch.from_numpy(pts).cuda(), torch.from_numpy(ring).cuda(), torch.from_numpy(off).cuda())
+        torch.cuda.synchronize()
+        want = oracle.run_from_points(pts, ring, elev, S, k, 0.5, 100.0, min_segment_size=mseg)
+        got = bp.frame(0)
+        np.testing.assert_array_equal(np.nan_to_num(got["ranges"], nan=-1.0), np.nan_to_num(want["ranges"], nan=-1.0))
+        np.testing.assert_array_equal(got["node_ids"], want["mesh"]["node_ids"])
+        np.testing.assert_array_equal(got["neighbors"], want["mesh"]["neighbors"])
+        np.testing.assert_array_equal(got["mask"], want["mask"])
+        np.testing.assert_array_equal(got["node_labels"], want["node_labels"])
+        np.testing.assert_array_equal(got["labels"], want["labels"])
