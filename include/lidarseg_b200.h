@@ -134,7 +134,8 @@ int lseg_prune_small(int32_t frames, int32_t rings, int32_t steps, const int32_t
  * bin_points: the whole hot path for F frames of points in one call.
  * Outputs as in the individual ops; normals32 (F,cap,3) f32;
  * node_labels (F,R,S) optional (NULL) = segment() output before completion;
- * labels (F,R,S) = after backfill + prune_small. */
+ * labels (F,R,S) = after backfill + prune_small; n_nodes (F) mesh nodes;
+ * n_labels (F) = number of segment() labels (before completion). */
 int lseg_run_pipeline(const lseg_sensor* sensor, int32_t frames, int32_t interval,
                       const double* thresholds, int32_t min_segment_size, const float* xyz,
                       const int32_t* ring, const int64_t* frame_offsets, int64_t total_points,

@@ -2106,12 +2106,10 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
 #else
     const size_t csmem = (size_t)NH * (3 * 8 + 4) + (size_t)NT * (3 * 4 + 2 + 2 + 2 + 3);  // see k_tile_cert
 #endif
-    static bool cattr = false;
-    if (!cattr) {
-      cudaFuncSetAttribute(k_tile_cert<TILE_R, TILE_C, TILE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)csmem);
-      cattr = true;
-    }
+    // per launch: cheap, and correct for every device / thread (a static
+    // "done" flag would not be)
+    cudaFuncSetAttribute(k_tile_cert<TILE_R, TILE_C, TILE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)csmem);
     float4* bn4 = reinterpret_cast<float4*>(ws.bnorm);
     k_tile_cert<TILE_R, TILE_C, TILE_T><<<(unsigned)nt, TILE_T, csmem, st>>>(
         sn, sh, ranges, ws.vbits, ws.wpre, cp, node_ids, neighbors, n32, nmask, ws.masks, bn4, ws.normals64, dbg_err,
@@ -2132,11 +2130,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
       (size_t)(3 * (TILE_R + 2) * (TILE_C + 2) + 3 * TILE_R * TILE_C) * 8 +
 #endif
       (size_t)(TILE_R + 2) * (TILE_C + 2) * 4 + (size_t)TILE_R * TILE_C * 4;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_tile<TILE_R, TILE_C, TILE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
-    attr_set = true;
-  }
+  cudaFuncSetAttribute(k_tile<TILE_R, TILE_C, TILE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
   k_tile<TILE_R, TILE_C, TILE_T><<<(unsigned)nt, TILE_T, tsmem, st>>>(sn, sh, ranges, ws.vbits, ws.wpre, thr[0], thr[1],
                                                                   thr[2], node_ids, neighbors, n32, nmask, ws.masks,
                                                                   ws.bnorm, ws.parent, ws.lroots);
