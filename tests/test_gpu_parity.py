@@ -390,3 +390,31 @@ def test_edge_shapes_vs_oracle(L, oracle, R, S, k, mseg, keep):
         np.testing.assert_array_equal(got["mask"], want["mask"])
         np.testing.assert_array_equal(got["node_labels"], want["node_labels"])
         np.testing.assert_array_equal(got["labels"], want["labels"])
+
+
+def test_cuda_graph_capture_replays_exactly(L):
+    """BatchPipeline.capture: one CUDA graph per scan (the latency path);
+    replaying it after refilling the inputs in place gives the eager result."""
+    from paper_2005_02704_b200 import synth
+    shape = synth.CONFIGS["vlp16"]
+    x0, r0, o0 = synth.make_batch(shape, frames=1, seed=30, device="cuda")
+    x1, r1, o1 = synth.make_batch(shape, frames=1, seed=31, device="cuda")
+    cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
+                         r_max=shape.r_max)
+    n = max(int(x0.shape[0]), int(x1.shape[0]))
+    xb = torch.zeros((n, 3), dtype=torch.float32, device="cuda")
+    rb = torch.zeros(n, dtype=torch.int32, device="cuda")
+    ob = torch.zeros(2, dtype=torch.int64, device="cuda")
+    eager = L.BatchPipeline(cfg, 1, frames=1)
+    for normals in ("exact", "certified"):
+        bp = L.BatchPipeline(cfg, 1, frames=1, normals=normals)
+        xb[: x0.shape[0]], rb[: r0.shape[0]], ob.copy_(o0)
+        g = bp.capture(xb, rb, ob)
+        for x, r, o in ((x1, r1, o1), (x0, r0, o0)):
+            xb[: x.shape[0]].copy_(x)
+            rb[: r.shape[0]].copy_(r)
+            ob.copy_(o)
+            g.replay()
+            want = eager.run(x, r, o)
+            torch.cuda.synchronize()
+            assert torch.equal(bp.labels, want)
