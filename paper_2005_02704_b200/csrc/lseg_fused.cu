@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
                                                 int32_t* __restrict__ neighbors, float* __restrict__ n32,
                                                 uint8_t* __restrict__ nmask, unsigned long long* __restrict__ masks,
                                                 double* __restrict__ bnorm, int32_t* __restrict__ parent,
-                                                uint32_t* __restrict__ lroots) {
+                                                uint32_t* __restrict__ lroots, int32_t* __restrict__ n_labels) {
   constexpr int GR = TR + 2, GC = TC + 2;  // halo rows r0-1..r0+TR, cols c0-1..c0+TC
   constexpr int NT = TR * TC;
 #if LSEG_PHASES
@@ -242,6 +242,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   const int32_t* wpf = wpre + (int64_t)f * sh.R * sh.Wk;
   const int64_t nbase = (int64_t)f * sh.cap;
   const int tid = threadIdx.x;
+  if (rem == 0 && tid == 0) n_labels[f] = 0;  // counted by k_root_flatten
 
   // A. halo positions dir*r (reference product order) and node ids (-1 absent).
   // All of a thread's loads are issued before any is used (one memory round
@@ -707,7 +708,8 @@ __global__ void __launch_bounds__(T, LSEG_CERT_MINB) k_tile_cert(
     lseg_sensor sn, Shape sh, const double* __restrict__ ranges, const uint32_t* __restrict__ vbits,
     const int32_t* __restrict__ wpre, CertParams cp, int32_t* __restrict__ node_ids, int32_t* __restrict__ neighbors,
     float* __restrict__ n32, uint8_t* __restrict__ nmask, unsigned long long* __restrict__ masks,
-    float4* __restrict__ bn4, double* __restrict__ xn, float* __restrict__ dbg_err, int32_t* __restrict__ fscal) {
+    float4* __restrict__ bn4, double* __restrict__ xn, float* __restrict__ dbg_err, int32_t* __restrict__ fscal,
+    int32_t* __restrict__ n_labels) {
   constexpr int GR = TR + 2, GC = TC + 2, NH = GR * GC;
   constexpr int NT = TR * TC;
   static_assert(TC == 64, "row masks assume 64-column tiles");
@@ -766,7 +768,10 @@ __global__ void __launch_bounds__(T, LSEG_CERT_MINB) k_tile_cert(
   long long ph_prev = clock64();
 #endif
   if (tid < 5) s_cnt[tid] = 0;
-  if (rem == 0 && tid == 0) fscal[f * 4 + 2] = 0;  // k_merge_cert's undecided-edge counter
+  if (rem == 0 && tid == 0) {
+    fscal[f * 4 + 2] = 0;  // k_merge_cert's undecided-edge counter
+    n_labels[f] = 0;       // counted by k_root_flatten
+  }
 
   // A. halo positions dir*r (reference product order) and node ids
   {
@@ -1506,7 +1511,7 @@ __device__ __forceinline__ int root_of(const int32_t* __restrict__ par, int x) {
 // and zero each root's histogram slot (labels are root cell + 1 until pruning).
 __global__ void k_root_flatten(Shape sh, int32_t* __restrict__ parent, const uint32_t* __restrict__ lroots,
                                uint32_t* __restrict__ rbits, int32_t* __restrict__ hist, int64_t K,
-                               int32_t* __restrict__ fscal) {
+                               int32_t* __restrict__ fscal, int32_t* __restrict__ n_labels) {
   // after k_merge: point every tile-local root straight at its final root
   // (the only cells whose chains can be long; every other cell points at its
   // tile-local root, so its final root is parent[parent[cell]]), mark final
@@ -1518,6 +1523,10 @@ __global__ void k_root_flatten(Shape sh, int32_t* __restrict__ parent, const uin
   int32_t* par = parent + (int64_t)f * sh.cap;
   int32_t* hf = hist + (int64_t)f * K;
   if (i == 0 && threadIdx.x == 0) fscal[f * 4] = 0;  // k_survivor_rows' any-small flag
+  __shared__ int s_nroot;
+  if (threadIdx.x == 0) s_nroot = 0;
+  __syncthreads();
+  int nroot = 0;
   for (int w = threadIdx.x >> 5; w < sh.Wk; w += blockDim.x >> 5) {
     const uint32_t lr = __ldg(lroots + (int64_t)row * sh.Wk + w);
     bool root = false;
@@ -1530,8 +1539,16 @@ __global__ void k_root_flatten(Shape sh, int32_t* __restrict__ parent, const uin
       if (root) hf[cell + 1] = 0;
     }
     const uint32_t b = __ballot_sync(0xffffffffu, root);
-    if (lane == 0) rbits[(int64_t)row * sh.Wk + w] = b;
+    if (lane == 0) {
+      rbits[(int64_t)row * sh.Wk + w] = b;
+      nroot += __popc(b);
+    }
   }
+  // segment() label count of the frame (zeroed by the tile kernel): one
+  // global atomic per row
+  if (lane == 0 && nroot) atomicAdd(&s_nroot, nroot);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_nroot) atomicAdd(n_labels + f, s_nroot);
 }
 
 // 1 + rank of root cell rc among the set bits of (bits, pre) = its label.
@@ -1844,41 +1861,68 @@ __global__ void k_ring_bounds(Shape sh, const RT* __restrict__ ring, const int64
   if (lane == 0) seg[(int64_t)f * (sh.R + 1) + i] = b;
 }
 
-// Generic path for frames flagged by k_bin_rows: reset the frame's row / bits.
-__global__ void k_bin_reset(Shape sh, const int32_t* __restrict__ fallback, double* __restrict__ ranges,
-                            uint32_t* __restrict__ vbits, uint32_t* __restrict__ fbits) {
-  const int64_t row = blockIdx.x;
-  const int f = (int)(row / sh.R);
-  if (!__ldg(fallback + f)) return;
-  for (int s = threadIdx.x; s < sh.S; s += blockDim.x)
-    ranges[row * sh.S + s] = __longlong_as_double(~0ll);
-  for (int w = threadIdx.x; w < sh.Wk; w += blockDim.x) vbits[row * sh.Wk + w] = 0u;
-  const int Wf = (sh.S + 31) / 32;
-  for (int w = threadIdx.x; w < Wf; w += blockDim.x) fbits[row * Wf + w] = 0u;
-}
-
-// Generic path: global 64-bit atomicMin per point + atomicOr of the kept bit.
-template <typename RT>
-__global__ void k_bin_atomic(lseg_sensor sn, Shape sh, const float* __restrict__ xyz, const RT* __restrict__ ring,
-                             const int64_t* __restrict__ off, const int32_t* __restrict__ fallback,
-                             double* __restrict__ ranges, uint32_t* __restrict__ vbits, uint32_t* __restrict__ fbits) {
-  const int f = blockIdx.y;
-  if (!__ldg(fallback + f)) return;
-  const int64_t p0 = __ldg(off + f), p1 = __ldg(off + f + 1);
-  for (int64_t p = p0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < p1; p += (int64_t)gridDim.x * blockDim.x) {
-    const int rg = (int)__ldg(ring + p);
-    double r;
-    int st;
-    if (rg < 0 || rg >= sh.R || !bin_one(sn, xyz, p, r, st)) continue;
-    const int64_t row = (int64_t)f * sh.R + rg;
-    atomicMin(reinterpret_cast<unsigned long long*>(ranges + row * sh.S + st),
-              (unsigned long long)__double_as_longlong(r));
-    if (st % sh.k == 0) {
-      const int c = st / sh.k;
-      atomicOr(vbits + row * sh.Wk + (c >> 5), 1u << (c & 31));
+// After k_bin_rows, one CTA per frame: a frame that k_bin_rows flagged (not
+// ring-major) is re-binned here by the generic path (reset, then global
+// atomics over its points -- the rare case), then the kept-cell valid bits
+// are scanned into node ids (the work of k_frame_scan).  One launch instead
+// of three on the common path.
+template <int T, int ITEMS, typename RT>
+__global__ void __launch_bounds__(T) k_bin_finish(lseg_sensor sn, Shape sh, const float* __restrict__ xyz,
+                                                  const RT* __restrict__ ring, const int64_t* __restrict__ off,
+                                                  const int32_t* __restrict__ fallback, double* __restrict__ ranges,
+                                                  uint32_t* __restrict__ vbits, uint32_t* __restrict__ fbits,
+                                                  int32_t* __restrict__ wpre, int32_t* __restrict__ n_nodes) {
+  const int f = blockIdx.x;
+  if (ring && fallback[f]) {
+    const int Wf = (sh.S + 31) / 32;
+    for (int64_t q = threadIdx.x; q < (int64_t)sh.R * sh.S; q += T)
+      ranges[(int64_t)f * sh.R * sh.S + q] = __longlong_as_double(~0ll);
+    for (int q = threadIdx.x; q < sh.R * sh.Wk; q += T) vbits[(int64_t)f * sh.R * sh.Wk + q] = 0u;
+    for (int q = threadIdx.x; q < sh.R * Wf; q += T) fbits[(int64_t)f * sh.R * Wf + q] = 0u;
+    __syncthreads();
+    const int64_t p0 = __ldg(off + f), p1 = __ldg(off + f + 1);
+    for (int64_t p = p0 + threadIdx.x; p < p1; p += T) {
+      const int rg = (int)__ldg(ring + p);
+      double r;
+      int stp;
+      if (rg < 0 || rg >= sh.R || !bin_one(sn, xyz, p, r, stp)) continue;
+      const int64_t row = (int64_t)f * sh.R + rg;
+      atomicMin(reinterpret_cast<unsigned long long*>(ranges + row * sh.S + stp),
+                (unsigned long long)__double_as_longlong(r));
+      if (stp % sh.k == 0) atomicOr(vbits + row * sh.Wk + (stp / sh.k >> 5), 1u << ((stp / sh.k) & 31));
+      atomicOr(fbits + row * Wf + (stp >> 5), 1u << (stp & 31));
     }
-    atomicOr(fbits + row * ((sh.S + 31) / 32) + (st >> 5), 1u << (st & 31));
+    __syncthreads();
   }
+  // valid-bit word prefix -> node ids (as k_frame_scan)
+  using Scan = cub::BlockScan<int, T>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry;
+  const int64_t n = (int64_t)sh.R * sh.Wk;
+  const uint32_t* vb = vbits + f * n;
+  int32_t* wp = wpre + f * n;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < n; base += (int64_t)T * ITEMS) {
+    int v[ITEMS];
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      const int64_t idx = base + (int64_t)threadIdx.x * ITEMS + j;
+      v[j] = idx < n ? __popc(vb[idx]) : 0;
+    }
+    int total;
+    Scan(tmp).ExclusiveSum(v, v, total);
+    const int c0 = carry;
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      const int64_t idx = base + (int64_t)threadIdx.x * ITEMS + j;
+      if (idx < n) wp[idx] = c0 + v[j];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry = c0 + total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) n_nodes[f] = carry;
 }
 
 template <typename RT>
@@ -1892,9 +1936,6 @@ static void bin_fused_t(const lseg_sensor& sn, const Shape& sh, const float* xyz
   k_bin_rows<256, RT><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, xyz, ring, off, ws.seg, ranges, ws.vbits, ws.fbits,
                                                      ws.fallback);
   prof_mark("bin_rows", st);
-  k_bin_reset<<<sh.F * sh.R, 256, 0, st>>>(sh, ws.fallback, ranges, ws.vbits, ws.fbits);
-  k_bin_atomic<RT><<<dim3(8, sh.F), 256, 0, st>>>(sn, sh, xyz, ring, off, ws.fallback, ranges, ws.vbits, ws.fbits);
-  prof_mark("bin_fallback", st);
 }
 
 // Ring-major points whose per-frame ring segments the caller passes
@@ -1912,10 +1953,22 @@ static void bin_fused_seg(const lseg_sensor& sn, const Shape& sh, const float* x
 
 void launch_bin_fused(const lseg_sensor& sn, const Shape& sh, const float* xyz, const void* ring, int ring_bytes,
                       const int64_t* off, const Workspace& ws, double* ranges, int32_t* n_nodes, cudaStream_t st) {
-  if (ring_bytes == 0) bin_fused_seg(sn, sh, xyz, static_cast<const int64_t*>(ring), off, ws, ranges, st);
-  else if (ring_bytes == 1) bin_fused_t(sn, sh, xyz, static_cast<const uint8_t*>(ring), off, ws, ranges, st);
-  else bin_fused_t(sn, sh, xyz, static_cast<const int32_t*>(ring), off, ws, ranges, st);
-  launch_frame_scan(sh, ws, n_nodes, st);
+  if (ring_bytes == 0) {  // caller-given ring segments: nothing can fall back
+    bin_fused_seg(sn, sh, xyz, static_cast<const int64_t*>(ring), off, ws, ranges, st);
+    k_bin_finish<1024, 4, uint8_t><<<sh.F, 1024, 0, st>>>(sn, sh, xyz, nullptr, off, ws.fallback, ranges, ws.vbits,
+                                                          ws.fbits, ws.wpre, n_nodes);
+  } else if (ring_bytes == 1) {
+    const uint8_t* r8 = static_cast<const uint8_t*>(ring);
+    bin_fused_t(sn, sh, xyz, r8, off, ws, ranges, st);
+    k_bin_finish<1024, 4, uint8_t><<<sh.F, 1024, 0, st>>>(sn, sh, xyz, r8, off, ws.fallback, ranges, ws.vbits,
+                                                          ws.fbits, ws.wpre, n_nodes);
+  } else {
+    const int32_t* r32 = static_cast<const int32_t*>(ring);
+    bin_fused_t(sn, sh, xyz, r32, off, ws, ranges, st);
+    k_bin_finish<1024, 4, int32_t><<<sh.F, 1024, 0, st>>>(sn, sh, xyz, r32, off, ws.fallback, ranges, ws.vbits,
+                                                          ws.fbits, ws.wpre, n_nodes);
+  }
+  prof_mark("frame_scan", st);
 }
 
 // Pruning plan over roots, one CTA per ring row (all rows in parallel): a
@@ -2002,11 +2055,15 @@ __global__ void __launch_bounds__(T, LSEG_ROW_MINB) k_prune_rows(Shape sh, const
   const int f = row / sh.R;
   const bool any_small = fscal[f * 4] != 0;
   const int32_t* hf = hist + (int64_t)f * K;
-  const uint32_t* bb = (any_small ? sbits : rbits) + (int64_t)f * sh.R * sh.Wk;
-  const int32_t* bp = (any_small ? spre : rpre) + (int64_t)f * sh.R * sh.Wk;
+  // final ids = 1 + rank of the root among the frame's survivors (all roots
+  // when nothing is small): row base + row-local word prefix + bit rank
+  const uint32_t* bb = sbits + (int64_t)f * sh.R * sh.Wk;
+  const int32_t* bp = spre + (int64_t)f * sh.R * sh.Wk;
+  (void)rbits;
+  (void)rpre;
   const int64_t rb = (int64_t)row * S;
   if (threadIdx.x == 0) s_any = 0;
-  if (any_small && threadIdx.x < 32) {  // row bases: exclusive scan of the frame's row counts
+  if (threadIdx.x < 32) {  // row bases: exclusive scan of the frame's row counts
     const int lane = threadIdx.x;
     int carry = 0;
     for (int c = 0; c < sh.R; c += 32) {
@@ -2053,7 +2110,7 @@ __global__ void __launch_bounds__(T, LSEG_ROW_MINB) k_prune_rows(Shape sh, const
     if (v > 0) {
       const int rc = v - 1;
       const int rr = fdiv(rc, sh.Sk, sh.inv_Sk), cc = rc - rr * sh.Sk;
-      o = 1 + (any_small ? s_base[rr] : 0) + node_id_at(bb + (int64_t)rr * sh.Wk, bp + (int64_t)rr * sh.Wk, cc);
+      o = 1 + s_base[rr] + node_id_at(bb + (int64_t)rr * sh.Wk, bp + (int64_t)rr * sh.Wk, cc);
     }
     out[rb + s] = o;
   }
@@ -2113,7 +2170,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
     float4* bn4 = reinterpret_cast<float4*>(ws.bnorm);
     k_tile_cert<TILE_R, TILE_C, TILE_T><<<(unsigned)nt, TILE_T, csmem, st>>>(
         sn, sh, ranges, ws.vbits, ws.wpre, cp, node_ids, neighbors, n32, nmask, ws.masks, bn4, ws.normals64, dbg_err,
-        ws.fscal);
+        ws.fscal, n_labels);
     prof_mark("tile", st);
     k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
     prof_mark("tile_cc", st);
@@ -2133,7 +2190,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   cudaFuncSetAttribute(k_tile<TILE_R, TILE_C, TILE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
   k_tile<TILE_R, TILE_C, TILE_T><<<(unsigned)nt, TILE_T, tsmem, st>>>(sn, sh, ranges, ws.vbits, ws.wpre, thr[0], thr[1],
                                                                   thr[2], node_ids, neighbors, n32, nmask, ws.masks,
-                                                                  ws.bnorm, ws.parent, ws.lroots);
+                                                                  ws.bnorm, ws.parent, ws.lroots, n_labels);
   prof_mark("tile", st);
 #if !LSEG_FUSE_CC
   k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
@@ -2148,10 +2205,13 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
     const int64_t blocks = (nwords * 32 + 255) / 256;
     (void)blocks;
     const int thr = sh.Wk >= 8 ? 256 : 32 * sh.Wk;
-    k_root_flatten<<<sh.F * sh.R, thr, 0, st>>>(sh, ws.parent, ws.lroots, ws.rbits, ws.hist, ws.K, ws.fscal);
+    k_root_flatten<<<sh.F * sh.R, thr, 0, st>>>(sh, ws.parent, ws.lroots, ws.rbits, ws.hist, ws.K, ws.fscal,
+                                                n_labels);
     prof_mark("root_flatten", st);
-    launch_scan_bits(sh, ws.rbits, ws.rpre, n_labels, nullptr, 0, st);
-    prof_mark("root_scan", st);
+    if (node_labels) {  // frame-level root ranks: only the segment() output needs them
+      launch_scan_bits(sh, ws.rbits, ws.rpre, n_labels, nullptr, 0, st);
+      prof_mark("root_scan", st);
+    }
   }
   // labels + backfill -> lab_tmp (+ histogram)
   const int nwr = (sh.S + 31) / 32;
