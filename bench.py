@@ -446,8 +446,11 @@ def main():
         cpu = cpu_baseline_port(shape, a.interval, a.cpu_seconds, a.seed)
 
     if rank == 0:
-        # memsets (bin fallback flags) are not kernels; every other stage is one launch
-        launches = sum(v[1] for k, v in stages.items() if k not in ("bin_fill",))
+        # kernels per profiled stage of the fused pipeline (csrc/lseg_fused.cu):
+        # "bin_rows" = k_ring_bounds + k_bin_rows; every other stage is one kernel
+        # (the fallback-flag memset is not a kernel)
+        per_stage = {"bin_rows": 2, "bin_fill": 0}
+        launches = sum(v[1] * per_stage.get(k, 1) for k, v in stages.items())
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": a.steps,
                 "warmup": max(a.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64" if a.normals == "exact" else "f32+f64",
