@@ -46,6 +46,9 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_CC_SV
 #define LSEG_CC_SV 1
 #endif
+#ifndef LSEG_GEN_POSG
+#define LSEG_GEN_POSG 1
+#endif
 #ifndef LSEG_ROW_MINB
 #define LSEG_ROW_MINB 8
 #endif
@@ -207,9 +210,10 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   double* s_sp = s_cp + GC;       // sin(az) per halo column
   double* s_nx = s_sp + GC;
   double* s_px = s_r;  // dead after the normals: reused by the fused CC (union-find array)
-  auto posg = [&](int gi) -> Vec3 {
-    const int yy = gi / GC, xx = gi - yy * GC;
-    const double ct = s_ct[yy], r = s_r[gi];
+  // position of halo cell (row yy, column xx): the row / column tables are
+  // indexed directly (no division), so a node's 7 lookups share their loads
+  auto posyx = [&](int yy, int xx) -> Vec3 {
+    const double ct = s_ct[yy], r = s_r[yy * GC + xx];
     Vec3 q;
     q.x = __dmul_rn(__dmul_rn(ct, s_cp[xx]), r);
     q.y = __dmul_rn(__dmul_rn(ct, s_sp[xx]), r);
@@ -221,7 +225,10 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   double* s_py = s_px + GR * GC;
   double* s_pz = s_py + GR * GC;
   double* s_nx = s_pz + GR * GC;
-  auto posg = [&](int gi) -> Vec3 { return Vec3{s_px[gi], s_py[gi], s_pz[gi]}; };
+  auto posyx = [&](int yy, int xx) -> Vec3 {
+    const int gi = yy * GC + xx;
+    return Vec3{s_px[gi], s_py[gi], s_pz[gi]};
+  };
 #endif
   double* s_ny = s_nx + NT;
   double* s_nz = s_ny + NT;
@@ -364,15 +371,13 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   for (int i = tid; i < nfan6; i += T) {
     const int e = s_list[i];
     const int y = e / TC, x = e - y * TC;
-    const int g = (y + 1) * GC + (x + 1);
-    const Vec3 p = posg(g);
+    const Vec3 p = posyx(y + 1, x + 1);
     double nv[3];
 #if LSEG_FAN6
     double vx[6], vy[6], vz[6];
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
-      const int gq = g + slot_dr(s) * GC + slot_dc(s);
-      const Vec3 q = posg(gq);
+      const Vec3 q = posyx(y + 1 + slot_dr(s), x + 1 + slot_dc(s));
       vx[s] = __dsub_rn(q.x, p.x);
       vy[s] = __dsub_rn(q.y, p.y);
       vz[s] = __dsub_rn(q.z, p.z);
@@ -384,8 +389,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     FanT<kFastMath> fan;
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
-      const int gq = g + slot_dr(s) * GC + slot_dc(s);
-      const Vec3 q = posg(gq);
+      const Vec3 q = posyx(y + 1 + slot_dr(s), x + 1 + slot_dc(s));
       fan.add(__dsub_rn(q.x, p.x), __dsub_rn(q.y, p.y), __dsub_rn(q.z, p.z));
     }
     const bool okn = fan.finish(p, nv);
@@ -400,15 +404,19 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   for (int i = tid; i < ngen; i += T) {
     const int e = s_list[NT - 1 - i];
     const int y = e / TC, x = e - y * TC;
-    const int g = (y + 1) * GC + (x + 1);
     const unsigned m = s_m[e];
-    const Vec3 p = posg(g);
+    const Vec3 p = posyx(y + 1, x + 1);
     FanT<kFastMath> fan;
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       if (!((m >> s) & 1u)) continue;
-      const int gq = g + slot_dr(s) * GC + slot_dc(s);
-      const Vec3 q = posg(gq);
+#if LSEG_GEN_POSG
+      const int gq = (y + 1 + slot_dr(s)) * GC + x + 1 + slot_dc(s);
+      const int yq = gq / GC;
+      const Vec3 q = posyx(yq, gq - yq * GC);
+#else
+      const Vec3 q = posyx(y + 1 + slot_dr(s), x + 1 + slot_dc(s));
+#endif
       fan.add(__dsub_rn(q.x, p.x), __dsub_rn(q.y, p.y), __dsub_rn(q.z, p.z));
     }
     double nv[3];
