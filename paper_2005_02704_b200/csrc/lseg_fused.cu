@@ -46,6 +46,12 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_CC_SV
 #define LSEG_CC_SV 1
 #endif
+#ifndef LSEG_CC_LIST
+#define LSEG_CC_LIST 1
+#endif
+#ifndef LSEG_CC_FIND
+#define LSEG_CC_FIND 0
+#endif
 #ifndef LSEG_GEN_POSG
 #define LSEG_GEN_POSG 1
 #endif
@@ -1343,12 +1349,61 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
          (w1 ? 2u << 30 : 0u);
     any |= w0 | w1;
   }
+#if LSEG_CC_FIND
+  auto findr = [&](int x) -> int {  // chase to the current root (labels decrease along a chain)
+    int p = s_par[x];
+    while (p != x) {
+      x = p;
+      p = s_par[x];
+    }
+    return x;
+  };
+#endif
   auto hook = [&](unsigned ia, unsigned ib) -> int {
+#if LSEG_CC_FIND
+    const int la = findr(ia), lb = findr(ib);
+#else
     const int la = s_par[ia], lb = s_par[ib];
+#endif
     if (la == lb) return 0;
     const int hi = max(la, lb), lo = min(la, lb);
     return atomicMin(s_par + hi, lo) > lo;
   };
+#if LSEG_CC_LIST
+  // the tile's edges as one dense shared-memory list (a | b << 10): every
+  // round walks only real edges instead of each thread's ten slots
+  __shared__ unsigned s_el[2 * NT + 64];
+  __shared__ int s_ne;
+  if (threadIdx.x == 0) s_ne = 0;
+  __syncthreads();
+  {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j <= NJ; ++j) {
+      const unsigned v = j < NJ ? pk[j] : pw;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const bool has = v & ((1u << 30) << h);
+        const unsigned bal = __ballot_sync(0xffffffffu, has);
+        if (!bal) continue;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&s_ne, __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (has) s_el[base + __popc(bal & ((1u << lane) - 1u))] = (v & 1023u) | (((v >> (10 + 10 * h)) & 1023u) << 10);
+      }
+    }
+  }
+  __syncthreads();
+  const int ne = s_ne;
+  if (ne) {
+    while (true) {
+      int changed = 0;
+      for (int k = threadIdx.x; k < ne; k += T) {
+        const unsigned v = s_el[k];
+        changed |= hook(v & 1023u, v >> 10);
+      }
+      __syncthreads();
+#else
   if (__syncthreads_or(any)) {
     while (true) {
       int changed = 0;
@@ -1359,6 +1414,7 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
         if (v & (2u << 30)) changed |= hook(v & 1023u, (v >> 20) & 1023u);
       }
       __syncthreads();
+#endif
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {  // shortcut at run starts
         if (!((starts >> j) & 1u)) continue;
