@@ -1897,7 +1897,9 @@ __global__ void __launch_bounds__(T, LSEG_BIN_MINB) k_bin_rows(lseg_sensor sn, S
   const int lane = threadIdx.x & 31;
   for (int w = threadIdx.x >> 5; w < sh.Wk; w += T / 32) {
     const int c = w * 32 + lane;
-    const bool v = (c < sh.Sk) && in_window(__longlong_as_double((long long)s_cell[c * sh.k]), sn.r_min, sn.r_max);
+    // every binned range passed the window test in bin_xyz: a cell is valid
+    // iff it received a point (the empty pattern ~0 is a NaN)
+    const bool v = (c < sh.Sk) && s_cell[c * sh.k] != ~0ull;
     const uint32_t b = __ballot_sync(0xffffffffu, v);
     if (lane == 0) vbits[row * sh.Wk + w] = b;
   }
@@ -1905,7 +1907,7 @@ __global__ void __launch_bounds__(T, LSEG_BIN_MINB) k_bin_rows(lseg_sensor sn, S
     const int Wf = (S + 31) / 32;
     for (int w = threadIdx.x >> 5; w < Wf; w += T / 32) {
       const int c = w * 32 + lane;
-      const bool v = (c < S) && in_window(__longlong_as_double((long long)s_cell[c]), sn.r_min, sn.r_max);
+      const bool v = (c < S) && s_cell[c] != ~0ull;
       const uint32_t b = __ballot_sync(0xffffffffu, v);
       if (lane == 0) fbits[row * Wf + w] = b;
     }
