@@ -1,15 +1,22 @@
-// Fused pipeline kernels (sm_100a): the batched hot path of lseg_run_pipeline.
+// Fused pipeline kernels (sm_100a): the batched hot path of lseg_run_pipeline
+// (DESIGN.md §4 has the table with bytes and bounds).  Per batch, in order:
 //
-//   k_tile     one CTA per (frame, TR x TC tile of kept cells): stages the
-//              ranges halo in shared memory, computes fp64 normals for the tile
-//              plus its forward halo, writes the mesh slots / normals, evaluates
-//              the homogeneity test on every forward edge and runs union-find
-//              in shared memory.  Edges leaving the tile are recorded as flag
-//              bits for k_merge.  No fp64 normals ever reach HBM.
-//   k_merge    global union-find over the tile-boundary edges only.
-//   k_labels_backfill  per ring row: node label = 1 + rank[root] (read-only
-//              root chase), then the nearest-donor backfill and the label
-//              histogram, in one pass (replaces label_dense + backfill).
+//   k_ring_bounds, k_bin_rows  per (frame, ring): the ring's points binned
+//              into a shared-memory row (smallest range wins), row + valid bits
+//              written once; non-ring-major frames are flagged
+//   k_bin_finish   per frame: generic re-binning of flagged frames, then the
+//              valid-bit prefix -> node numbering
+//   k_tile / k_tile_cert  per 16 x 64 tile: halo staging, normals (exact fp64,
+//              or certified fp32 with exact fallback), mesh outputs, pass
+//              masks of the internal edges, border normals for k_merge
+//   k_tile_cc  per tile: components of the pass masks (run-level label
+//              propagation in shared memory) -> parent = tile-local root
+//   k_merge(_cert, _exact)  global union-find over tile-border edges only
+//   k_root_flatten  per ring row: tile-local roots -> final roots, root bits
+//   k_labels_backfill  per ring row: labels (root cell + 1), nearest-donor
+//              backfill, label histogram
+//   k_survivor_rows, k_prune_rows  per ring row: pruning plan and the
+//              compacted final ids (reference segment.py:127-160)
 #include <cub/block/block_scan.cuh>
 #include <cuda_fp16.h>
 #include <stdio.h>
@@ -26,9 +33,6 @@ namespace lseg {
 #if LSEG_PHASES
 __device__ unsigned long long g_ph[8];
 #endif
-#ifndef LSEG_FUSE_CC
-#define LSEG_FUSE_CC 0
-#endif
 #ifndef LSEG_UNR
 #define LSEG_UNR 1
 #endif
@@ -37,24 +41,6 @@ static constexpr int kUnrollNormals = LSEG_UNR;
 #define LSEG_FAST_MATH 1
 #endif
 static constexpr bool kFastMath = LSEG_FAST_MATH;
-#ifndef LSEG_POS_RECOMPUTE
-#define LSEG_POS_RECOMPUTE 1
-#endif
-#ifndef LSEG_FAN6
-#define LSEG_FAN6 0
-#endif
-#ifndef LSEG_CC_SV
-#define LSEG_CC_SV 1
-#endif
-#ifndef LSEG_CC_LIST
-#define LSEG_CC_LIST 1
-#endif
-#ifndef LSEG_CC_FIND
-#define LSEG_CC_FIND 0
-#endif
-#ifndef LSEG_GEN_POSG
-#define LSEG_GEN_POSG 1
-#endif
 #ifndef LSEG_ROW_MINB
 #define LSEG_ROW_MINB 8
 #endif
@@ -63,15 +49,6 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #endif
 #ifndef LSEG_CC_MINB
 #define LSEG_CC_MINB 8
-#endif
-#ifndef LSEG_CERT_IDMASK
-#define LSEG_CERT_IDMASK 1
-#endif
-#ifndef LSEG_CERT_SPLITC
-#define LSEG_CERT_SPLITC 0
-#endif
-#ifndef LSEG_CERT_RECOMP
-#define LSEG_CERT_RECOMP 0
 #endif
 #ifndef LSEG_CERT_MINB
 #define LSEG_CERT_MINB 4
@@ -87,30 +64,6 @@ __device__ __forceinline__ int wrapc(int c, int Sk) { return c < 0 ? c + Sk : (c
 
 __device__ __forceinline__ int id_at(const uint32_t* vbf, const int32_t* wpf, int Wk, int r, int c) {
   return node_id_at(vbf + (int64_t)r * Wk, wpf + (int64_t)r * Wk, c);
-}
-
-// local (shared-memory) union-find, same min-root invariant as the global one
-__device__ __forceinline__ int lfind(volatile int* par, int x) {
-  int p = par[x];
-  while (p != x) {
-    const int g = par[p];
-    if (g != p) par[x] = g;  // halving
-    x = p;
-    p = g;
-  }
-  return x;
-}
-
-__device__ __forceinline__ void lunion(int* par, int a, int b) {
-  volatile int* vp = par;
-  int ra = lfind(vp, a), rb = lfind(vp, b);
-  while (ra != rb) {
-    if (ra < rb) { const int t = ra; ra = rb; rb = t; }
-    const int old = atomicCAS(par + ra, ra, rb);
-    if (old == ra) break;
-    ra = lfind(vp, old);
-    rb = lfind(vp, rb);
-  }
 }
 
 // Is the forward edge (r, c) -> slot s internal to the (TR x TC) tile that
@@ -134,37 +87,6 @@ __device__ __forceinline__ int64_t bn_col(const Shape& sh, int TR, int slot, int
   return ((int64_t)2 * ((sh.R + TR - 1) / TR) * sh.Sk + (int64_t)slot * sh.R + r) * 3;
 }
 __device__ __forceinline__ void bn_put(double* o, double a, double b, double c) { o[0] = a; o[1] = b; o[2] = c; }
-
-// Normal of a node whose 6 slots are all present: the same operation sequence
-// as Fan (pairs (0,1)..(4,5),(5,0) accumulated in order) but straight-line, so
-// the six square roots / reciprocals are independent and can overlap.
-__device__ __forceinline__ bool fan6(const double* vx, const double* vy, const double* vz, const Vec3& p,
-                                     double out[3]) {
-  double l[6];
-#pragma unroll
-  for (int a = 0; a < 6; ++a) l[a] = norm3(vx[a], vy[a], vz[a]);
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, ws = 0.0;
-#pragma unroll
-  for (int a = 0; a < 6; ++a) {
-    const int b = (a + 1) % 6;
-    const double L = __dadd_rn(l[a], l[b]);
-    const double w = (L > 0.0) ? __drcp_rn(L) : 0.0;
-    a0 = __dadd_rn(a0, __dmul_rn(w, __dsub_rn(__dmul_rn(vy[a], vz[b]), __dmul_rn(vz[a], vy[b]))));
-    a1 = __dadd_rn(a1, __dmul_rn(w, __dsub_rn(__dmul_rn(vz[a], vx[b]), __dmul_rn(vx[a], vz[b]))));
-    a2 = __dadd_rn(a2, __dmul_rn(w, __dsub_rn(__dmul_rn(vx[a], vy[b]), __dmul_rn(vy[a], vx[b]))));
-    ws = __dadd_rn(ws, w);
-  }
-  if (!(ws > 0.0)) return false;
-  double m0, m1, m2, u0, u1, u2;
-  div3(a0, a1, a2, ws, m0, m1, m2);
-  const double mag = norm3(m0, m1, m2);
-  if (!(mag >= 1e-12)) return false;
-  div3(m0, m1, m2, mag, u0, u1, u2);
-  const double dot = __dadd_rn(__dadd_rn(__dmul_rn(u0, p.x), __dmul_rn(u2, p.z)), __dmul_rn(u1, p.y));
-  if (dot > 0.0) { u0 = -u0; u1 = -u1; u2 = -u2; }
-  out[0] = u0; out[1] = u1; out[2] = u2;
-  return true;
-}
 
 template <int TR, int TC, int T>
 __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int c0, int TRe, int TCe,
@@ -206,7 +128,6 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
 #endif
   // dynamic shared memory (58 KB > the 48 KB static limit), see tile_smem_bytes()
   extern __shared__ __align__(16) unsigned char s_dyn[];
-#if LSEG_POS_RECOMPUTE
   // ranges + separable direction tables; positions are rebuilt on use
   // (5 multiplies) -- 19 KB less shared memory buys a 4th CTA per SM
   double* s_r = reinterpret_cast<double*>(s_dyn);
@@ -215,7 +136,6 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   double* s_cp = s_st + GR;       // cos(az) per halo column
   double* s_sp = s_cp + GC;       // sin(az) per halo column
   double* s_nx = s_sp + GC;
-  double* s_px = s_r;  // dead after the normals: reused by the fused CC (union-find array)
   // position of halo cell (row yy, column xx): the row / column tables are
   // indexed directly (no division), so a node's 7 lookups share their loads
   auto posyx = [&](int yy, int xx) -> Vec3 {
@@ -226,16 +146,6 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     q.z = __dmul_rn(s_st[yy], r);
     return q;
   };
-#else
-  double* s_px = reinterpret_cast<double*>(s_dyn);
-  double* s_py = s_px + GR * GC;
-  double* s_pz = s_py + GR * GC;
-  double* s_nx = s_pz + GR * GC;
-  auto posyx = [&](int yy, int xx) -> Vec3 {
-    const int gi = yy * GC + xx;
-    return Vec3{s_px[gi], s_py[gi], s_pz[gi]};
-  };
-#endif
   double* s_ny = s_nx + NT;
   double* s_nz = s_ny + NT;
   int* s_id = reinterpret_cast<int*>(s_nz + NT);
@@ -289,18 +199,9 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       const int cc = wrapc(c0 - 1 + x, sh.Sk);
       const uint32_t bit = 1u << (cc & 31);
       const int id = (wv[j] & bit) ? pv[j] + __popc(wv[j] & (bit - 1u)) : -1;
-#if LSEG_POS_RECOMPUTE
       s_r[e] = id >= 0 ? rv[j] : 0.0;
-#else
-      Vec3 q = {0.0, 0.0, 0.0};
-      if (id >= 0) q = cell_pos(sn, rr, cc * sh.k, rv[j]);
-      s_px[e] = q.x;
-      s_py[e] = q.y;
-      s_pz[e] = q.z;
-#endif
       s_id[e] = id;
     }
-#if LSEG_POS_RECOMPUTE
     for (int e = tid; e < GR + GC; e += T) {
       if (e < GR) {
         const int rr = min(max(r0 - 1 + e, 0), sh.R - 1);
@@ -312,7 +213,6 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
         s_sp[e - GR] = __ldg(sn.sin_az + cc);
       }
     }
-#endif
   }
   __syncthreads();
   PH_MARK(1);
@@ -379,17 +279,6 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     const int y = e / TC, x = e - y * TC;
     const Vec3 p = posyx(y + 1, x + 1);
     double nv[3];
-#if LSEG_FAN6
-    double vx[6], vy[6], vz[6];
-#pragma unroll
-    for (int s = 0; s < 6; ++s) {
-      const Vec3 q = posyx(y + 1 + slot_dr(s), x + 1 + slot_dc(s));
-      vx[s] = __dsub_rn(q.x, p.x);
-      vy[s] = __dsub_rn(q.y, p.y);
-      vz[s] = __dsub_rn(q.z, p.z);
-    }
-    const bool okn = fan6(vx, vy, vz, p, nv);
-#else
     // streamed: only first / previous / current vectors live (fewer registers,
     // more resident warps)
     FanT<kFastMath> fan;
@@ -399,7 +288,6 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       fan.add(__dsub_rn(q.x, p.x), __dsub_rn(q.y, p.y), __dsub_rn(q.z, p.z));
     }
     const bool okn = fan.finish(p, nv);
-#endif
     if (okn) {
       s_nx[e] = nv[0];
       s_ny[e] = nv[1];
@@ -416,13 +304,9 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       if (!((m >> s) & 1u)) continue;
-#if LSEG_GEN_POSG
       const int gq = (y + 1 + slot_dr(s)) * GC + x + 1 + slot_dc(s);
       const int yq = gq / GC;
       const Vec3 q = posyx(yq, gq - yq * GC);
-#else
-      const Vec3 q = posyx(y + 1 + slot_dr(s), x + 1 + slot_dc(s));
-#endif
       fan.add(__dsub_rn(q.x, p.x), __dsub_rn(q.y, p.y), __dsub_rn(q.z, p.z));
     }
     double nv[3];
@@ -487,10 +371,6 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   const int lane = tid & 31;
   const bool full_width = (c0 == 0 && TCe == sh.Sk);
   unsigned long long* mrow = masks + (((int64_t)f * tilesR + r0 / TR) * tilesC + c0 / TC) * (TR * 5);
-#if LSEG_FUSE_CC
-  __shared__ unsigned long long s_mk[TR * 5];
-  (void)mrow;
-#endif
   for (int y = tid >> 5; y < TR; y += T / 32) {
     unsigned long long H = 0, V0 = 0, V1 = 0, HS = 0;
     bool w0 = false, w1 = false;
@@ -536,27 +416,13 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     }
     const unsigned W = (__ballot_sync(0xffffffffu, w0) ? 1u : 0u) | (__ballot_sync(0xffffffffu, w1) ? 2u : 0u);
     if (lane == 0) {
-#if LSEG_FUSE_CC
-      s_mk[y * 5 + 0] = H;
-      s_mk[y * 5 + 1] = V0;
-      s_mk[y * 5 + 2] = V1;
-      s_mk[y * 5 + 3] = HS;
-      s_mk[y * 5 + 4] = W;
-#else
       mrow[y * 5 + 0] = H;
       mrow[y * 5 + 1] = V0;
       mrow[y * 5 + 2] = V1;
       mrow[y * 5 + 3] = HS;
       mrow[y * 5 + 4] = W;
-#endif
     }
   }
-#if LSEG_FUSE_CC
-  __syncthreads();
-  // positions are dead after the normals: their shared memory holds the
-  // union-find array of the tile-local components
-  tile_cc_body<TR, TC, T>(sh, f, r0, c0, TRe, TCe, s_mk, reinterpret_cast<int*>(s_px), parent, lroots);
-#endif
 #if LSEG_PHASES
   __syncthreads();
 #endif
@@ -728,28 +594,11 @@ __global__ void __launch_bounds__(T, LSEG_CERT_MINB) k_tile_cert(
   constexpr int NT = TR * TC;
   static_assert(TC == 64, "row masks assume 64-column tiles");
   extern __shared__ __align__(16) unsigned char s_dyn[];
-#if LSEG_CERT_RECOMP
-  // ranges + separable direction tables; positions rebuilt on use (fewer
-  // shared bytes -> more resident CTAs)
-  double* s_r = reinterpret_cast<double*>(s_dyn);
-  double* s_ct = s_r + NH;
-  double* s_st = s_ct + GR;
-  double* s_cp = s_st + GR;
-  double* s_sp = s_cp + GC;
-  float* s_nx = reinterpret_cast<float*>(s_sp + GC);
-  auto posg = [&](int gi) -> Vec3 {
-    const int yy = gi / GC, xx = gi - yy * GC;
-    const double ct = s_ct[yy], r = s_r[gi];
-    return Vec3{__dmul_rn(__dmul_rn(ct, s_cp[xx]), r), __dmul_rn(__dmul_rn(ct, s_sp[xx]), r),
-                __dmul_rn(s_st[yy], r)};
-  };
-#else
   double* s_px = reinterpret_cast<double*>(s_dyn);
   double* s_py = s_px + NH;
   double* s_pz = s_py + NH;
   float* s_nx = reinterpret_cast<float*>(s_pz + NH);
   auto posg = [&](int gi) -> Vec3 { return Vec3{s_px[gi], s_py[gi], s_pz[gi]}; };
-#endif
   float* s_ny = s_nx + NT;
   float* s_nz = s_ny + NT;
   __half* s_eh = reinterpret_cast<__half*>(s_nz + NT);  // err / u, rounded up (<= 64 kAcc + 8 < 65504)
@@ -817,31 +666,13 @@ __global__ void __launch_bounds__(T, LSEG_CERT_MINB) k_tile_cert(
       const int cc = wrapc(c0 - 1 + x, sh.Sk);
       const uint32_t bit = 1u << (cc & 31);
       const int id = (wv[j] & bit) ? pv[j] + __popc(wv[j] & (bit - 1u)) : -1;
-#if LSEG_CERT_RECOMP
-      s_r[e] = id >= 0 ? rv[j] : 0.0;
-      (void)rr;
-#else
       Vec3 q = {0.0, 0.0, 0.0};
       if (id >= 0) q = cell_pos(sn, rr, cc * sh.k, rv[j]);
       s_px[e] = q.x;
       s_py[e] = q.y;
       s_pz[e] = q.z;
-#endif
       s_id[e] = id;
     }
-#if LSEG_CERT_RECOMP
-    for (int e = tid; e < GR + GC; e += T) {
-      if (e < GR) {
-        const int rr = min(max(r0 - 1 + e, 0), sh.R - 1);
-        s_ct[e] = __ldg(sn.cos_el + rr);
-        s_st[e] = __ldg(sn.sin_el + rr);
-      } else {
-        const int cc = wrapc(c0 - 1 + (e - GR), sh.Sk) * sh.k;
-        s_cp[e - GR] = __ldg(sn.cos_az + cc);
-        s_sp[e - GR] = __ldg(sn.sin_az + cc);
-      }
-    }
-#endif
   }
   __syncthreads();
   for (int hy = warp; hy < GR; hy += T / 32) {
@@ -868,15 +699,10 @@ __global__ void __launch_bounds__(T, LSEG_CERT_MINB) k_tile_cert(
     unsigned m = 0;
     const bool node = y < TRe && x < TCe && pres(hy, x);
     if (node) {
-#if LSEG_CERT_IDMASK
       const int g = hy * GC + x + 1;
 #pragma unroll
       for (int s = 0; s < 6; ++s)
         if (s_id[g + slot_dr(s) * GC + slot_dc(s)] >= 0 && !(s == 5 && sh.Sk == 2)) m |= 1u << s;
-#else
-      m = pres(hy + 1, x) | pres(hy + 1, x + 1) << 1 | pres(hy, x + 1) << 2 | pres(hy - 1, x) << 3 |
-          pres(hy - 1, x - 1) << 4 | (sh.Sk == 2 ? 0u : pres(hy, x - 1) << 5);
-#endif
     }
     s_m[e] = (uint8_t)m;
     s_has[e] = 0;
@@ -1030,7 +856,7 @@ __global__ void __launch_bounds__(T, LSEG_CERT_MINB) k_tile_cert(
         UW |= (__ballot_sync(0xffffffffu, w0 == 2) ? 1u : 0u) | (__ballot_sync(0xffffffffu, w1 == 2) ? 2u : 0u);
       }
       // per-node outputs
-      if (!LSEG_CERT_SPLITC && in) {
+      if (in) {
         const int rr = r0 + y, cc = c0 + x;
         const int g = (y + 1) * GC + (x + 1);
         const int id = s_id[g];
@@ -1080,43 +906,6 @@ __global__ void __launch_bounds__(T, LSEG_CERT_MINB) k_tile_cert(
   __syncthreads();
   PH_MARK(5);
 
-#if LSEG_CERT_SPLITC
-  for (int e = tid; e < NT; e += T) {
-    const int y = e / TC, x = e - y * TC;
-    if (y >= TRe || x >= TCe) continue;
-    const int rr = r0 + y, cc = c0 + x;
-    const int g = (y + 1) * GC + (x + 1);
-    const int id = s_id[g];
-    if (node_ids) node_ids[nbase + (int64_t)rr * sh.Sk + cc] = id;
-    if (id < 0) continue;
-    int nb[6];
-#pragma unroll
-    for (int s = 0; s < 6; ++s) nb[s] = s_id[g + slot_dr(s) * GC + slot_dc(s)];
-    if (sh.Sk == 2 && nb[5] == nb[2]) nb[5] = -1;
-    int2* o2 = reinterpret_cast<int2*>(neighbors + (nbase + id) * 6);
-    o2[0] = make_int2(nb[0], nb[1]);
-    o2[1] = make_int2(nb[2], nb[3]);
-    o2[2] = make_int2(nb[4], nb[5]);
-    const bool hs = s_has[e] != 0;
-    const float qn = __int_as_float(0x7fc00000);
-    const float4 v = hs ? make_float4(s_nx[e], s_ny[e], s_nz[e], __half2float(s_eh[e]) * kU32)
-                        : make_float4(qn, qn, qn, -1.0f);
-    if (n32) {
-      float* o = n32 + (nbase + id) * 3;
-      o[0] = v.x;
-      o[1] = v.y;
-      o[2] = v.z;
-    }
-    if (dbg_err) dbg_err[nbase + id] = s_req[e] >= 2 ? -10.0f - s_req[e] : v.w;
-    nmask[nbase + id] = hs ? 1 : 0;
-    if (hs) {
-      if (y == 0) bf[bn4_row(sh, 2 * tr, cc)] = v;
-      if (y == TRe - 1) bf[bn4_row(sh, 2 * tr + 1, cc)] = v;
-      if (x == 0) bf[bn4_col(sh, TR, 2 * tc, rr)] = v;
-      if (x == TCe - 1) bf[bn4_col(sh, TR, 2 * tc + 1, rr)] = v;
-    }
-  }
-#endif
 
   // X1 + D2 (rare; block-uniform): settle the undecided edges on exact normals
   if (s_cnt[4]) {
@@ -1273,14 +1062,13 @@ __global__ void k_merge_exact(lseg_sensor sn, Shape sh, const double* __restrict
   }
 }
 
-// Tile-local connected components from k_tile's masks (one small CTA per
-// tile): each node's parent starts as the first cell of its horizontal run
-// (bit arithmetic), vertical / diagonal edges join runs with shared-memory
-// union-find -- skipping an edge when the parallel edge one column to the left
-// already joins the same two runs -- and each labelled cell gets
-// parent[cell] = minimum cell of its tile-local component (-1 without normal).
-// Tile-local connected components from the pass masks in shared memory (the
-// body of k_tile_cc, also run inside k_tile when the two are fused).
+// Tile-local connected components from the tile's pass masks (the body of
+// k_tile_cc, one small CTA per tile): each node's parent starts as the first
+// cell of its horizontal run (bit arithmetic); vertical / diagonal edges --
+// minus those whose parallel edge one column to the left already joins the
+// same two runs -- join runs by label propagation in shared memory; each
+// labelled cell gets parent[cell] = minimum cell of its tile-local component
+// (-1 without a normal).
 template <int TR, int TC, int T>
 __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int c0, int TRe, int TCe,
                                              const unsigned long long* s_m, int* s_par, int32_t* __restrict__ parent,
@@ -1309,7 +1097,6 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
     s_U[2 * y + 1] = U1;
   }
   __syncthreads();
-#if LSEG_CC_SV
   // Run-level label propagation (Shiloach-Vishkin style, every thread doing
   // the same work -- the serial union-find chains of divergent lanes were the
   // cost here): labels live at run starts, L[start] <= start, and every other
@@ -1349,27 +1136,12 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
          (w1 ? 2u << 30 : 0u);
     any |= w0 | w1;
   }
-#if LSEG_CC_FIND
-  auto findr = [&](int x) -> int {  // chase to the current root (labels decrease along a chain)
-    int p = s_par[x];
-    while (p != x) {
-      x = p;
-      p = s_par[x];
-    }
-    return x;
-  };
-#endif
   auto hook = [&](unsigned ia, unsigned ib) -> int {
-#if LSEG_CC_FIND
-    const int la = findr(ia), lb = findr(ib);
-#else
     const int la = s_par[ia], lb = s_par[ib];
-#endif
     if (la == lb) return 0;
     const int hi = max(la, lb), lo = min(la, lb);
     return atomicMin(s_par + hi, lo) > lo;
   };
-#if LSEG_CC_LIST
   // the tile's edges as one dense shared-memory list (a | b << 10): every
   // round walks only real edges instead of each thread's ten slots
   __shared__ unsigned s_el[2 * NT + 64];
@@ -1403,18 +1175,6 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
         changed |= hook(v & 1023u, v >> 10);
       }
       __syncthreads();
-#else
-  if (__syncthreads_or(any)) {
-    while (true) {
-      int changed = 0;
-#pragma unroll
-      for (int j = 0; j <= NJ; ++j) {
-        const unsigned v = j < NJ ? pk[j] : pw;
-        if (v & (1u << 30)) changed |= hook(v & 1023u, (v >> 10) & 1023u);
-        if (v & (2u << 30)) changed |= hook(v & 1023u, (v >> 20) & 1023u);
-      }
-      __syncthreads();
-#endif
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {  // shortcut at run starts
         if (!((starts >> j) & 1u)) continue;
@@ -1426,26 +1186,6 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
       if (!__syncthreads_or(changed)) break;
     }
   }
-#else
-  for (int e = threadIdx.x; e < NT; e += T) {
-    const int y = e / TC, x = e - y * TC;
-    if ((s_U[2 * y] >> x) & 1ull) lunion(s_par, e, e + TC);
-    if ((s_U[2 * y + 1] >> x) & 1ull) lunion(s_par, e, e + TC + 1);
-  }
-  for (int y = threadIdx.x; y < TRe; y += T) {  // full-width column wrap (x = S'-1 -> 0)
-    const unsigned W = (unsigned)s_m[y * 5 + 4];
-    if (W & 1u) lunion(s_par, y * TC + TCe - 1, y * TC);
-    if (W & 2u) lunion(s_par, y * TC + TCe - 1, (y + 1) * TC);
-  }
-  __syncthreads();
-  // resolve each run start to its component root (minimum cell) ...
-  for (int e = threadIdx.x; e < NT; e += T) {
-    const int y = e / TC, x = e - y * TC;
-    const unsigned long long H = s_m[y * 5];
-    if (x == 0 || !((H >> (x - 1)) & 1ull)) s_par[e] = lfind(s_par, e);
-  }
-  __syncthreads();
-#endif
   // ... and give every labelled cell its run start's root; tile-local roots
   // (cells that are their own root) also get a bit in `lroots`, so the global
   // flatten only has to chase those
@@ -1455,12 +1195,7 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
     const bool in = (y < TRe && x < TCe);
     int pc = -1;
     if (in && ((s_m[y * 5 + 3] >> x) & 1ull)) {
-#if LSEG_CC_SV
       const int lr = s_par[s_par[e]];  // run start -> its label
-#else
-      const unsigned long long Z = ~s_m[y * 5] & ((1ull << x) - 1ull);
-      const int lr = s_par[y * TC + (Z ? 64 - __clzll((long long)Z) : 0)];
-#endif
       pc = (r0 + lr / TC) * sh.Sk + c0 + lr % TC;
     }
     const int cell = (r0 + y) * sh.Sk + c0 + x;
@@ -2223,12 +1958,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
     }
     cp.deg2 = 1e-30f;  // |V| < 1e-15: fp32 squares would leave the normal range
     constexpr int NH = (TILE_R + 2) * (TILE_C + 2), NT = TILE_R * TILE_C;
-#if LSEG_CERT_RECOMP
-    const size_t csmem = (size_t)NH * (8 + 4) + (size_t)(2 * (TILE_R + 2) + 2 * (TILE_C + 2)) * 8 +
-                         (size_t)NT * (3 * 4 + 2 + 2 + 2 + 3);  // see k_tile_cert
-#else
     const size_t csmem = (size_t)NH * (3 * 8 + 4) + (size_t)NT * (3 * 4 + 2 + 2 + 2 + 3);  // see k_tile_cert
-#endif
     // per launch: cheap, and correct for every device / thread (a static
     // "done" flag would not be)
     cudaFuncSetAttribute(k_tile_cert<TILE_R, TILE_C, TILE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2247,21 +1977,15 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
     prof_mark("merge", st);
   } else {
   const size_t tsmem =
-#if LSEG_POS_RECOMPUTE
       (size_t)((TILE_R + 2) * (TILE_C + 2) + 2 * (TILE_R + 2) + 2 * (TILE_C + 2) + 3 * TILE_R * TILE_C) * 8 +
-#else
-      (size_t)(3 * (TILE_R + 2) * (TILE_C + 2) + 3 * TILE_R * TILE_C) * 8 +
-#endif
       (size_t)(TILE_R + 2) * (TILE_C + 2) * 4 + (size_t)TILE_R * TILE_C * 4;
   cudaFuncSetAttribute(k_tile<TILE_R, TILE_C, TILE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
   k_tile<TILE_R, TILE_C, TILE_T><<<(unsigned)nt, TILE_T, tsmem, st>>>(sn, sh, ranges, ws.vbits, ws.wpre, thr[0], thr[1],
                                                                   thr[2], node_ids, neighbors, n32, nmask, ws.masks,
                                                                   ws.bnorm, ws.parent, ws.lroots, n_labels);
   prof_mark("tile", st);
-#if !LSEG_FUSE_CC
   k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
   prof_mark("tile_cc", st);
-#endif
   k_merge<TILE_R, TILE_C><<<dim3((per + 255) / 256, sh.F), 256, 0, st>>>(
       sh, ws.bnorm, thr[0], thr[1], thr[2], ws.parent);
   prof_mark("merge", st);
