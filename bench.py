@@ -150,7 +150,7 @@ def committed_traffic(kernel, frames, interval):
         return None
     e = t.get(kernel)
     if e and e.get("frames") == frames and e.get("interval") == interval:
-        return e["dram_bytes_per_launch"]
+        return e
     return None
 
 
@@ -346,10 +346,17 @@ def main():
         dom_ms = stages[dom][0] / stages[dom][1]
         ach = sb.get(dom, 0) / (dom_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "peak_kind": peak_kind,
-                "unit": "GB/s", "frac": ach / peak, "traffic": committed_traffic(dom, F, a.interval),
+                "unit": "GB/s", "frac": ach / peak,
                 "ms_per_launch": dom_ms,
                 "share_of_step": stages[dom][0] / a.steps / ms_step,
                 "alg_bytes_per_launch": sb.get(dom, 0)}
+        ct = committed_traffic(dom, F, a.interval)
+        roof["traffic"] = ct["dram_bytes_per_launch"] if ct else None
+        if ct and "fp64_pipe_active" in ct:
+            # what actually limits it (same capture): the kernel is FP64 / issue
+            # bound, not HBM bound -- see DESIGN.md §5
+            roof["limiter"] = {"fp64_pipe_active": ct["fp64_pipe_active"], "issue_active": ct["issue_active"],
+                               "source": ct["source"]}
     pb = pipeline_bytes(P, C, N)
     pipe_roof = {"alg_bytes_per_step": pb, "achieved_gbs": pb / (ms_step / 1e3) / 1e9,
                  "frac": pb / (ms_step / 1e3) / 1e9 / peak, "frac_of_8tbs": pb / (ms_step / 1e3) / 1e9 / 8000.0}
