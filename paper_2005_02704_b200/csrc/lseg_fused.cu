@@ -987,7 +987,8 @@ __device__ __forceinline__ void merge_cert_frame(const lseg_sensor& sn, const Sh
       r = v - bc * sh.R;
     }
     const int p = r * sh.Sk + c;
-    if (__ldcg(par + p) < 0) continue;  // no normal
+    const int pp = __ldcg(par + p);
+    if (pp < 0) continue;  // no normal
     const int tr = r / TR;
     const bool last_row = (r == min(tr * TR + TR - 1, sh.R - 1));
 #pragma unroll
@@ -996,7 +997,8 @@ __device__ __forceinline__ void merge_cert_frame(const lseg_sensor& sn, const Sh
       if (edge_internal<TR, TC>(r, c, s, sh.Sk)) continue;
       const int rq = r + slot_dr(s), cq = wrapc(c + slot_dc(s), sh.Sk);
       const int q = rq * sh.Sk + cq;
-      if (__ldcg(par + q) < 0) continue;
+      const int pq = __ldcg(par + q);
+      if (pq < 0) continue;
       float4 a, bq;
       if (slot_dr(s) == 1 && last_row) {
         a = __ldcg(bn + bn4_row(sh, 2 * tr + 1, c));
@@ -1022,7 +1024,7 @@ __device__ __forceinline__ void merge_cert_frame(const lseg_sensor& sn, const Sh
           }
         }
       }
-      if (d == 1) uf_union(par, p, q);
+      if (d == 1) uf_union_pre(par, p, pp, q, pq);  // a stale parent is still an ancestor
     }
   }
 }
@@ -1268,7 +1270,8 @@ __global__ void k_merge(Shape sh, const double* __restrict__ bnorm, double t0, d
       r = v - bc * sh.R;
     }
     const int p = r * sh.Sk + c;
-    if (__ldcg(par + p) < 0) continue;  // no normal
+    const int pp = __ldcg(par + p);
+    if (pp < 0) continue;  // no normal
     const int tr = r / TR, tc = c / TC;
     const bool last_row = (r == min(tr * TR + TR - 1, sh.R - 1));
     const bool last_col = (c == min(tc * TC + TC - 1, sh.Sk - 1));
@@ -1278,7 +1281,8 @@ __global__ void k_merge(Shape sh, const double* __restrict__ bnorm, double t0, d
       if (edge_internal<TR, TC>(r, c, s, sh.Sk)) continue;
       const int rq = r + slot_dr(s), cq = wrapc(c + slot_dc(s), sh.Sk);
       const int q = rq * sh.Sk + cq;
-      if (__ldcg(par + q) < 0) continue;
+      const int pq = __ldcg(par + q);
+      if (pq < 0) continue;
       // an edge that crosses a tile-row boundary reads both normals from the
       // row border store, one that only crosses a column boundary from the
       // column border store
@@ -1293,7 +1297,7 @@ __global__ void k_merge(Shape sh, const double* __restrict__ bnorm, double t0, d
       (void)last_col;
       const double a[3] = {__ldcg(pa), __ldcg(pa + 1), __ldcg(pa + 2)};
       const double b[3] = {__ldcg(pb), __ldcg(pb + 1), __ldcg(pb + 2)};
-      if (normals_pass(a, b, t0, t1, t2)) uf_union(par, p, q);
+      if (normals_pass(a, b, t0, t1, t2)) uf_union_pre(par, p, pp, q, pq);  // a stale parent is still an ancestor
     }
   }
 }
