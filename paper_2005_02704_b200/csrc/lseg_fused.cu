@@ -42,13 +42,22 @@ static constexpr int kUnrollNormals = LSEG_UNR;
 #endif
 static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_ROW_MINB
-#define LSEG_ROW_MINB 8
+#define LSEG_ROW_MINB 16
 #endif
 #ifndef LSEG_BIN_MINB
 #define LSEG_BIN_MINB 8
 #endif
+#ifndef LSEG_ROW_T
+#define LSEG_ROW_T 128
+#endif
+#ifndef LSEG_BIN_T
+#define LSEG_BIN_T 256
+#endif
+#ifndef LSEG_CC_T
+#define LSEG_CC_T 128
+#endif
 #ifndef LSEG_CC_MINB
-#define LSEG_CC_MINB 8
+#define LSEG_CC_MINB 16
 #endif
 #ifndef LSEG_CERT_MINB
 #define LSEG_CERT_MINB 4
@@ -1736,9 +1745,9 @@ static void bin_fused_t(const lseg_sensor& sn, const Shape& sh, const float* xyz
   cudaMemsetAsync(ws.fallback, 0, sizeof(int32_t) * sh.F, st);
   const size_t smem = sizeof(unsigned long long) * sh.S;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_bin_rows<256, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_bin_rows<LSEG_BIN_T, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_ring_bounds<RT><<<dim3((sh.R + 1 + 7) / 8, sh.F), 256, 0, st>>>(sh, ring, off, ws.seg);
-  k_bin_rows<256, RT><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, xyz, ring, off, ws.seg, ranges, ws.vbits, ws.fbits,
+  k_bin_rows<LSEG_BIN_T, RT><<<sh.F * sh.R, LSEG_BIN_T, smem, st>>>(sn, sh, xyz, ring, off, ws.seg, ranges, ws.vbits, ws.fbits,
                                                      ws.fallback);
   prof_mark("bin_rows", st);
 }
@@ -1750,8 +1759,8 @@ static void bin_fused_seg(const lseg_sensor& sn, const Shape& sh, const float* x
                           const int64_t* off, const Workspace& ws, double* ranges, cudaStream_t st) {
   const size_t smem = sizeof(unsigned long long) * sh.S;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_bin_rows<256, uint8_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_bin_rows<256, uint8_t, false><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, xyz, nullptr, off, segs, ranges, ws.vbits,
+    cudaFuncSetAttribute(k_bin_rows<LSEG_BIN_T, uint8_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_bin_rows<LSEG_BIN_T, uint8_t, false><<<sh.F * sh.R, LSEG_BIN_T, smem, st>>>(sn, sh, xyz, nullptr, off, segs, ranges, ws.vbits,
                                                                   ws.fbits, ws.fallback);
   prof_mark("bin_rows", st);
 }
@@ -1922,14 +1931,14 @@ __global__ void __launch_bounds__(T, LSEG_ROW_MINB) k_prune_rows(Shape sh, const
 }
 
 void launch_prune_fused(const Shape& sh, const Workspace& ws, int32_t min_size, int32_t* labels, cudaStream_t st) {
-  k_survivor_rows<256><<<sh.F * sh.R, 256, sizeof(int) * (size_t)sh.Wk, st>>>(
+  k_survivor_rows<LSEG_ROW_T><<<sh.F * sh.R, LSEG_ROW_T, sizeof(int) * (size_t)sh.Wk, st>>>(
       sh, ws.rbits, ws.hist, ws.K, min_size, ws.sbits, ws.spre, ws.rcnt, ws.fscal);
   prof_mark("prune_plan", st);
   const int nwr = (sh.S + 31) / 32;
   const size_t smem = sizeof(int) * ((size_t)nwr * 33 + (size_t)sh.R);
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_prune_rows<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_prune_rows<256><<<sh.F * sh.R, 256, smem, st>>>(sh, ws.lab_tmp, labels, ws.hist, ws.K, min_size, ws.fscal, ws.rbits,
+    cudaFuncSetAttribute(k_prune_rows<LSEG_ROW_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_prune_rows<LSEG_ROW_T><<<sh.F * sh.R, LSEG_ROW_T, smem, st>>>(sh, ws.lab_tmp, labels, ws.hist, ws.K, min_size, ws.fscal, ws.rbits,
                                                     ws.rpre, ws.sbits, ws.spre, ws.rcnt);
   prof_mark("prune_apply", st);
 }
@@ -1972,7 +1981,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
         sn, sh, ranges, ws.vbits, ws.wpre, cp, node_ids, neighbors, n32, nmask, ws.masks, bn4, ws.normals64, dbg_err,
         ws.fscal, n_labels);
     prof_mark("tile", st);
-    k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
+    k_tile_cc<TILE_R, TILE_C, LSEG_CC_T><<<(unsigned)nt, LSEG_CC_T, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
     prof_mark("tile_cc", st);
     k_merge_cert<TILE_R, TILE_C><<<dim3((per + 255) / 256, sh.F), 256, 0, st>>>(sn, sh, ranges, ws.vbits, bn4, cp,
                                                                                 ws.parent, ws.rank, ws.fscal);
@@ -1988,7 +1997,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
                                                                   thr[2], node_ids, neighbors, n32, nmask, ws.masks,
                                                                   ws.bnorm, ws.parent, ws.lroots, n_labels);
   prof_mark("tile", st);
-  k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
+  k_tile_cc<TILE_R, TILE_C, LSEG_CC_T><<<(unsigned)nt, LSEG_CC_T, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
   prof_mark("tile_cc", st);
   k_merge<TILE_R, TILE_C><<<dim3((per + 255) / 256, sh.F), 256, 0, st>>>(
       sh, ws.bnorm, thr[0], thr[1], thr[2], ws.parent);
@@ -2012,8 +2021,8 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   const size_t smem = sizeof(int) * (size_t)nwr * 33;
   const uint32_t* fb = (sh.k > 1 && fbits_valid) ? ws.fbits : nullptr;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_labels_backfill<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_labels_backfill<256><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits, ws.rpre,
+    cudaFuncSetAttribute(k_labels_backfill<LSEG_ROW_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_labels_backfill<LSEG_ROW_T><<<sh.F * sh.R, LSEG_ROW_T, smem, st>>>(sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits, ws.rpre,
                                                          node_labels, ws.lab_tmp, ws.hist, ws.K);
   prof_mark("labels_backfill", st);
 }
