@@ -47,6 +47,12 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_BIN_MINB
 #define LSEG_BIN_MINB 8
 #endif
+#ifndef LSEG_FLAT_T
+#define LSEG_FLAT_T 128
+#endif
+#ifndef LSEG_MERGE_T
+#define LSEG_MERGE_T 128
+#endif
 #ifndef LSEG_ROW_T
 #define LSEG_ROW_T 128
 #endif
@@ -1983,7 +1989,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
     prof_mark("tile", st);
     k_tile_cc<TILE_R, TILE_C, LSEG_CC_T><<<(unsigned)nt, LSEG_CC_T, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
     prof_mark("tile_cc", st);
-    k_merge_cert<TILE_R, TILE_C><<<dim3((per + 255) / 256, sh.F), 256, 0, st>>>(sn, sh, ranges, ws.vbits, bn4, cp,
+    k_merge_cert<TILE_R, TILE_C><<<dim3((per + LSEG_MERGE_T - 1) / LSEG_MERGE_T, sh.F), LSEG_MERGE_T, 0, st>>>(sn, sh, ranges, ws.vbits, bn4, cp,
                                                                                 ws.parent, ws.rank, ws.fscal);
     k_merge_exact<TILE_R, TILE_C><<<dim3(1, sh.F), 128, 0, st>>>(sn, sh, ranges, ws.vbits, bn4, cp, ws.parent,
                                                                  ws.rank, ws.fscal);
@@ -1999,7 +2005,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   prof_mark("tile", st);
   k_tile_cc<TILE_R, TILE_C, LSEG_CC_T><<<(unsigned)nt, LSEG_CC_T, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
   prof_mark("tile_cc", st);
-  k_merge<TILE_R, TILE_C><<<dim3((per + 255) / 256, sh.F), 256, 0, st>>>(
+  k_merge<TILE_R, TILE_C><<<dim3((per + LSEG_MERGE_T - 1) / LSEG_MERGE_T, sh.F), LSEG_MERGE_T, 0, st>>>(
       sh, ws.bnorm, thr[0], thr[1], thr[2], ws.parent);
   prof_mark("merge", st);
   }
@@ -2007,7 +2013,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
     const int64_t nwords = (int64_t)sh.F * sh.R * sh.Wk;
     const int64_t blocks = (nwords * 32 + 255) / 256;
     (void)blocks;
-    const int thr = sh.Wk >= 8 ? 256 : 32 * sh.Wk;
+    const int thr = sh.Wk >= LSEG_FLAT_T / 32 ? LSEG_FLAT_T : 32 * sh.Wk;
     k_root_flatten<<<sh.F * sh.R, thr, 0, st>>>(sh, ws.parent, ws.lroots, ws.rbits, ws.hist, ws.K, ws.fscal,
                                                 n_labels);
     prof_mark("root_flatten", st);
