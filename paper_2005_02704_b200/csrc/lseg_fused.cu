@@ -41,29 +41,8 @@ static constexpr int kUnrollNormals = LSEG_UNR;
 #define LSEG_FAST_MATH 1
 #endif
 static constexpr bool kFastMath = LSEG_FAST_MATH;
-#ifndef LSEG_ROW_MINB
-#define LSEG_ROW_MINB 16
-#endif
 #ifndef LSEG_BIN_MINB
 #define LSEG_BIN_MINB 8
-#endif
-#ifndef LSEG_FLAT_T
-#define LSEG_FLAT_T 128
-#endif
-#ifndef LSEG_MERGE_T
-#define LSEG_MERGE_T 128
-#endif
-#ifndef LSEG_ROW_T
-#define LSEG_ROW_T 128
-#endif
-#ifndef LSEG_BIN_T
-#define LSEG_BIN_T 256
-#endif
-#ifndef LSEG_CC_T
-#define LSEG_CC_T 128
-#endif
-#ifndef LSEG_CC_MINB
-#define LSEG_CC_MINB 16
 #endif
 #ifndef LSEG_CERT_MINB
 #define LSEG_CERT_MINB 4
@@ -1242,7 +1221,7 @@ void debug_tile_cc(int n, const unsigned long long* masks, int32_t* parent, uint
 }
 
 template <int TR, int TC, int T>
-__global__ void __launch_bounds__(T, LSEG_CC_MINB) k_tile_cc(Shape sh, const unsigned long long* __restrict__ masks,
+__global__ void __launch_bounds__(T, 2048 / T) k_tile_cc(Shape sh, const unsigned long long* __restrict__ masks,
                                                int32_t* __restrict__ parent, uint32_t* __restrict__ lroots) {
   __shared__ int s_par[TR * TC];
   __shared__ unsigned long long s_m[TR * 5];
@@ -1431,7 +1410,7 @@ __device__ __forceinline__ void hist_add(int32_t* hw, int lab) {
 // label ids are root cell + 1 (ascending root cell == ascending reference
 // label, so the compaction in k_prune_rows reproduces the reference ids).
 template <int T>
-__global__ void __launch_bounds__(T, LSEG_ROW_MINB) k_labels_backfill(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
+__global__ void __launch_bounds__(T, 2048 / T) k_labels_backfill(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
                                                        const uint32_t* __restrict__ vbits,
                                                        const uint32_t* __restrict__ fbits,
                                                        const int32_t* __restrict__ parent,
@@ -1751,9 +1730,9 @@ static void bin_fused_t(const lseg_sensor& sn, const Shape& sh, const float* xyz
   cudaMemsetAsync(ws.fallback, 0, sizeof(int32_t) * sh.F, st);
   const size_t smem = sizeof(unsigned long long) * sh.S;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_bin_rows<LSEG_BIN_T, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_bin_rows<256, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_ring_bounds<RT><<<dim3((sh.R + 1 + 7) / 8, sh.F), 256, 0, st>>>(sh, ring, off, ws.seg);
-  k_bin_rows<LSEG_BIN_T, RT><<<sh.F * sh.R, LSEG_BIN_T, smem, st>>>(sn, sh, xyz, ring, off, ws.seg, ranges, ws.vbits, ws.fbits,
+  k_bin_rows<256, RT><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, xyz, ring, off, ws.seg, ranges, ws.vbits, ws.fbits,
                                                      ws.fallback);
   prof_mark("bin_rows", st);
 }
@@ -1765,8 +1744,8 @@ static void bin_fused_seg(const lseg_sensor& sn, const Shape& sh, const float* x
                           const int64_t* off, const Workspace& ws, double* ranges, cudaStream_t st) {
   const size_t smem = sizeof(unsigned long long) * sh.S;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_bin_rows<LSEG_BIN_T, uint8_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_bin_rows<LSEG_BIN_T, uint8_t, false><<<sh.F * sh.R, LSEG_BIN_T, smem, st>>>(sn, sh, xyz, nullptr, off, segs, ranges, ws.vbits,
+    cudaFuncSetAttribute(k_bin_rows<256, uint8_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_bin_rows<256, uint8_t, false><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, xyz, nullptr, off, segs, ranges, ws.vbits,
                                                                   ws.fbits, ws.fallback);
   prof_mark("bin_rows", st);
 }
@@ -1859,7 +1838,7 @@ __global__ void __launch_bounds__(T) k_survivor_rows(Shape sh, const uint32_t* _
 // Dissolve small segments into the nearest surviving ring donor (reference
 // segment.py:141-154) and write the final compacted ids, one CTA per ring row.
 template <int T>
-__global__ void __launch_bounds__(T, LSEG_ROW_MINB) k_prune_rows(Shape sh, const int32_t* __restrict__ lab_in,
+__global__ void __launch_bounds__(T, 2048 / T) k_prune_rows(Shape sh, const int32_t* __restrict__ lab_in,
                                                   int32_t* __restrict__ out, const int32_t* __restrict__ hist,
                                                   int64_t K, int32_t min_size, const int32_t* __restrict__ fscal,
                                                   const uint32_t* __restrict__ rbits, const int32_t* __restrict__ rpre,
@@ -1937,15 +1916,27 @@ __global__ void __launch_bounds__(T, LSEG_ROW_MINB) k_prune_rows(Shape sh, const
 }
 
 void launch_prune_fused(const Shape& sh, const Workspace& ws, int32_t min_size, int32_t* labels, cudaStream_t st) {
-  k_survivor_rows<LSEG_ROW_T><<<sh.F * sh.R, LSEG_ROW_T, sizeof(int) * (size_t)sh.Wk, st>>>(
-      sh, ws.rbits, ws.hist, ws.K, min_size, ws.sbits, ws.spre, ws.rcnt, ws.fscal);
+  // 128-thread CTAs (16 per SM) for throughput; one-wave batches (single
+  // scans) use 256 threads per row to cut the per-row latency
+  const bool wide = (int64_t)sh.F * sh.R < 148 * 8;
+  if (wide)
+    k_survivor_rows<256><<<sh.F * sh.R, 256, sizeof(int) * (size_t)sh.Wk, st>>>(
+        sh, ws.rbits, ws.hist, ws.K, min_size, ws.sbits, ws.spre, ws.rcnt, ws.fscal);
+  else
+    k_survivor_rows<128><<<sh.F * sh.R, 128, sizeof(int) * (size_t)sh.Wk, st>>>(
+        sh, ws.rbits, ws.hist, ws.K, min_size, ws.sbits, ws.spre, ws.rcnt, ws.fscal);
   prof_mark("prune_plan", st);
   const int nwr = (sh.S + 31) / 32;
   const size_t smem = sizeof(int) * ((size_t)nwr * 33 + (size_t)sh.R);
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_prune_rows<LSEG_ROW_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_prune_rows<LSEG_ROW_T><<<sh.F * sh.R, LSEG_ROW_T, smem, st>>>(sh, ws.lab_tmp, labels, ws.hist, ws.K, min_size, ws.fscal, ws.rbits,
-                                                    ws.rpre, ws.sbits, ws.spre, ws.rcnt);
+    for (auto fn : {k_prune_rows<128>, k_prune_rows<256>})
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (wide)
+    k_prune_rows<256><<<sh.F * sh.R, 256, smem, st>>>(sh, ws.lab_tmp, labels, ws.hist, ws.K, min_size, ws.fscal,
+                                                      ws.rbits, ws.rpre, ws.sbits, ws.spre, ws.rcnt);
+  else
+    k_prune_rows<128><<<sh.F * sh.R, 128, smem, st>>>(sh, ws.lab_tmp, labels, ws.hist, ws.K, min_size, ws.fscal,
+                                                      ws.rbits, ws.rpre, ws.sbits, ws.spre, ws.rcnt);
   prof_mark("prune_apply", st);
 }
 
@@ -1968,6 +1959,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   const int tilesC = (sh.Sk + TILE_C - 1) / TILE_C, tilesR = (sh.R + TILE_R - 1) / TILE_R;
   const int64_t nt = (int64_t)sh.F * tilesR * tilesC;
   const int per = tilesR * sh.Sk + tilesC * sh.R;
+  const int mt = sh.F < 8 ? 64 : 128;  // border-merge threads per CTA (more CTAs for single scans)
   if (!exact_normals) {
     CertParams cp;
     for (int c = 0; c < 3; ++c) {
@@ -1987,9 +1979,12 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
         sn, sh, ranges, ws.vbits, ws.wpre, cp, node_ids, neighbors, n32, nmask, ws.masks, bn4, ws.normals64, dbg_err,
         ws.fscal, n_labels);
     prof_mark("tile", st);
-    k_tile_cc<TILE_R, TILE_C, LSEG_CC_T><<<(unsigned)nt, LSEG_CC_T, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
+    if (nt < 148 * 16)  // one-wave batches: 256 threads per tile for latency
+      k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
+    else
+      k_tile_cc<TILE_R, TILE_C, 128><<<(unsigned)nt, 128, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
     prof_mark("tile_cc", st);
-    k_merge_cert<TILE_R, TILE_C><<<dim3((per + LSEG_MERGE_T - 1) / LSEG_MERGE_T, sh.F), LSEG_MERGE_T, 0, st>>>(sn, sh, ranges, ws.vbits, bn4, cp,
+    k_merge_cert<TILE_R, TILE_C><<<dim3((per + mt - 1) / mt, sh.F), mt, 0, st>>>(sn, sh, ranges, ws.vbits, bn4, cp,
                                                                                 ws.parent, ws.rank, ws.fscal);
     k_merge_exact<TILE_R, TILE_C><<<dim3(1, sh.F), 128, 0, st>>>(sn, sh, ranges, ws.vbits, bn4, cp, ws.parent,
                                                                  ws.rank, ws.fscal);
@@ -2003,9 +1998,12 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
                                                                   thr[2], node_ids, neighbors, n32, nmask, ws.masks,
                                                                   ws.bnorm, ws.parent, ws.lroots, n_labels);
   prof_mark("tile", st);
-  k_tile_cc<TILE_R, TILE_C, LSEG_CC_T><<<(unsigned)nt, LSEG_CC_T, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
+  if (nt < 148 * 16)  // one-wave batches: 256 threads per tile for latency
+    k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
+  else
+    k_tile_cc<TILE_R, TILE_C, 128><<<(unsigned)nt, 128, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
   prof_mark("tile_cc", st);
-  k_merge<TILE_R, TILE_C><<<dim3((per + LSEG_MERGE_T - 1) / LSEG_MERGE_T, sh.F), LSEG_MERGE_T, 0, st>>>(
+  k_merge<TILE_R, TILE_C><<<dim3((per + mt - 1) / mt, sh.F), mt, 0, st>>>(
       sh, ws.bnorm, thr[0], thr[1], thr[2], ws.parent);
   prof_mark("merge", st);
   }
@@ -2013,7 +2011,8 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
     const int64_t nwords = (int64_t)sh.F * sh.R * sh.Wk;
     const int64_t blocks = (nwords * 32 + 255) / 256;
     (void)blocks;
-    const int thr = sh.Wk >= LSEG_FLAT_T / 32 ? LSEG_FLAT_T : 32 * sh.Wk;
+    const int ft = (int64_t)sh.F * sh.R < 148 * 8 ? 256 : 128;  // one-wave batches: wider CTAs
+    const int thr = sh.Wk >= ft / 32 ? ft : 32 * sh.Wk;
     k_root_flatten<<<sh.F * sh.R, thr, 0, st>>>(sh, ws.parent, ws.lroots, ws.rbits, ws.hist, ws.K, ws.fscal,
                                                 n_labels);
     prof_mark("root_flatten", st);
@@ -2027,9 +2026,14 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   const size_t smem = sizeof(int) * (size_t)nwr * 33;
   const uint32_t* fb = (sh.k > 1 && fbits_valid) ? ws.fbits : nullptr;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_labels_backfill<LSEG_ROW_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_labels_backfill<LSEG_ROW_T><<<sh.F * sh.R, LSEG_ROW_T, smem, st>>>(sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits, ws.rpre,
-                                                         node_labels, ws.lab_tmp, ws.hist, ws.K);
+    for (auto fn : {k_labels_backfill<128>, k_labels_backfill<256>})
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if ((int64_t)sh.F * sh.R < 148 * 8)  // one-wave batches: 256 threads per row for latency
+    k_labels_backfill<256><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits,
+                                                           ws.rpre, node_labels, ws.lab_tmp, ws.hist, ws.K);
+  else
+    k_labels_backfill<128><<<sh.F * sh.R, 128, smem, st>>>(sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits,
+                                                           ws.rpre, node_labels, ws.lab_tmp, ws.hist, ws.K);
   prof_mark("labels_backfill", st);
 }
 
