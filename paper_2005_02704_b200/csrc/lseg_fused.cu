@@ -44,6 +44,9 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_BIN_MINB
 #define LSEG_BIN_MINB 8
 #endif
+#ifndef LSEG_PF
+#define LSEG_PF 8
+#endif
 #ifndef LSEG_CERT_MINB
 #define LSEG_CERT_MINB 4
 #endif
@@ -1438,7 +1441,7 @@ __global__ void __launch_bounds__(T, 2048 / T) k_labels_backfill(lseg_sensor sn,
   // classify: donor label / target -2 / passive 0.  Chunks of PF cells per
   // thread with all loads of a chunk issued before they are used (the two
   // dependent parent loads would otherwise serialise per cell).
-  constexpr int PF = 8;
+  constexpr int PF = LSEG_PF;
   for (int s0 = 0; s0 < nw * 32; s0 += T * PF) {
     int pv[PF], lv[PF];
 #pragma unroll
@@ -1879,7 +1882,7 @@ __global__ void __launch_bounds__(T, 2048 / T) k_prune_rows(Shape sh, const int3
   }
   __syncthreads();
   bool any = false;
-  constexpr int PF = 8;
+  constexpr int PF = LSEG_PF;
   for (int s0 = 0; s0 < nw * 32; s0 += T * PF) {
     int lv[PF], hv[PF];
 #pragma unroll
