@@ -280,6 +280,7 @@ class StreamingPipeline:
                  ring_dtype=torch.int32, normals: str = "exact"):
         self.device = torch.device(device or "cuda")
         self.cf = int(chunk_frames)
+        self.taper_min = max(1, self.cf // 8)
         R, S = config.rings, config.azimuth_steps
         self.maxp = int(max_chunk_points or self.cf * R * S)
         self.bps = [BatchPipeline(config, interval, segmenter, frames=self.cf, device=self.device, normals=normals)
@@ -307,9 +308,17 @@ class StreamingPipeline:
         start.record(cur)
         for s in (self.s_in, self.s_run, self.s_out):
             s.wait_event(start)
-        for ci, f0 in enumerate(range(0, F, self.cf)):
+        # chunk boundaries: full chunks, then a geometric taper (1/2, 1/4, ...)
+        # so the pipeline drain -- the last chunk's kernels + label copy,
+        # which nothing overlaps -- is short
+        bounds = [0]
+        while bounds[-1] < F:
+            left = F - bounds[-1]
+            step = self.cf if left > 2 * self.cf else max(self.taper_min, min(self.cf, (left + 1) // 2))
+            bounds.append(min(F, bounds[-1] + step))
+        for ci in range(len(bounds) - 1):
             b = ci % 2
-            f1 = min(F, f0 + self.cf)
+            f0, f1 = bounds[ci], bounds[ci + 1]
             nf = f1 - f0
             p0, p1 = offs[f0], offs[f1]
             if p1 - p0 > self.maxp:
