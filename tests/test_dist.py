@@ -4,8 +4,6 @@ owned exactly once, and the reduced totals equal a single-process run."""
 import os
 import socket
 
-import numpy as np
-import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 

@@ -3,7 +3,6 @@ writer must reproduce the reference's bytes exactly (tests/golden/io0.npz,
 made by make_golden_io.py), parsers must round-trip, and the native repr
 formatter must equal Python's repr(float) on edge cases."""
 
-import ctypes as C
 
 import numpy as np
 import pytest
