@@ -418,3 +418,36 @@ def test_cuda_graph_capture_replays_exactly(L):
             want = eager.run(x, r, o)
             torch.cuda.synchronize()
             assert torch.equal(bp.labels, want)
+
+
+def test_full_bench_batch_sampled_vs_oracle(L, oracle):
+    """The bench workload at its full size (512 HDL-64 frames, one batch):
+    four sampled frames equal the oracle exactly, and every frame satisfies
+    the size-independent invariants -- final labels are exactly 1..n_final
+    (compacted, no gaps), every labelled cell is a valid cell, and a ring
+    with any label has all its valid cells labelled (backfill)."""
+    from paper_2005_02704_b200 import synth
+    shape = synth.CONFIGS["hdl64_batch"]
+    F = shape.frames
+    xyz, ring, off = synth.make_batch(shape, frames=F, seed=2005, device="cuda")
+    cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
+                         r_max=shape.r_max)
+    bp = L.BatchPipeline(cfg, 1, frames=F)
+    labels = bp.run(xyz, ring, off)
+    torch.cuda.synchronize()
+    # invariants on every frame (device-side)
+    valid = torch.isfinite(bp.ranges) & (bp.ranges >= shape.r_min) & (bp.ranges <= shape.r_max)
+    assert not bool(((labels > 0) & ~valid).any())
+    mx = labels.amax(dim=(1, 2))
+    for f in range(F):
+        present = torch.zeros(int(mx[f]) + 1, dtype=torch.bool, device="cuda")
+        present[labels[f].reshape(-1).long()] = True
+        assert bool(present[1:].all()), f"frame {f}: label ids not compact"
+    ring_has = (labels > 0).any(dim=2, keepdim=True)
+    assert not bool((ring_has & valid & (labels == 0)).any())
+    # four sampled frames against the oracle
+    xh, rh, oh = xyz.cpu().numpy(), ring.cpu().numpy(), off.cpu().numpy()
+    for f in (0, 137, 300, F - 1):
+        sl = slice(oh[f], oh[f + 1])
+        want = oracle.run_from_points(xh[sl], rh[sl], shape.elevations, shape.steps, 1, shape.r_min, shape.r_max)
+        np.testing.assert_array_equal(labels[f].cpu().numpy(), want["labels"])
