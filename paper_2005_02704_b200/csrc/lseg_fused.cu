@@ -1065,7 +1065,7 @@ __global__ void k_merge_exact(lseg_sensor sn, Shape sh, const double* __restrict
 // k_tile_cc, one small CTA per tile): each node's parent starts as the first
 // cell of its horizontal run (bit arithmetic); vertical / diagonal edges --
 // minus those whose parallel edge one column to the left already joins the
-// same two runs -- join runs by label propagation in shared memory; each
+// same two runs -- join runs by union-find in shared memory; each
 // labelled cell gets parent[cell] = minimum cell of its tile-local component
 // (-1 without a normal).
 template <int TR, int TC, int T>
@@ -1096,15 +1096,13 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
     s_U[2 * y + 1] = U1;
   }
   __syncthreads();
-  // Run-level label propagation (Shiloach-Vishkin style, every thread doing
-  // the same work -- the serial union-find chains of divergent lanes were the
-  // cost here): labels live at run starts, L[start] <= start, and every other
-  // cell keeps s_par = its run start throughout.  Hook: for every kept
-  // vertical edge link the larger of the two current labels to the smaller
-  // (atomicMin); shortcut (run starts only): L[a] = L[L[a]].  Repeat until
-  // nothing changes; then every run's label is its component's minimum run
-  // start.  A thread's edges live in registers, packed as
-  // a | b0 << 10 | b1 << 20 | valid bits << 30 (10-bit tile cell indices).
+  // Union-find over runs: labels live at run starts (every other cell keeps
+  // s_par = its run start throughout).  The tile's run-to-run edges are
+  // gathered into one dense shared-memory list (packed per thread first as
+  // a | b0 << 10 | b1 << 20 | valid bits << 30, 10-bit tile cell indices);
+  // all threads then union them lock-free (atomicCAS, larger root hooked
+  // under the smaller, so each root is its component's minimum run start)
+  // and compress the run starts -- two barriers, no rounds.
   static_assert(NT <= 1024, "10-bit cell indices");
   constexpr int NJ = (NT + T - 1) / T;
   unsigned pk[NJ];
@@ -1135,12 +1133,6 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
          (w1 ? 2u << 30 : 0u);
     any |= w0 | w1;
   }
-  auto hook = [&](unsigned ia, unsigned ib) -> int {
-    const int la = s_par[ia], lb = s_par[ib];
-    if (la == lb) return 0;
-    const int hi = max(la, lb), lo = min(la, lb);
-    return atomicMin(s_par + hi, lo) > lo;
-  };
   // the tile's edges as one dense shared-memory list (a | b << 10): every
   // round walks only real edges instead of each thread's ten slots
   __shared__ unsigned s_el[2 * NT + 64];
@@ -1167,23 +1159,33 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
   __syncthreads();
   const int ne = s_ne;
   if (ne) {
-    while (true) {
-      int changed = 0;
-      for (int k = threadIdx.x; k < ne; k += T) {
-        const unsigned v = s_el[k];
-        changed |= hook(v & 1023u, v >> 10);
+    // lock-free union-find over the run-start labels (larger root hooked
+    // under the smaller: root = component minimum), then full compression
+    // at run starts
+    auto root = [&](int x) -> int {
+      int p = s_par[x];
+      while (p != x) {
+        x = p;
+        p = s_par[x];
       }
-      __syncthreads();
-#pragma unroll
-      for (int j = 0; j < NJ; ++j) {  // shortcut at run starts
-        if (!((starts >> j) & 1u)) continue;
-        const int e = threadIdx.x + j * T;
-        const int l = s_par[e];
-        const int ll = s_par[l];
-        if (ll != l) { s_par[e] = ll; changed = 1; }
+      return x;
+    };
+    for (int k = threadIdx.x; k < ne; k += T) {
+      const unsigned v = s_el[k];
+      int ra = root(v & 1023u), rb = root(v >> 10);
+      while (ra != rb) {
+        if (ra < rb) { const int t = ra; ra = rb; rb = t; }
+        const int old = atomicCAS(s_par + ra, ra, rb);
+        if (old == ra) break;
+        ra = root(old);
+        rb = root(rb);
       }
-      if (!__syncthreads_or(changed)) break;
     }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+      if ((starts >> j) & 1u) s_par[threadIdx.x + j * T] = root(threadIdx.x + j * T);
+    __syncthreads();
   }
   // ... and give every labelled cell its run start's root; tile-local roots
   // (cells that are their own root) also get a bit in `lroots`, so the global
