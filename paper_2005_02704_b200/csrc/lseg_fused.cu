@@ -44,6 +44,9 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_BIN_MINB
 #define LSEG_BIN_MINB 8
 #endif
+#ifndef LSEG_CC_TBIG
+#define LSEG_CC_TBIG 128
+#endif
 #ifndef LSEG_PF
 #define LSEG_PF 8
 #endif
@@ -1987,7 +1990,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
     if (nt < 148 * 16)  // one-wave batches: 256 threads per tile for latency
       k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
     else
-      k_tile_cc<TILE_R, TILE_C, 128><<<(unsigned)nt, 128, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
+      k_tile_cc<TILE_R, TILE_C, LSEG_CC_TBIG><<<(unsigned)nt, LSEG_CC_TBIG, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
     prof_mark("tile_cc", st);
     k_merge_cert<TILE_R, TILE_C><<<dim3((per + mt - 1) / mt, sh.F), mt, 0, st>>>(sn, sh, ranges, ws.vbits, bn4, cp,
                                                                                 ws.parent, ws.rank, ws.fscal);
@@ -2006,7 +2009,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   if (nt < 148 * 16)  // one-wave batches: 256 threads per tile for latency
     k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
   else
-    k_tile_cc<TILE_R, TILE_C, 128><<<(unsigned)nt, 128, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
+    k_tile_cc<TILE_R, TILE_C, LSEG_CC_TBIG><<<(unsigned)nt, LSEG_CC_TBIG, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
   prof_mark("tile_cc", st);
   k_merge<TILE_R, TILE_C><<<dim3((per + mt - 1) / mt, sh.F), mt, 0, st>>>(
       sh, ws.bnorm, thr[0], thr[1], thr[2], ws.parent);
