@@ -48,7 +48,7 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #define LSEG_CC_TBIG 128
 #endif
 #ifndef LSEG_PF
-#define LSEG_PF 8
+#define LSEG_PF 4
 #endif
 #ifndef LSEG_CERT_MINB
 #define LSEG_CERT_MINB 4
@@ -1861,7 +1861,6 @@ __global__ void __launch_bounds__(T, 2048 / T) k_prune_rows(Shape sh, const int3
   const int row = blockIdx.x;
   const int f = row / sh.R;
   const bool any_small = fscal[f * 4] != 0;
-  const int32_t* hf = hist + (int64_t)f * K;
   // final ids = 1 + rank of the root among the frame's survivors (all roots
   // when nothing is small): row base + row-local word prefix + bit rank
   const uint32_t* bb = sbits + (int64_t)f * sh.R * sh.Wk;
@@ -1886,22 +1885,49 @@ __global__ void __launch_bounds__(T, 2048 / T) k_prune_rows(Shape sh, const int3
     }
   }
   __syncthreads();
+  // pass 1: each labelled cell's root is looked up in the survivor bits --
+  // dissolved (not a survivor) -> target (-2), survivor -> its final id
+  // right away, so the fill pass only copies ids
+  (void)hist;
+  (void)K;
+  (void)min_size;
+  (void)any_small;
   bool any = false;
   constexpr int PF = LSEG_PF;
   for (int s0 = 0; s0 < nw * 32; s0 += T * PF) {
-    int lv[PF], hv[PF];
+    int lv[PF], ro[PF], cb[PF];
+    uint32_t wv[PF];
+    int pv[PF];
 #pragma unroll
     for (int j = 0; j < PF; ++j) {
       const int s = s0 + threadIdx.x + j * T;
       lv[j] = (s < S) ? __ldcg(lab_in + rb + s) : 0;
     }
 #pragma unroll
-    for (int j = 0; j < PF; ++j) hv[j] = (any_small && lv[j] > 0) ? __ldg(hf + lv[j]) : INT_MAX;
+    for (int j = 0; j < PF; ++j) {
+      ro[j] = 0;
+      cb[j] = 0;
+      wv[j] = 0u;
+      pv[j] = 0;
+      if (lv[j] > 0) {
+        const int rc = lv[j] - 1;
+        const int rr = fdiv(rc, sh.Sk, sh.inv_Sk), cc = rc - rr * sh.Sk;
+        ro[j] = rr;
+        cb[j] = cc & 31;
+        const int64_t wi = (int64_t)rr * sh.Wk + (cc >> 5);
+        wv[j] = __ldg(bb + wi);
+        pv[j] = __ldg(bp + wi);
+      }
+    }
 #pragma unroll
     for (int j = 0; j < PF; ++j) {
       const int s = s0 + threadIdx.x + j * T;
       if (s >= nw * 32) break;
-      const int v = (hv[j] < min_size) ? -2 : lv[j];  // dissolved: becomes a target
+      int v = 0;
+      if (lv[j] > 0) {
+        const uint32_t bit = 1u << cb[j];
+        v = (wv[j] & bit) ? 1 + s_base[ro[j]] + pv[j] + __popc(wv[j] & (bit - 1u)) : -2;
+      }
       s_val[s] = v;
       const uint32_t dm = __ballot_sync(0xffffffffu, v > 0);
       if ((s & 31) == 0) s_dm[s >> 5] = dm;
@@ -1911,16 +1937,7 @@ __global__ void __launch_bounds__(T, 2048 / T) k_prune_rows(Shape sh, const int3
   if (any && (threadIdx.x & 31) == 0) s_any = 1;
   __syncthreads();
   const bool rany = s_any != 0;
-  for (int s = threadIdx.x; s < S; s += T) {
-    const int v = fill_one(s_val, s_dm, nw, S, s, rany);
-    int o = 0;
-    if (v > 0) {
-      const int rc = v - 1;
-      const int rr = fdiv(rc, sh.Sk, sh.inv_Sk), cc = rc - rr * sh.Sk;
-      o = 1 + s_base[rr] + node_id_at(bb + (int64_t)rr * sh.Wk, bp + (int64_t)rr * sh.Wk, cc);
-    }
-    out[rb + s] = o;
-  }
+  for (int s = threadIdx.x; s < S; s += T) out[rb + s] = fill_one(s_val, s_dm, nw, S, s, rany);
 }
 
 void launch_prune_fused(const Shape& sh, const Workspace& ws, int32_t min_size, int32_t* labels, cudaStream_t st) {
