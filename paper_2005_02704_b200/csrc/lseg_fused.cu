@@ -1634,12 +1634,22 @@ __global__ void __launch_bounds__(T, LSEG_BIN_MINB) k_bin_rows(lseg_sensor sn, S
     return;
   }
   double* out = ranges + row * S;
-  for (int s = threadIdx.x; s < S; s += T) out[s] = __longlong_as_double((long long)s_cell[s]);
   const int lane = threadIdx.x & 31;
+  // every binned range passed the window test in bin_xyz: a cell is valid
+  // iff it received a point (the empty pattern ~0 is a NaN)
+  if (sh.k == 1) {  // row out + valid bits in one pass (kept cells = cells)
+    for (int w = threadIdx.x >> 5; w < sh.Wk; w += T / 32) {
+      const int c = w * 32 + lane;
+      const unsigned long long v = c < S ? s_cell[c] : ~0ull;
+      if (c < S) out[c] = __longlong_as_double((long long)v);
+      const uint32_t b = __ballot_sync(0xffffffffu, v != ~0ull);
+      if (lane == 0) vbits[row * sh.Wk + w] = b;
+    }
+    return;
+  }
+  for (int s = threadIdx.x; s < S; s += T) out[s] = __longlong_as_double((long long)s_cell[s]);
   for (int w = threadIdx.x >> 5; w < sh.Wk; w += T / 32) {
     const int c = w * 32 + lane;
-    // every binned range passed the window test in bin_xyz: a cell is valid
-    // iff it received a point (the empty pattern ~0 is a NaN)
     const bool v = (c < sh.Sk) && s_cell[c * sh.k] != ~0ull;
     const uint32_t b = __ballot_sync(0xffffffffu, v);
     if (lane == 0) vbits[row * sh.Wk + w] = b;
