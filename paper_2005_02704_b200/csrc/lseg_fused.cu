@@ -1110,7 +1110,6 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
   constexpr int NJ = (NT + T - 1) / T;
   unsigned pk[NJ];
   unsigned starts = 0;  // which of this thread's cells are run starts
-  int any = 0;
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
     const int e = threadIdx.x + j * T;
@@ -1122,59 +1121,56 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
       const bool u0 = (s_U[2 * y] >> x) & 1ull, u1 = (s_U[2 * y + 1] >> x) & 1ull;
       const unsigned b0 = u0 ? (unsigned)s_par[e + TC] : 0u, b1 = u1 ? (unsigned)s_par[e + TC + 1] : 0u;
       pk[j] = (unsigned)a | b0 << 10 | b1 << 20 | (u0 ? 1u << 30 : 0u) | (u1 ? 2u << 30 : 0u);
-      any |= u0 | u1;
     }
   }
   unsigned pw = 0;
-  if (threadIdx.x < TRe) {  // full-width column wrap (x = S'-1 -> 0)
-    const int y = threadIdx.x;
+  const int wy = (int)threadIdx.x - (T - 32);  // the last warp (fewest edges: it holds row TR-1) adds the wraps
+  if (wy >= 0 && wy < TRe) {  // full-width column wrap (x = S'-1 -> 0)
+    const int y = wy;
     const unsigned W = (unsigned)s_m[y * 5 + 4];
     const unsigned a = (unsigned)s_par[y * TC + TCe - 1];
     const bool w0 = W & 1u, w1 = (W & 2u) && (y + 1 < TRe);
     // (y + 1) * TC is 1024 on the last row: only packed when that edge exists
     pw = a | (unsigned)(y * TC) << 10 | (w1 ? (unsigned)((y + 1) * TC) << 20 : 0u) | (w0 ? 1u << 30 : 0u) |
          (w1 ? 2u << 30 : 0u);
-    any |= w0 | w1;
   }
-  // the tile's edges as one dense shared-memory list (a | b << 10): every
-  // round walks only real edges instead of each thread's ten slots
-  __shared__ unsigned s_el[2 * NT + 64];
-  __shared__ int s_ne;
-  if (threadIdx.x == 0) s_ne = 0;
-  __syncthreads();
-  {
-    const int lane = threadIdx.x & 31;
+  // each warp's edges as a dense list (a | b << 10) in its own shared-memory
+  // segment (appended without atomics), then unioned by the same warp:
+  // no block barrier between gathering and union
+  constexpr int SEG = 2 * NT / (T / 32);  // >= 2 edges per cell of the warp (+ the wraps, see above)
+  __shared__ unsigned s_el[2 * NT];
+  const int lane = threadIdx.x & 31;
+  unsigned* el = s_el + (threadIdx.x >> 5) * SEG;
+  int ne = 0;
 #pragma unroll
-    for (int j = 0; j <= NJ; ++j) {
-      const unsigned v = j < NJ ? pk[j] : pw;
+  for (int j = 0; j <= NJ; ++j) {
+    const unsigned v = j < NJ ? pk[j] : pw;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const bool has = v & ((1u << 30) << h);
-        const unsigned bal = __ballot_sync(0xffffffffu, has);
-        if (!bal) continue;
-        int base = 0;
-        if (lane == 0) base = atomicAdd(&s_ne, __popc(bal));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (has) s_el[base + __popc(bal & ((1u << lane) - 1u))] = (v & 1023u) | (((v >> (10 + 10 * h)) & 1023u) << 10);
-      }
+    for (int h = 0; h < 2; ++h) {
+      const bool has = v & ((1u << 30) << h);
+      const unsigned bal = __ballot_sync(0xffffffffu, has);
+      if (has) el[ne + __popc(bal & ((1u << lane) - 1u))] = (v & 1023u) | (((v >> (10 + 10 * h)) & 1023u) << 10);
+      ne += __popc(bal);
     }
   }
-  __syncthreads();
-  const int ne = s_ne;
-  if (ne) {
+  __syncwarp();
+  const int any_edge = __syncthreads_or(ne);
+  if (any_edge) {
     // lock-free union-find over the run-start labels (larger root hooked
-    // under the smaller: root = component minimum), then full compression
-    // at run starts
+    // under the smaller: root = component minimum; path halving on the way),
+    // then full compression at run starts
     auto root = [&](int x) -> int {
       int p = s_par[x];
       while (p != x) {
+        const int g = s_par[p];
+        if (g != p) s_par[x] = g;  // x is not a root: only ever points further up
         x = p;
-        p = s_par[x];
+        p = g;
       }
       return x;
     };
-    for (int k = threadIdx.x; k < ne; k += T) {
-      const unsigned v = s_el[k];
+    for (int k = lane; k < ne; k += 32) {
+      const unsigned v = el[k];
       int ra = root(v & 1023u), rb = root(v >> 10);
       while (ra != rb) {
         if (ra < rb) { const int t = ra; ra = rb; rb = t; }
