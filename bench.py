@@ -132,8 +132,7 @@ def stage_bytes(P, C, Ck, N):
         "root_flatten": 4 * Ck + Ck / 8,
         "root_scan": Ck / 4,
         "labels_backfill": 4 * Ck + Ck / 8 + 8 * (C - Ck) + 4 * C,
-        "prune_plan": Ck / 8 + Ck / 4,
-        "prune_apply": 8 * C + Ck / 4,
+        "prune_apply": 8 * C + Ck / 8 + Ck / 4 + Ck / 4,  # labels in/out; root bits in, survivor bits + prefix out
         # single-op (unfused) path stages
         "bin_fill": 8 * C, "bin": 24 * P, "valid_bits": 8 * Ck, "mesh": 4 * Ck + 24 * N,
         "normals": 12 * Ck + 24 * N + 37 * N,

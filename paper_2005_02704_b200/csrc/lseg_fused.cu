@@ -1312,7 +1312,8 @@ __device__ __forceinline__ int root_of(const int32_t* __restrict__ par, int x) {
 // and zero each root's histogram slot (labels are root cell + 1 until pruning).
 __global__ void k_root_flatten(Shape sh, int32_t* __restrict__ parent, const uint32_t* __restrict__ lroots,
                                uint32_t* __restrict__ rbits, int32_t* __restrict__ hist, int64_t K,
-                               int32_t* __restrict__ fscal, int32_t* __restrict__ n_labels) {
+                               int32_t* __restrict__ fscal, int32_t* __restrict__ rstat,
+                               int32_t* __restrict__ n_labels) {
   // after k_merge: point every tile-local root straight at its final root
   // (the only cells whose chains can be long; every other cell points at its
   // tile-local root, so its final root is parent[parent[cell]]), mark final
@@ -1323,7 +1324,10 @@ __global__ void k_root_flatten(Shape sh, int32_t* __restrict__ parent, const uin
   const int lane = threadIdx.x & 31;
   int32_t* par = parent + (int64_t)f * sh.cap;
   int32_t* hf = hist + (int64_t)f * K;
-  if (i == 0 && threadIdx.x == 0) fscal[f * 4] = 0;  // k_survivor_rows' any-small flag
+  if (threadIdx.x == 0) {
+    rstat[row] = 0;                   // k_prune_rows' per-row survivor count (+ ready flag)
+    if (row == 0) fscal[3] = 0;       // k_prune_rows' row ticket
+  }
   __shared__ int s_nroot;
   if (threadIdx.x == 0) s_nroot = 0;
   __syncthreads();
@@ -1784,120 +1788,120 @@ void launch_bin_fused(const lseg_sensor& sn, const Shape& sh, const float* xyz, 
   prof_mark("frame_scan", st);
 }
 
-// Pruning plan over roots, one CTA per ring row (all rows in parallel): a
-// root survives unless its post-backfill count is below min_size (reference
-// segment.py:136-140); survivor bits, their row-local exclusive word prefix
-// and the row's survivor count.  k_prune_rows turns the per-row counts into
-// row bases.  fscal[f*4] = 1 when some label of frame f is small (zeroed by
-// k_root_flatten).  One warp per 32-cell word: the histogram reads of a word
-// are one coalesced load.
-template <int T>
-__global__ void __launch_bounds__(T) k_survivor_rows(Shape sh, const uint32_t* __restrict__ rbits,
-                                                     const int32_t* __restrict__ hist, int64_t K, int32_t min_size,
-                                                     uint32_t* __restrict__ sbits, int32_t* __restrict__ spre,
-                                                     int32_t* __restrict__ rcnt, int32_t* __restrict__ fscal) {
-  constexpr int NW = T / 32;
-  extern __shared__ int s_wc[];  // per-word survivor counts of the row
-  __shared__ int s_part[NW];
-  const int row = blockIdx.x;
-  const int f = row / sh.R, i = row - f * sh.R;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int32_t* hf = hist + (int64_t)f * K + (int64_t)i * sh.Sk + 1;
-  bool small = false;
-  for (int w = warp; w < sh.Wk; w += NW) {
-    const uint32_t rb = __ldg(rbits + (int64_t)row * sh.Wk + w);
-    bool surv = false;
-    if ((rb >> lane) & 1u) {
-      const bool sm = (min_size > 0) && (__ldg(hf + w * 32 + lane) < min_size);
-      small |= sm;
-      surv = !sm;
-    }
-    const uint32_t b = __ballot_sync(0xffffffffu, surv);
-    if (lane == 0) {
-      sbits[(int64_t)row * sh.Wk + w] = b;
-      s_wc[w] = __popc(b);
-    }
-  }
-  if (__any_sync(0xffffffffu, small) && lane == 0) atomicOr(fscal + f * 4, 1);
-  __syncthreads();
-  // row-local exclusive prefix over the words: each warp scans a contiguous
-  // block of words, then the block totals are offset
-  const int per = (sh.Wk + NW - 1) / NW;
-  const int w0 = warp * per, w1 = min(sh.Wk, w0 + per);
-  int carry = 0;
-  for (int c = w0; c < w1; c += 32) {
-    const int w = c + lane;
-    const int v = (w < w1) ? s_wc[w] : 0;
-    int x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += t;
-    }
-    if (w < w1) s_wc[w] = carry + x - v;  // exclusive within the warp's block
-    carry += __shfl_sync(0xffffffffu, x, 31);
-  }
-  if (lane == 0) s_part[warp] = carry;
-  __syncthreads();
-  int base = 0;
-  for (int q = 0; q < warp; ++q) base += s_part[q];
-  for (int w = w0 + lane; w < w1; w += 32) spre[(int64_t)row * sh.Wk + w] = base + s_wc[w];
-  if (threadIdx.x == 0) {
-    int tot = 0;
-    for (int q = 0; q < NW; ++q) tot += s_part[q];
-    rcnt[row] = tot;
-  }
-}
-
 // Dissolve small segments into the nearest surviving ring donor (reference
-// segment.py:141-154) and write the final compacted ids, one CTA per ring row.
+// segment.py:136-154) and write the final compacted ids, one CTA per ring row,
+// in one pass:
+//   A  the row's roots survive unless their post-backfill count is below
+//      min_size: survivor bits + row-local word prefix (global, read by later
+//      rows of the frame) and the row's survivor count, published in
+//      rstat[row] with a ready flag;
+//   B  row bases = the published counts of the frame's earlier rows (every
+//      label of a row has its root in that row or an earlier one: roots are
+//      component minima and donors lie in the same row);
+//   C  each labelled cell's root looked up in the survivor bits -- dissolved
+//      -> target, survivor -> final id -- and the targets filled from the
+//      nearest surviving donor.
+// Rows are claimed in ticket order, so every earlier row belongs to a CTA
+// that is already running and publishes without waiting: no deadlock.
+// rstat and the ticket (fscal[3]) are zeroed by k_root_flatten.
 template <int T>
 __global__ void __launch_bounds__(T, 2048 / T) k_prune_rows(Shape sh, const int32_t* __restrict__ lab_in,
                                                   int32_t* __restrict__ out, const int32_t* __restrict__ hist,
-                                                  int64_t K, int32_t min_size, const int32_t* __restrict__ fscal,
-                                                  const uint32_t* __restrict__ rbits, const int32_t* __restrict__ rpre,
-                                                  const uint32_t* __restrict__ sbits,
-                                                  const int32_t* __restrict__ spre, const int32_t* __restrict__ rcnt) {
+                                                  int64_t K, int32_t min_size, const uint32_t* __restrict__ rbits,
+                                                  uint32_t* __restrict__ sbits, int32_t* __restrict__ spre,
+                                                  int32_t* __restrict__ rstat, int32_t* __restrict__ ticket) {
+  constexpr int NW = T / 32;
+  constexpr int kReady = 1 << 30;
   extern __shared__ int s_dynrow[];
   const int S = sh.S, nw = (S + 31) / 32;
   int* s_val = s_dynrow;
   uint32_t* s_dm = reinterpret_cast<uint32_t*>(s_dynrow + nw * 32);
   int* s_base = reinterpret_cast<int*>(s_dm + nw);  // survivor rank of each ring row's first root
-  __shared__ int s_any;
-  const int row = blockIdx.x;
-  const int f = row / sh.R;
-  const bool any_small = fscal[f * 4] != 0;
-  // final ids = 1 + rank of the root among the frame's survivors (all roots
-  // when nothing is small): row base + row-local word prefix + bit rank
-  const uint32_t* bb = sbits + (int64_t)f * sh.R * sh.Wk;
-  const int32_t* bp = spre + (int64_t)f * sh.R * sh.Wk;
-  (void)rbits;
-  (void)rpre;
-  const int64_t rb = (int64_t)row * S;
-  if (threadIdx.x == 0) s_any = 0;
-  if (threadIdx.x < 32) {  // row bases: exclusive scan of the frame's row counts
-    const int lane = threadIdx.x;
+  int* s_wc = s_base + sh.R;                        // per-word survivor counts of this row
+  __shared__ int s_any, s_row, s_part[NW];
+  if (threadIdx.x == 0) {
+    s_row = atomicAdd(ticket, 1);
+    s_any = 0;
+  }
+  __syncthreads();
+  const int row = s_row;
+  const int f = row / sh.R, i = row - f * sh.R;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // A. survivors of this row's roots, one warp per 32-cell word (the
+  // histogram reads of a word are one coalesced load)
+  {
+    const int32_t* hf = hist + (int64_t)f * K + (int64_t)i * sh.Sk + 1;
+    for (int w = warp; w < sh.Wk; w += NW) {
+      const uint32_t rb = __ldg(rbits + (int64_t)row * sh.Wk + w);
+      bool surv = false;
+      if ((rb >> lane) & 1u) surv = !((min_size > 0) && (__ldcg(hf + w * 32 + lane) < min_size));
+      const uint32_t b = __ballot_sync(0xffffffffu, surv);
+      if (lane == 0) {
+        sbits[(int64_t)row * sh.Wk + w] = b;
+        s_wc[w] = __popc(b);
+      }
+    }
+    __syncthreads();
+    // row-local exclusive prefix over the words: each warp scans a
+    // contiguous block of words, then the block totals are offset
+    const int per = (sh.Wk + NW - 1) / NW;
+    const int w0 = warp * per, w1 = min(sh.Wk, w0 + per);
     int carry = 0;
-    for (int c = 0; c < sh.R; c += 32) {
-      const int v = (c + lane < sh.R) ? __ldg(rcnt + (int64_t)f * sh.R + c + lane) : 0;
+    for (int c = w0; c < w1; c += 32) {
+      const int w = c + lane;
+      const int v = (w < w1) ? s_wc[w] : 0;
       int x = v;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int t = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += t;
       }
-      if (c + lane < sh.R) s_base[c + lane] = carry + x - v;
+      if (w < w1) s_wc[w] = carry + x - v;
       carry += __shfl_sync(0xffffffffu, x, 31);
     }
+    if (lane == 0) s_part[warp] = carry;
+    __syncthreads();
+    int base = 0;
+    for (int q = 0; q < warp; ++q) base += s_part[q];
+    for (int w = w0 + lane; w < w1; w += 32) spre[(int64_t)row * sh.Wk + w] = base + s_wc[w];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int q = 0; q < NW; ++q) tot += s_part[q];
+      __threadfence();  // sbits / spre of this row before its ready flag
+      atomicExch(rstat + row, kReady | tot);
+    }
+  }
+  // B. row bases: exclusive scan of the frame's published row counts (rows
+  // before this one; later rows are never referenced)
+  if (warp == 0) {
+    const volatile int32_t* rs = rstat + (int64_t)f * sh.R;
+    int carry = 0;
+    for (int c = 0; c <= i; c += 32) {
+      int v = 0;
+      if (c + lane < i) {
+        while (((v = rs[c + lane]) & kReady) == 0) {
+        }
+        v &= kReady - 1;
+      }
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += t;
+      }
+      if (c + lane <= i) s_base[c + lane] = carry + x - v;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    __threadfence();  // acquire: the earlier rows' sbits / spre
   }
   __syncthreads();
-  // pass 1: each labelled cell's root is looked up in the survivor bits --
-  // dissolved (not a survivor) -> target (-2), survivor -> its final id
-  // right away, so the fill pass only copies ids
-  (void)hist;
-  (void)K;
-  (void)min_size;
-  (void)any_small;
+  // C. pass 1: each labelled cell's root is looked up in the survivor bits
+  // (L2 loads: written by other CTAs of this launch) -- dissolved -> target
+  // (-2), survivor -> its final id right away, so the fill only copies ids
+  const uint32_t* bb = sbits + (int64_t)f * sh.R * sh.Wk;
+  const int32_t* bp = spre + (int64_t)f * sh.R * sh.Wk;
+  const int64_t rb = (int64_t)row * S;
   bool any = false;
   constexpr int PF = LSEG_PF;
   for (int s0 = 0; s0 < nw * 32; s0 += T * PF) {
@@ -1921,8 +1925,8 @@ __global__ void __launch_bounds__(T, 2048 / T) k_prune_rows(Shape sh, const int3
         ro[j] = rr;
         cb[j] = cc & 31;
         const int64_t wi = (int64_t)rr * sh.Wk + (cc >> 5);
-        wv[j] = __ldg(bb + wi);
-        pv[j] = __ldg(bp + wi);
+        wv[j] = __ldcg(bb + wi);
+        pv[j] = __ldcg(bp + wi);
       }
     }
 #pragma unroll
@@ -1940,7 +1944,7 @@ __global__ void __launch_bounds__(T, 2048 / T) k_prune_rows(Shape sh, const int3
       any |= dm != 0;
     }
   }
-  if (any && (threadIdx.x & 31) == 0) s_any = 1;
+  if (any && lane == 0) s_any = 1;
   __syncthreads();
   const bool rany = s_any != 0;
   for (int s = threadIdx.x; s < S; s += T) out[rb + s] = fill_one(s_val, s_dm, nw, S, s, rany);
@@ -1950,24 +1954,17 @@ void launch_prune_fused(const Shape& sh, const Workspace& ws, int32_t min_size, 
   // 128-thread CTAs (16 per SM) for throughput; one-wave batches (single
   // scans) use 256 threads per row to cut the per-row latency
   const bool wide = (int64_t)sh.F * sh.R < 148 * 8;
-  if (wide)
-    k_survivor_rows<256><<<sh.F * sh.R, 256, sizeof(int) * (size_t)sh.Wk, st>>>(
-        sh, ws.rbits, ws.hist, ws.K, min_size, ws.sbits, ws.spre, ws.rcnt, ws.fscal);
-  else
-    k_survivor_rows<128><<<sh.F * sh.R, 128, sizeof(int) * (size_t)sh.Wk, st>>>(
-        sh, ws.rbits, ws.hist, ws.K, min_size, ws.sbits, ws.spre, ws.rcnt, ws.fscal);
-  prof_mark("prune_plan", st);
   const int nwr = (sh.S + 31) / 32;
-  const size_t smem = sizeof(int) * ((size_t)nwr * 33 + (size_t)sh.R);
+  const size_t smem = sizeof(int) * ((size_t)nwr * 33 + (size_t)sh.R + (size_t)sh.Wk);
   if (smem > 48 * 1024)
     for (auto fn : {k_prune_rows<128>, k_prune_rows<256>})
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (wide)
-    k_prune_rows<256><<<sh.F * sh.R, 256, smem, st>>>(sh, ws.lab_tmp, labels, ws.hist, ws.K, min_size, ws.fscal,
-                                                      ws.rbits, ws.rpre, ws.sbits, ws.spre, ws.rcnt);
+    k_prune_rows<256><<<sh.F * sh.R, 256, smem, st>>>(sh, ws.lab_tmp, labels, ws.hist, ws.K, min_size, ws.rbits,
+                                                      ws.sbits, ws.spre, ws.rcnt, ws.fscal + 3);
   else
-    k_prune_rows<128><<<sh.F * sh.R, 128, smem, st>>>(sh, ws.lab_tmp, labels, ws.hist, ws.K, min_size, ws.fscal,
-                                                      ws.rbits, ws.rpre, ws.sbits, ws.spre, ws.rcnt);
+    k_prune_rows<128><<<sh.F * sh.R, 128, smem, st>>>(sh, ws.lab_tmp, labels, ws.hist, ws.K, min_size, ws.rbits,
+                                                      ws.sbits, ws.spre, ws.rcnt, ws.fscal + 3);
   prof_mark("prune_apply", st);
 }
 
@@ -2039,13 +2036,10 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   prof_mark("merge", st);
   }
   {
-    const int64_t nwords = (int64_t)sh.F * sh.R * sh.Wk;
-    const int64_t blocks = (nwords * 32 + 255) / 256;
-    (void)blocks;
     const int ft = (int64_t)sh.F * sh.R < 148 * 8 ? 256 : 128;  // one-wave batches: wider CTAs
     const int thr = sh.Wk >= ft / 32 ? ft : 32 * sh.Wk;
     k_root_flatten<<<sh.F * sh.R, thr, 0, st>>>(sh, ws.parent, ws.lroots, ws.rbits, ws.hist, ws.K, ws.fscal,
-                                                n_labels);
+                                                ws.rcnt, n_labels);
     prof_mark("root_flatten", st);
     if (node_labels) {  // frame-level root ranks: only the segment() output needs them
       launch_scan_bits(sh, ws.rbits, ws.rpre, n_labels, nullptr, 0, st);
