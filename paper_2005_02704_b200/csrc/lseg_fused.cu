@@ -9,14 +9,15 @@
 //   k_tile / k_tile_cert  per 16 x 64 tile: halo staging, normals (exact fp64,
 //              or certified fp32 with exact fallback), mesh outputs, pass
 //              masks of the internal edges, border normals for k_merge
-//   k_tile_cc  per tile: components of the pass masks (run-level label
-//              propagation in shared memory) -> parent = tile-local root
+//   k_tile_cc  per tile: components of the pass masks (lock-free union-find
+//              over horizontal runs in shared memory) -> parent = tile-local root
 //   k_merge(_cert, _exact)  global union-find over tile-border edges only
 //   k_root_flatten  per ring row: tile-local roots -> final roots, root bits
 //   k_labels_backfill  per ring row: labels (root cell + 1), nearest-donor
 //              backfill, label histogram
-//   k_survivor_rows, k_prune_rows  per ring row: pruning plan and the
-//              compacted final ids (reference segment.py:127-160)
+//   k_prune_rows  per ring row: surviving roots (published per row), row
+//              bases from the earlier rows, compacted final ids (reference
+//              segment.py:127-160)
 #include <cub/block/block_scan.cuh>
 #include <cuda_fp16.h>
 #include <stdio.h>
@@ -87,11 +88,6 @@ __device__ __forceinline__ int64_t bn_col(const Shape& sh, int TR, int slot, int
   return ((int64_t)2 * ((sh.R + TR - 1) / TR) * sh.Sk + (int64_t)slot * sh.R + r) * 3;
 }
 __device__ __forceinline__ void bn_put(double* o, double a, double b, double c) { o[0] = a; o[1] = b; o[2] = c; }
-
-template <int TR, int TC, int T>
-__device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int c0, int TRe, int TCe,
-                                             const unsigned long long* s_m, int* s_par, int32_t* __restrict__ parent,
-                                             uint32_t* __restrict__ lroots);
 
 // One CTA per (frame, TR x TC tile of kept cells).
 //   A  ranges + node ids of the tile and a 1-cell halo into shared memory
