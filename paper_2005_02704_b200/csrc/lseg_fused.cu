@@ -42,6 +42,9 @@ static constexpr int kUnrollNormals = LSEG_UNR;
 #define LSEG_FAST_MATH 1
 #endif
 static constexpr bool kFastMath = LSEG_FAST_MATH;
+#ifndef LSEG_BIN_B
+#define LSEG_BIN_B 2  // points per thread in flight in k_bin_rows (4: register spills, -5 %)
+#endif
 #ifndef LSEG_BIN_MINB
 #define LSEG_BIN_MINB 8
 #endif
@@ -1155,7 +1158,7 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
     // lock-free union-find over the run-start labels (larger root hooked
     // under the smaller: root = component minimum; path halving on the way),
     // then full compression at run starts
-    auto root = [&](int x) -> int {
+    auto find = [&](int x) -> int {  // with path halving: unions only
       int p = s_par[x];
       while (p != x) {
         const int g = s_par[p];
@@ -1165,15 +1168,25 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
       }
       return x;
     };
+    // read-only find for the compression (a halving store there could
+    // overwrite a run start another thread has already compressed)
+    auto root = [&](int x) -> int {
+      int p = s_par[x];
+      while (p != x) {
+        x = p;
+        p = s_par[x];
+      }
+      return x;
+    };
     for (int k = lane; k < ne; k += 32) {
       const unsigned v = el[k];
-      int ra = root(v & 1023u), rb = root(v >> 10);
+      int ra = find(v & 1023u), rb = find(v >> 10);
       while (ra != rb) {
         if (ra < rb) { const int t = ra; ra = rb; rb = t; }
         const int old = atomicCAS(s_par + ra, ra, rb);
         if (old == ra) break;
-        ra = root(old);
-        rb = root(rb);
+        ra = find(old);
+        rb = find(rb);
       }
     }
     __syncthreads();
@@ -1593,7 +1606,7 @@ __global__ void __launch_bounds__(T, LSEG_BIN_MINB) k_bin_rows(lseg_sensor sn, S
   __syncthreads();
   int bad = 0;
   // batches of B points per thread: all loads of a batch are issued first
-  constexpr int B = 4;
+  constexpr int B = LSEG_BIN_B;
   for (int64_t base = lo; base < hi; base += (int64_t)T * B) {
     float px[B], py[B], pz[B];
     int pr[B];
