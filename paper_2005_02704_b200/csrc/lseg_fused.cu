@@ -1408,7 +1408,52 @@ __device__ __forceinline__ int nearest_donor(const uint32_t* s_dm, int nw, int S
   return dl < dr ? left : (dr < dl ? right : min(left, right));
 }
 
-// Shared body of the two ring-row kernels: s_val[s] holds a donor label (> 0),
+// Nearest donor of cell s when the donors are kept cells (cell = column * k):
+// the highest donor column <= cl0 and the lowest >= cr0, both cyclic over the
+// kept-column bits, then the reference rule (segment.py:91-106: cyclic step
+// distance, ties to the smaller step index).  cl0 = the last column whose
+// cell is < s (-1 wraps), cr0 = the first whose cell is > s.  The row must
+// hold at least one donor.  Returns the donor column.
+__device__ __forceinline__ int nearest_kept_donor(const uint32_t* s_kdm, int nwk, int k, int S, int s, int cl0,
+                                                  int cr0) {
+  int cl;
+  {
+    int ww;
+    uint32_t m;
+    if (cl0 < 0) {
+      ww = nwk - 1;
+      m = s_kdm[ww];
+    } else {
+      ww = cl0 >> 5;
+      const int b = cl0 & 31;
+      m = s_kdm[ww] & (b == 31 ? 0xffffffffu : ((2u << b) - 1u));
+    }
+    while (!m) {
+      ww = (ww == 0) ? nwk - 1 : ww - 1;
+      m = s_kdm[ww];
+    }
+    cl = ww * 32 + 31 - __clz(m);
+  }
+  int cr;
+  {
+    int ww = cr0 >> 5;
+    uint32_t m = (ww < nwk) ? (s_kdm[ww] & ~((1u << (cr0 & 31)) - 1u)) : 0u;
+    if (ww >= nwk) ww = nwk - 1;
+    while (!m) {
+      ww = (ww + 1 == nwk) ? 0 : ww + 1;
+      m = s_kdm[ww];
+    }
+    cr = ww * 32 + __ffs(m) - 1;
+  }
+  const int L = cl * k, Rc = cr * k;
+  int dl = s - L;
+  if (dl <= 0) dl += S;
+  int dr = Rc - s;
+  if (dr <= 0) dr += S;
+  return dl < dr ? cl : (dr < dl ? cr : (L < Rc ? cl : cr));
+}
+
+// Shared body of k_prune_rows' fill: s_val[s] holds a donor label (> 0),
 // 0 (passive: stays 0) or -2 (target: nearest donor's label, 0 if the row has
 // no donor); s_dm the donor bits.  Returns the filled label of cell s.
 __device__ __forceinline__ int fill_one(const int* s_val, const uint32_t* s_dm, int nw, int S, int s, bool any) {
@@ -1426,6 +1471,10 @@ __device__ __forceinline__ void hist_add(int32_t* hw, int lab) {
 // Node labels + backfill + histogram, one CTA per ring row.  Provisional
 // label ids are root cell + 1 (ascending root cell == ascending reference
 // label, so the compaction in k_prune_rows reproduces the reference ids).
+// Donors are kept cells only, so the row is classified per kept column
+// (label / valid-without-label target / invalid) and every cell then takes
+// its value: a non-kept valid cell between two donor columns picks the nearer
+// one directly, the rest search the donor-column bits.
 template <int T>
 __global__ void __launch_bounds__(T, 2048 / T) k_labels_backfill(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
                                                        const uint32_t* __restrict__ vbits,
@@ -1436,14 +1485,14 @@ __global__ void __launch_bounds__(T, 2048 / T) k_labels_backfill(lseg_sensor sn,
                                                        int32_t* __restrict__ node_labels, int32_t* __restrict__ out,
                                                        int32_t* __restrict__ hist, int64_t K) {
   extern __shared__ int s_dynrow[];
-  const int S = sh.S, nw = (S + 31) / 32;
-  int* s_val = s_dynrow;
-  uint32_t* s_dm = reinterpret_cast<uint32_t*>(s_dynrow + nw * 32);
+  const int S = sh.S, Sk = sh.Sk, k = sh.k, nwk = sh.Wk, nw = (S + 31) / 32;
+  int* s_kv = s_dynrow;                                                 // per kept column
+  uint32_t* s_kdm = reinterpret_cast<uint32_t*>(s_dynrow + nwk * 32);  // donor columns
   __shared__ int s_any;
   const int row = blockIdx.x;
   const int f = row / sh.R, i = row - f * sh.R;
   const uint32_t* vbr = vbits + (int64_t)row * sh.Wk;
-  const uint32_t* fbr = fbits ? fbits + (int64_t)row * ((S + 31) / 32) : nullptr;
+  const uint32_t* fbr = fbits ? fbits + (int64_t)row * nw : nullptr;
   const int32_t* parf = parent + (int64_t)f * sh.cap;
   const int32_t* par = parf + (int64_t)i * sh.Sk;
   const uint32_t* rbf = rbits + (int64_t)f * sh.R * sh.Wk;
@@ -1452,45 +1501,29 @@ __global__ void __launch_bounds__(T, 2048 / T) k_labels_backfill(lseg_sensor sn,
   if (threadIdx.x == 0) s_any = 0;
   __syncthreads();
   bool any = false;
-  // classify: donor label / target -2 / passive 0.  Chunks of PF cells per
-  // thread with all loads of a chunk issued before they are used (the two
-  // dependent parent loads would otherwise serialise per cell).
+  // classify the kept columns: donor label / target -2 / passive 0.  Chunks
+  // of PF columns per thread with all loads of a chunk issued before they
+  // are used (the two dependent parent loads would otherwise serialise).
   constexpr int PF = LSEG_PF;
-  for (int s0 = 0; s0 < nw * 32; s0 += T * PF) {
+  for (int c0 = 0; c0 < nwk * 32; c0 += T * PF) {
     int pv[PF], lv[PF];
 #pragma unroll
     for (int j = 0; j < PF; ++j) {
-      const int s = s0 + threadIdx.x + j * T;
-      pv[j] = -1;
-      if (s < S) {
-        const int c = (sh.k == 1) ? s : fdiv(s, sh.k, sh.inv_k);
-        if (sh.k == 1 || c * sh.k == s) pv[j] = __ldcg(par + c);  // tile-local root
-        else pv[j] = -2;
-      }
+      const int c = c0 + threadIdx.x + j * T;
+      pv[j] = (c < Sk) ? __ldcg(par + c) : -1;  // tile-local root
     }
 #pragma unroll
     for (int j = 0; j < PF; ++j) lv[j] = pv[j] >= 0 ? __ldcg(parf + pv[j]) : 0;  // its parent: the final root
 #pragma unroll
     for (int j = 0; j < PF; ++j) {
-      const int s = s0 + threadIdx.x + j * T;
-      if (s >= nw * 32) break;
+      const int c = c0 + threadIdx.x + j * T;
+      if (c >= nwk * 32) break;
       int v = 0;
-      if (s < S) {
-        if (pv[j] >= 0) {
-          v = lv[j] + 1;
-        } else if (pv[j] == -1) {  // kept cell without a normal: valid?
-          const int c = (sh.k == 1) ? s : fdiv(s, sh.k, sh.inv_k);
-          v = ((__ldg(vbr + (c >> 5)) >> (c & 31)) & 1u) ? -2 : 0;
-        } else {  // not a kept cell: valid full-resolution cell? (bits from k_bin_rows)
-          v = fbr ? (((__ldg(fbr + (s >> 5)) >> (s & 31)) & 1u) ? -2 : 0)
-                  : (in_window(__ldg(ranges + rb + s), sn.r_min, sn.r_max) ? -2 : 0);
-        }
-        if (node_labels)  // reference segment() output: 1 + rank of the root
-          node_labels[rb + s] = v > 0 ? rank_label(rbf, rpf, sh.Wk, sh.Sk, v - 1, sh.inv_Sk) : 0;
-      }
-      s_val[s] = v;
+      if (pv[j] >= 0) v = lv[j] + 1;
+      else if (c < Sk) v = ((__ldg(vbr + (c >> 5)) >> (c & 31)) & 1u) ? -2 : 0;  // valid, no normal
+      s_kv[c] = v;
       const uint32_t dm = __ballot_sync(0xffffffffu, v > 0);
-      if ((s & 31) == 0) s_dm[s >> 5] = dm;
+      if ((c & 31) == 0) s_kdm[c >> 5] = dm;
       any |= dm != 0;
     }
   }
@@ -1498,9 +1531,35 @@ __global__ void __launch_bounds__(T, 2048 / T) k_labels_backfill(lseg_sensor sn,
   __syncthreads();
   const bool rany = s_any != 0;
   int32_t* hw = hist + (int64_t)f * K;
-  for (int s = threadIdx.x; s < nw * 32; s += T) {
-    const int r = (s < S) ? fill_one(s_val, s_dm, nw, S, s, rany) : 0;
-    if (s < S) out[rb + s] = r;
+  for (int s = threadIdx.x; s < nw * 32; s += T) {  // whole warps (hist_add)
+    int r = 0;
+    if (s < S) {
+      const int c = (k == 1) ? s : fdiv(s, k, sh.inv_k);
+      const int j = s - c * k;
+      int v;
+      if (j == 0) v = s_kv[c];
+      else  // not a kept cell: valid full-resolution cell? (bits from k_bin_rows)
+        v = fbr ? (((__ldg(fbr + (s >> 5)) >> (s & 31)) & 1u) ? -2 : 0)
+                : (in_window(__ldg(ranges + rb + s), sn.r_min, sn.r_max) ? -2 : 0);
+      if (v > 0) {
+        r = v;
+      } else if (v == -2 && rany) {
+        bool done = false;
+        if (j > 0) {  // between donor columns c and c + 1 (cyclic): nearer one, ties to the smaller cell
+          const bool wrap = (c + 1 == Sk);
+          const int vl = s_kv[c], vr = s_kv[wrap ? 0 : c + 1];
+          if (vl > 0 && vr > 0) {
+            const int dr = wrap ? S - s : k - j;
+            r = (j < dr) ? vl : (dr < j ? vr : (wrap ? vr : vl));
+            done = true;
+          }
+        }
+        if (!done) r = s_kv[nearest_kept_donor(s_kdm, nwk, k, S, s, j > 0 ? c : c - 1, c + 1)];
+      }
+      if (node_labels)  // reference segment() output: 1 + rank of the root
+        node_labels[rb + s] = (j == 0 && v > 0) ? rank_label(rbf, rpf, sh.Wk, sh.Sk, v - 1, sh.inv_Sk) : 0;
+      out[rb + s] = r;
+    }
     hist_add(hw, r);
   }
 }
@@ -2056,8 +2115,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
     }
   }
   // labels + backfill -> lab_tmp (+ histogram)
-  const int nwr = (sh.S + 31) / 32;
-  const size_t smem = sizeof(int) * (size_t)nwr * 33;
+  const size_t smem = sizeof(int) * (size_t)sh.Wk * 33;
   const uint32_t* fb = (sh.k > 1 && fbits_valid) ? ws.fbits : nullptr;
   if (smem > 48 * 1024)
     for (auto fn : {k_labels_backfill<128>, k_labels_backfill<256>})

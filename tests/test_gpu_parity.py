@@ -368,6 +368,8 @@ def _grid_points(rng, R, S, top, bottom, base=5.0, noise=0.3, keep=0.9, planar=T
     (6, 64, 1, 10 ** 6, 0.9),  # everything small: all labels dissolve to 0
     (7, 130, 2, 1, 0.0),       # no valid point at all
     (16, 1800, 3, 5, 0.5),     # sparse, fragmented
+    (3, 40, 6, 2, 0.9),        # backfill tie across the wrap gap (cell 38: 2 steps to 36 and to 0)
+    (4, 50, 4, 2, 0.95),       # interior ties (j = k / 2 -> left donor) and a wrap tie (cell 49)
 ])
 def test_edge_shapes_vs_oracle(L, oracle, R, S, k, mseg, keep):
     """Edge cases of the batched path (the reference's own tests cover them
