@@ -90,8 +90,6 @@ Workspace carve(const Shape& s, int64_t label_bound, void* base) {
   w.rbits = reinterpret_cast<uint32_t*>(take(words * 4));
   w.lroots = reinterpret_cast<uint32_t*>(take(words * 4));
   w.rpre = reinterpret_cast<int32_t*>(take(words * 4));
-  w.sbits = reinterpret_cast<uint32_t*>(take(words * 4));
-  w.spre = reinterpret_cast<int32_t*>(take(words * 4));
   w.rcnt = reinterpret_cast<int32_t*>(take((size_t)s.F * s.R * 4));
   w.ucnt = reinterpret_cast<unsigned long long*>(take(2 * 8));
   w.bytes = off;

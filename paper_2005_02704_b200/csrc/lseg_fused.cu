@@ -1860,33 +1860,34 @@ void launch_bin_fused(const lseg_sensor& sn, const Shape& sh, const float* xyz, 
 // segment.py:136-154) and write the final compacted ids, one CTA per ring row,
 // in one pass:
 //   A  the row's roots survive unless their post-backfill count is below
-//      min_size: survivor bits + row-local word prefix (global, read by later
-//      rows of the frame) and the row's survivor count, published in
-//      rstat[row] with a ready flag;
-//   B  row bases = the published counts of the frame's earlier rows (every
-//      label of a row has its root in that row or an earlier one: roots are
-//      component minima and donors lie in the same row);
-//   C  each labelled cell's root looked up in the survivor bits -- dissolved
-//      -> target, survivor -> final id -- and the targets filled from the
-//      nearest surviving donor.
+//      min_size: survivor bits and row-local word prefix (shared memory);
+//      the row's survivor count is published in rstat[row] (ready flag);
+//   B  row base = the published counts of the frame's earlier rows;
+//   C  final id of each of the row's roots (1 + rank among the frame's
+//      survivors, -2 = dissolved) into remap[root cell], then a second flag;
+//   D  once the earlier rows' ids are published (every label of a row has
+//      its root in that row or an earlier one: roots are component minima and
+//      donors lie in the same row), each labelled cell reads its root's id
+//      and the dissolved cells are filled from the nearest surviving donor.
 // Rows are claimed in ticket order, so every earlier row belongs to a CTA
-// that is already running and publishes without waiting: no deadlock.
-// rstat and the ticket (fscal[3]) are zeroed by k_root_flatten.
+// that is already running; a row waits only for earlier rows' counts before
+// publishing its ids, so no wait chain forms and nothing deadlocks.
+// rstat and the ticket are zeroed by k_root_flatten.
 template <int T>
 __global__ void __launch_bounds__(T, 2048 / T) k_prune_rows(Shape sh, const int32_t* __restrict__ lab_in,
                                                   int32_t* __restrict__ out, const int32_t* __restrict__ hist,
                                                   int64_t K, int32_t min_size, const uint32_t* __restrict__ rbits,
-                                                  uint32_t* __restrict__ sbits, int32_t* __restrict__ spre,
-                                                  int32_t* __restrict__ rstat, int32_t* __restrict__ ticket) {
+                                                  int32_t* __restrict__ remap, int32_t* __restrict__ rstat,
+                                                  int32_t* __restrict__ ticket) {
   constexpr int NW = T / 32;
-  constexpr int kReady = 1 << 30;
+  constexpr int kReady = 1 << 30, kIds = 1 << 29;
   extern __shared__ int s_dynrow[];
   const int S = sh.S, nw = (S + 31) / 32;
   int* s_val = s_dynrow;
   uint32_t* s_dm = reinterpret_cast<uint32_t*>(s_dynrow + nw * 32);
-  int* s_base = reinterpret_cast<int*>(s_dm + nw);  // survivor rank of each ring row's first root
-  int* s_wc = s_base + sh.R;                        // per-word survivor counts of this row
-  __shared__ int s_any, s_row, s_part[NW];
+  int* s_wc = reinterpret_cast<int*>(s_dm + nw);  // per-word survivor counts -> row-local prefix
+  uint32_t* s_sb = reinterpret_cast<uint32_t*>(s_wc + sh.Wk);  // survivor bits of the row
+  __shared__ int s_any, s_row, s_base, s_part[NW];
   if (threadIdx.x == 0) {
     s_row = atomicAdd(ticket, 1);
     s_any = 0;
@@ -1895,6 +1896,8 @@ __global__ void __launch_bounds__(T, 2048 / T) k_prune_rows(Shape sh, const int3
   const int row = s_row;
   const int f = row / sh.R, i = row - f * sh.R;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const volatile int32_t* rs = rstat + (int64_t)f * sh.R;
+  int32_t* rmf = remap + (int64_t)f * K;
   // A. survivors of this row's roots, one warp per 32-cell word (the
   // histogram reads of a word are one coalesced load)
   {
@@ -1905,7 +1908,7 @@ __global__ void __launch_bounds__(T, 2048 / T) k_prune_rows(Shape sh, const int3
       if ((rb >> lane) & 1u) surv = !((min_size > 0) && (__ldcg(hf + w * 32 + lane) < min_size));
       const uint32_t b = __ballot_sync(0xffffffffu, surv);
       if (lane == 0) {
-        sbits[(int64_t)row * sh.Wk + w] = b;
+        s_sb[w] = b;
         s_wc[w] = __popc(b);
       }
     }
@@ -1931,83 +1934,71 @@ __global__ void __launch_bounds__(T, 2048 / T) k_prune_rows(Shape sh, const int3
     __syncthreads();
     int base = 0;
     for (int q = 0; q < warp; ++q) base += s_part[q];
-    for (int w = w0 + lane; w < w1; w += 32) spre[(int64_t)row * sh.Wk + w] = base + s_wc[w];
-    __syncthreads();
+    for (int w = w0 + lane; w < w1; w += 32) s_wc[w] += base;
     if (threadIdx.x == 0) {
       int tot = 0;
       for (int q = 0; q < NW; ++q) tot += s_part[q];
-      __threadfence();  // sbits / spre of this row before its ready flag
-      atomicExch(rstat + row, kReady | tot);
+      atomicExch(rstat + row, kReady | tot);  // only the count: no data behind it
     }
   }
-  // B. row bases: exclusive scan of the frame's published row counts (rows
-  // before this one; later rows are never referenced)
+  // B. row base: the published counts of the frame's earlier rows
   if (warp == 0) {
-    const volatile int32_t* rs = rstat + (int64_t)f * sh.R;
-    int carry = 0;
-    for (int c = 0; c <= i; c += 32) {
-      int v = 0;
-      if (c + lane < i) {
-        while (((v = rs[c + lane]) & kReady) == 0) {
-        }
-        v &= kReady - 1;
+    int sum = 0;
+    for (int r = lane; r < i; r += 32) {
+      int v;
+      while (((v = rs[r]) & kReady) == 0) {
       }
-      int x = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += t;
-      }
-      if (c + lane <= i) s_base[c + lane] = carry + x - v;
-      carry += __shfl_sync(0xffffffffu, x, 31);
+      sum += v & (kIds - 1);
     }
-    __threadfence();  // acquire: the earlier rows' sbits / spre
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) s_base = sum;
   }
   __syncthreads();
-  // C. pass 1: each labelled cell's root is looked up in the survivor bits
-  // (L2 loads: written by other CTAs of this launch) -- dissolved -> target
-  // (-2), survivor -> its final id right away, so the fill only copies ids
-  const uint32_t* bb = sbits + (int64_t)f * sh.R * sh.Wk;
-  const int32_t* bp = spre + (int64_t)f * sh.R * sh.Wk;
+  // C. final ids of this row's roots, then the second flag
+  {
+    const int base = s_base;
+    for (int w = warp; w < sh.Wk; w += NW) {
+      const uint32_t rb = __ldg(rbits + (int64_t)row * sh.Wk + w);
+      if ((rb >> lane) & 1u) {
+        const uint32_t sb = s_sb[w], bit = 1u << lane;
+        rmf[i * sh.Sk + w * 32 + lane] = (sb & bit) ? 1 + base + s_wc[w] + __popc(sb & (bit - 1u)) : -2;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();  // this row's ids before its flag
+      atomicOr(rstat + row, kIds);
+    }
+  }
+  // D. wait for the earlier rows' ids, then pass 1: each labelled cell's
+  // root id (L2 loads: written by other CTAs of this launch) -- dissolved
+  // -> target (-2), survivor -> its final id, so the fill only copies ids
+  if (warp == 0) {
+    for (int r = lane; r < i; r += 32)
+      while ((rs[r] & kIds) == 0) {
+      }
+    __threadfence();  // acquire: the earlier rows' ids
+  }
+  __syncthreads();
   const int64_t rb = (int64_t)row * S;
   bool any = false;
   constexpr int PF = LSEG_PF;
   for (int s0 = 0; s0 < nw * 32; s0 += T * PF) {
-    int lv[PF], ro[PF], cb[PF];
-    uint32_t wv[PF];
-    int pv[PF];
+    int lv[PF];
 #pragma unroll
     for (int j = 0; j < PF; ++j) {
       const int s = s0 + threadIdx.x + j * T;
       lv[j] = (s < S) ? __ldcg(lab_in + rb + s) : 0;
     }
 #pragma unroll
-    for (int j = 0; j < PF; ++j) {
-      ro[j] = 0;
-      cb[j] = 0;
-      wv[j] = 0u;
-      pv[j] = 0;
-      if (lv[j] > 0) {
-        const int rc = lv[j] - 1;
-        const int rr = fdiv(rc, sh.Sk, sh.inv_Sk), cc = rc - rr * sh.Sk;
-        ro[j] = rr;
-        cb[j] = cc & 31;
-        const int64_t wi = (int64_t)rr * sh.Wk + (cc >> 5);
-        wv[j] = __ldcg(bb + wi);
-        pv[j] = __ldcg(bp + wi);
-      }
-    }
+    for (int j = 0; j < PF; ++j) lv[j] = lv[j] > 0 ? __ldcg(rmf + lv[j] - 1) : 0;
 #pragma unroll
     for (int j = 0; j < PF; ++j) {
       const int s = s0 + threadIdx.x + j * T;
       if (s >= nw * 32) break;
-      int v = 0;
-      if (lv[j] > 0) {
-        const uint32_t bit = 1u << cb[j];
-        v = (wv[j] & bit) ? 1 + s_base[ro[j]] + pv[j] + __popc(wv[j] & (bit - 1u)) : -2;
-      }
-      s_val[s] = v;
-      const uint32_t dm = __ballot_sync(0xffffffffu, v > 0);
+      s_val[s] = lv[j];
+      const uint32_t dm = __ballot_sync(0xffffffffu, lv[j] > 0);
       if ((s & 31) == 0) s_dm[s >> 5] = dm;
       any |= dm != 0;
     }
@@ -2023,16 +2014,16 @@ void launch_prune_fused(const Shape& sh, const Workspace& ws, int32_t min_size, 
   // scans) use 256 threads per row to cut the per-row latency
   const bool wide = (int64_t)sh.F * sh.R < 148 * 8;
   const int nwr = (sh.S + 31) / 32;
-  const size_t smem = sizeof(int) * ((size_t)nwr * 33 + (size_t)sh.R + (size_t)sh.Wk);
+  const size_t smem = sizeof(int) * ((size_t)nwr * 33 + 2 * (size_t)sh.Wk);
   if (smem > 48 * 1024)
     for (auto fn : {k_prune_rows<128>, k_prune_rows<256>})
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (wide)
     k_prune_rows<256><<<sh.F * sh.R, 256, smem, st>>>(sh, ws.lab_tmp, labels, ws.hist, ws.K, min_size, ws.rbits,
-                                                      ws.sbits, ws.spre, ws.rcnt, ws.fscal + 3);
+                                                      ws.remap, ws.rcnt, ws.fscal + 3);
   else
     k_prune_rows<128><<<sh.F * sh.R, 128, smem, st>>>(sh, ws.lab_tmp, labels, ws.hist, ws.K, min_size, ws.rbits,
-                                                      ws.sbits, ws.spre, ws.rcnt, ws.fscal + 3);
+                                                      ws.remap, ws.rcnt, ws.fscal + 3);
   prof_mark("prune_apply", st);
 }
 
