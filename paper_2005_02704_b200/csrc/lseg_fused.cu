@@ -1531,10 +1531,12 @@ __global__ void __launch_bounds__(T, 2048 / T) k_labels_backfill(lseg_sensor sn,
   __syncthreads();
   const bool rany = s_any != 0;
   int32_t* hw = hist + (int64_t)f * K;
+  // s / k as a multiply-high: exact for s < 2^32 / k (S <= 16384 here)
+  const unsigned kmag = 0xffffffffu / (unsigned)k + 1u;
   for (int s = threadIdx.x; s < nw * 32; s += T) {  // whole warps (hist_add)
     int r = 0;
     if (s < S) {
-      const int c = (k == 1) ? s : fdiv(s, k, sh.inv_k);
+      const int c = (k == 1) ? s : (int)__umulhi((unsigned)s, kmag);
       const int j = s - c * k;
       int v;
       if (j == 0) v = s_kv[c];
@@ -1715,21 +1717,21 @@ __global__ void __launch_bounds__(T, LSEG_BIN_MINB) k_bin_rows(lseg_sensor sn, S
     }
     return;
   }
-  for (int s = threadIdx.x; s < S; s += T) out[s] = __longlong_as_double((long long)s_cell[s]);
+  {  // row out + full-resolution valid bits (the backfill's target test) in one pass
+    const int Wf = (S + 31) / 32;
+    for (int w = threadIdx.x >> 5; w < Wf; w += T / 32) {
+      const int c = w * 32 + lane;
+      const unsigned long long v = c < S ? s_cell[c] : ~0ull;
+      if (c < S) out[c] = __longlong_as_double((long long)v);
+      const uint32_t b = __ballot_sync(0xffffffffu, v != ~0ull);
+      if (fbits && lane == 0) fbits[row * Wf + w] = b;
+    }
+  }
   for (int w = threadIdx.x >> 5; w < sh.Wk; w += T / 32) {
     const int c = w * 32 + lane;
     const bool v = (c < sh.Sk) && s_cell[c * sh.k] != ~0ull;
     const uint32_t b = __ballot_sync(0xffffffffu, v);
     if (lane == 0) vbits[row * sh.Wk + w] = b;
-  }
-  if (fbits && sh.k > 1) {  // full-resolution valid bits (the backfill's target test)
-    const int Wf = (S + 31) / 32;
-    for (int w = threadIdx.x >> 5; w < Wf; w += T / 32) {
-      const int c = w * 32 + lane;
-      const bool v = (c < S) && s_cell[c] != ~0ull;
-      const uint32_t b = __ballot_sync(0xffffffffu, v);
-      if (lane == 0) fbits[row * Wf + w] = b;
-    }
   }
 }
 
