@@ -1253,7 +1253,11 @@ __global__ void __launch_bounds__(T, 2048 / T) k_tile_cc(Shape sh, const unsigne
 
 // Global union over the forward edges that leave a tile.  Threads enumerate
 // the cells of each tile's last row and last column (corner duplicates are
-// harmless); both endpoints' fp64 normals come from `bnorm`.
+// harmless); both endpoints' fp64 normals come from `bnorm`.  Along a tile
+// border most passing edges join the same two tile-local components, so a
+// warp first collapses edges with equal (parent of p, parent of q) -- the
+// same union -- and only one lane per distinct pair runs it: far fewer CAS
+// on the few large roots.
 template <int TR, int TC>
 __global__ void k_merge(Shape sh, const double* __restrict__ bnorm, double t0, double t1, double t2,
                         int32_t* __restrict__ parent) {
@@ -1264,47 +1268,56 @@ __global__ void k_merge(Shape sh, const double* __restrict__ bnorm, double t0, d
   const int per = nbr * sh.Sk + nbc * sh.R;
   int32_t* par = parent + (int64_t)f * sh.cap;
   const double* bn = bnorm + (int64_t)f * bn_frame(sh, TR, TC);
-  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < per; u += gridDim.x * blockDim.x) {
-    int r, c;
-    if (u < nbr * sh.Sk) {
-      const int br = u / sh.Sk;
-      r = min(br * TR + TR - 1, sh.R - 1);
-      c = u - br * sh.Sk;
-    } else {
-      const int v = u - nbr * sh.Sk;
-      const int bc = v / sh.R;
-      c = min(bc * TC + TC - 1, sh.Sk - 1);
-      r = v - bc * sh.R;
+  const int lane = threadIdx.x & 31;
+  // warp-uniform trip count (the dedup below needs whole warps)
+  for (int u0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); u0 < per; u0 += gridDim.x * blockDim.x) {
+    const int u = u0 + lane;
+    int r = 0, c = 0, pp = -1;
+    if (u < per) {
+      if (u < nbr * sh.Sk) {
+        const int br = u / sh.Sk;
+        r = min(br * TR + TR - 1, sh.R - 1);
+        c = u - br * sh.Sk;
+      } else {
+        const int v = u - nbr * sh.Sk;
+        const int bc = v / sh.R;
+        c = min(bc * TC + TC - 1, sh.Sk - 1);
+        r = v - bc * sh.R;
+      }
+      pp = __ldcg(par + r * sh.Sk + c);  // -1: no normal
     }
     const int p = r * sh.Sk + c;
-    const int pp = __ldcg(par + p);
-    if (pp < 0) continue;  // no normal
     const int tr = r / TR, tc = c / TC;
     const bool last_row = (r == min(tr * TR + TR - 1, sh.R - 1));
-    const bool last_col = (c == min(tc * TC + TC - 1, sh.Sk - 1));
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
-      if (r + slot_dr(s) >= sh.R) continue;
-      if (edge_internal<TR, TC>(r, c, s, sh.Sk)) continue;
-      const int rq = r + slot_dr(s), cq = wrapc(c + slot_dc(s), sh.Sk);
-      const int q = rq * sh.Sk + cq;
-      const int pq = __ldcg(par + q);
-      if (pq < 0) continue;
-      // an edge that crosses a tile-row boundary reads both normals from the
-      // row border store, one that only crosses a column boundary from the
-      // column border store
-      const double *pa, *pb;
-      if (slot_dr(s) == 1 && last_row) {
-        pa = bn + bn_row(sh, 2 * tr + 1, c);
-        pb = bn + bn_row(sh, 2 * (rq / TR), cq);
-      } else {
-        pa = bn + bn_col(sh, TR, 2 * tc + 1, r);
-        pb = bn + bn_col(sh, TR, 2 * (cq / TC), rq);
+      bool want = false;
+      int q = 0, pq = -1;
+      if (pp >= 0 && r + slot_dr(s) < sh.R && !edge_internal<TR, TC>(r, c, s, sh.Sk)) {
+        const int rq = r + slot_dr(s), cq = wrapc(c + slot_dc(s), sh.Sk);
+        q = rq * sh.Sk + cq;
+        pq = __ldcg(par + q);
+        if (pq >= 0) {
+          // an edge that crosses a tile-row boundary reads both normals from
+          // the row border store, one that only crosses a column boundary
+          // from the column border store
+          const double *pa, *pb;
+          if (slot_dr(s) == 1 && last_row) {
+            pa = bn + bn_row(sh, 2 * tr + 1, c);
+            pb = bn + bn_row(sh, 2 * (rq / TR), cq);
+          } else {
+            pa = bn + bn_col(sh, TR, 2 * tc + 1, r);
+            pb = bn + bn_col(sh, TR, 2 * (cq / TC), rq);
+          }
+          const double a[3] = {__ldcg(pa), __ldcg(pa + 1), __ldcg(pa + 2)};
+          const double b[3] = {__ldcg(pb), __ldcg(pb + 1), __ldcg(pb + 2)};
+          want = normals_pass(a, b, t0, t1, t2);
+        }
       }
-      (void)last_col;
-      const double a[3] = {__ldcg(pa), __ldcg(pa + 1), __ldcg(pa + 2)};
-      const double b[3] = {__ldcg(pb), __ldcg(pb + 1), __ldcg(pb + 2)};
-      if (normals_pass(a, b, t0, t1, t2)) uf_union_pre(par, p, pp, q, pq);  // a stale parent is still an ancestor
+      const unsigned long long key =
+          want ? ((unsigned long long)(unsigned)pp << 32 | (unsigned)pq) : ~0ull;
+      const unsigned m = __match_any_sync(0xffffffffu, key);
+      if (want && lane == __ffs(m) - 1) uf_union_pre(par, p, pp, q, pq);  // stale parents are ancestors
     }
   }
 }
