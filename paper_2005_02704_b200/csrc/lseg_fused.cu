@@ -1107,49 +1107,48 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
   // and compress the run starts -- two barriers, no rounds.
   static_assert(NT <= 1024, "10-bit cell indices");
   constexpr int NJ = (NT + T - 1) / T;
-  unsigned pk[NJ];
+  static_assert(NT % T == 0 && TC % 32 == 0, "each warp step covers a 32-cell chunk of one row");
+  // each warp's edges as a dense list (a | b << 10) in its own shared-memory
+  // segment (appended without atomics), then unioned by the same warp:
+  // no block barrier between gathering and union.  At step j the warp's
+  // lanes are one 32-cell chunk of a row, so the chunk's edge bits are read
+  // straight from the row masks and chunks without edges are skipped.
+  constexpr int SEG = 2 * NT / (T / 32);  // >= 2 edges per cell of the warp (+ the wraps, see below)
+  __shared__ unsigned s_el[2 * NT];
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned* el = s_el + (threadIdx.x >> 5) * SEG;
+  int ne = 0;
   unsigned starts = 0;  // which of this thread's cells are run starts
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
-    const int e = threadIdx.x + j * T;
-    const int y = e / TC, x = e - y * TC;
-    pk[j] = 0;
-    if (e < NT) {
-      const int a = s_par[e];
-      if (a == e) starts |= 1u << j;
-      const bool u0 = (s_U[2 * y] >> x) & 1ull, u1 = (s_U[2 * y + 1] >> x) & 1ull;
-      const unsigned b0 = u0 ? (unsigned)s_par[e + TC] : 0u, b1 = u1 ? (unsigned)s_par[e + TC + 1] : 0u;
-      pk[j] = (unsigned)a | b0 << 10 | b1 << 20 | (u0 ? 1u << 30 : 0u) | (u1 ? 2u << 30 : 0u);
+    const int e0 = (threadIdx.x & ~31) + j * T;
+    const int y = e0 / TC, x0 = e0 - y * TC;
+    const int e = e0 + lane;
+    if (((~(s_m[y * 5] << 1) >> x0) >> lane) & 1ull) starts |= 1u << j;  // x = 0 or no run edge from x - 1
+    const unsigned c0 = (unsigned)(s_U[2 * y] >> x0), c1 = (unsigned)(s_U[2 * y + 1] >> x0);
+    if (c0 | c1) {  // warp-uniform
+      const unsigned a = (unsigned)s_par[e];
+      if ((c0 >> lane) & 1u) el[ne + __popc(c0 & lt)] = a | (unsigned)s_par[e + TC] << 10;
+      ne += __popc(c0);
+      if ((c1 >> lane) & 1u) el[ne + __popc(c1 & lt)] = a | (unsigned)s_par[e + TC + 1] << 10;
+      ne += __popc(c1);
     }
   }
-  unsigned pw = 0;
-  const int wy = (int)threadIdx.x - (T - 32);  // the last warp (fewest edges: it holds row TR-1) adds the wraps
-  if (wy >= 0 && wy < TRe) {  // full-width column wrap (x = S'-1 -> 0)
-    const int y = wy;
-    const unsigned W = (unsigned)s_m[y * 5 + 4];
-    const unsigned a = (unsigned)s_par[y * TC + TCe - 1];
+  // full-width column wrap (x = S'-1 -> 0), added by the last warp (fewest
+  // edges: it holds row TR-1)
+  if (threadIdx.x >= T - 32) {
+    const int y = lane;
+    const unsigned W = (y < TRe) ? (unsigned)s_m[y * 5 + 4] : 0u;
     const bool w0 = W & 1u, w1 = (W & 2u) && (y + 1 < TRe);
-    // (y + 1) * TC is 1024 on the last row: only packed when that edge exists
-    pw = a | (unsigned)(y * TC) << 10 | (w1 ? (unsigned)((y + 1) * TC) << 20 : 0u) | (w0 ? 1u << 30 : 0u) |
-         (w1 ? 2u << 30 : 0u);
-  }
-  // each warp's edges as a dense list (a | b << 10) in its own shared-memory
-  // segment (appended without atomics), then unioned by the same warp:
-  // no block barrier between gathering and union
-  constexpr int SEG = 2 * NT / (T / 32);  // >= 2 edges per cell of the warp (+ the wraps, see above)
-  __shared__ unsigned s_el[2 * NT];
-  const int lane = threadIdx.x & 31;
-  unsigned* el = s_el + (threadIdx.x >> 5) * SEG;
-  int ne = 0;
-#pragma unroll
-  for (int j = 0; j <= NJ; ++j) {
-    const unsigned v = j < NJ ? pk[j] : pw;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const bool has = v & ((1u << 30) << h);
-      const unsigned bal = __ballot_sync(0xffffffffu, has);
-      if (has) el[ne + __popc(bal & ((1u << lane) - 1u))] = (v & 1023u) | (((v >> (10 + 10 * h)) & 1023u) << 10);
-      ne += __popc(bal);
+    const unsigned b0 = __ballot_sync(0xffffffffu, w0), b1 = __ballot_sync(0xffffffffu, w1);
+    if (b0 | b1) {
+      const unsigned a = (y < TRe) ? (unsigned)s_par[y * TC + TCe - 1] : 0u;
+      if (w0) el[ne + __popc(b0 & lt)] = a | (unsigned)(y * TC) << 10;
+      ne += __popc(b0);
+      // (y + 1) * TC is 1024 on the last row: only when that edge exists
+      if (w1) el[ne + __popc(b1 & lt)] = a | (unsigned)((y + 1) * TC) << 10;
+      ne += __popc(b1);
     }
   }
   __syncwarp();
