@@ -12,9 +12,11 @@
 //   k_tile_cc  per tile: components of the pass masks (lock-free union-find
 //              over horizontal runs in shared memory) -> parent = tile-local root
 //   k_merge(_cert, _exact)  global union-find over tile-border edges only
-//   k_root_flatten  per ring row: tile-local roots -> final roots, root bits
-//   k_labels_backfill  per ring row: labels (root cell + 1), nearest-donor
-//              backfill, label histogram
+//   k_labels_backfill  per ring row: tile-local roots chased to the final
+//              roots (root bits, label count), labels (root cell + 1),
+//              nearest-donor backfill, label histogram (slots zeroed by
+//              k_tile_cc).  With the segment() output requested, k_root_flatten
+//              + the root-rank scan run first instead.
 //   k_prune_rows  per ring row: surviving roots (published per row), row
 //              bases from the earlier rows, compacted final ids (reference
 //              segment.py:127-160)
@@ -50,6 +52,9 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #endif
 #ifndef LSEG_CC_TBIG
 #define LSEG_CC_TBIG 128
+#endif
+#ifndef LSEG_FOLD_FLATTEN
+#define LSEG_FOLD_FLATTEN 1
 #endif
 #ifndef LSEG_PF
 #define LSEG_PF 4
@@ -164,7 +169,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   const int32_t* wpf = wpre + (int64_t)f * sh.R * sh.Wk;
   const int64_t nbase = (int64_t)f * sh.cap;
   const int tid = threadIdx.x;
-  if (rem == 0 && tid == 0) n_labels[f] = 0;  // counted by k_root_flatten
+  if (rem == 0 && tid == 0) n_labels[f] = 0;  // counted by k_labels_backfill (or k_root_flatten)
 
   // A. halo positions dir*r (reference product order) and node ids (-1 absent).
   // All of a thread's loads are issued before any is used (one memory round
@@ -632,7 +637,7 @@ __global__ void __launch_bounds__(T, LSEG_CERT_MINB) k_tile_cert(
   if (tid < 5) s_cnt[tid] = 0;
   if (rem == 0 && tid == 0) {
     fscal[f * 4 + 2] = 0;  // k_merge_cert's undecided-edge counter
-    n_labels[f] = 0;       // counted by k_root_flatten
+    n_labels[f] = 0;       // counted by k_labels_backfill (or k_root_flatten)
   }
 
   // A. halo positions dir*r (reference product order) and node ids
@@ -1073,7 +1078,7 @@ __global__ void k_merge_exact(lseg_sensor sn, Shape sh, const double* __restrict
 template <int TR, int TC, int T>
 __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int c0, int TRe, int TCe,
                                              const unsigned long long* s_m, int* s_par, int32_t* __restrict__ parent,
-                                             uint32_t* __restrict__ lroots) {
+                                             uint32_t* __restrict__ lroots, int32_t* __restrict__ hist, int64_t K) {
   constexpr int NT = TR * TC;
   // run starts: parent of every cell = first cell of its horizontal run
   for (int e = threadIdx.x; e < NT; e += T) {
@@ -1208,6 +1213,9 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
     }
     const int cell = (r0 + y) * sh.Sk + c0 + x;
     if (in) parent[nbase + cell] = pc;
+    // histogram slot of every tile-local root zeroed here (a superset of the
+    // final roots k_labels_backfill counts into)
+    if (hist && in && pc == cell) hist[(int64_t)f * K + cell + 1] = 0;
     const uint32_t b = __ballot_sync(0xffffffffu, in && pc == cell);
     const int word = (c0 + x) >> 5;
     if ((threadIdx.x & 31) == 0 && y < TRe && word < sh.Wk) lroots[((int64_t)f * sh.R + r0 + y) * sh.Wk + word] = b;
@@ -1225,7 +1233,7 @@ __global__ void k_tile_cc_dbg(Shape sh, const unsigned long long* __restrict__ m
   const int f = blockIdx.x;
   for (int j = threadIdx.x; j < TR * 5; j += T) s_m[j] = masks[(int64_t)f * TR * 5 + j];
   __syncthreads();
-  tile_cc_body<TR, TC, T>(sh, f, 0, 0, TR, TC, s_m, s_par, parent, lroots);
+  tile_cc_body<TR, TC, T>(sh, f, 0, 0, TR, TC, s_m, s_par, parent, lroots, nullptr, 0);
 }
 void debug_tile_cc(int n, const unsigned long long* masks, int32_t* parent, uint32_t* lroots) {
   const Shape sh = make_shape(n, TILE_R, TILE_C, 1);
@@ -1234,7 +1242,8 @@ void debug_tile_cc(int n, const unsigned long long* masks, int32_t* parent, uint
 
 template <int TR, int TC, int T>
 __global__ void __launch_bounds__(T, 2048 / T) k_tile_cc(Shape sh, const unsigned long long* __restrict__ masks,
-                                               int32_t* __restrict__ parent, uint32_t* __restrict__ lroots) {
+                                               int32_t* __restrict__ parent, uint32_t* __restrict__ lroots,
+                                               int32_t* __restrict__ hist, int64_t K) {
   __shared__ int s_par[TR * TC];
   __shared__ unsigned long long s_m[TR * 5];
   const int tilesC = (sh.Sk + TC - 1) / TC;
@@ -1247,7 +1256,7 @@ __global__ void __launch_bounds__(T, 2048 / T) k_tile_cc(Shape sh, const unsigne
   const unsigned long long* mrow = masks + b * (TR * 5);
   for (int j = threadIdx.x; j < TR * 5; j += T) s_m[j] = __ldg(mrow + j);
   __syncthreads();
-  tile_cc_body<TR, TC, T>(sh, f, r0, c0, TRe, TCe, s_m, s_par, parent, lroots);
+  tile_cc_body<TR, TC, T>(sh, f, r0, c0, TRe, TCe, s_m, s_par, parent, lroots, hist, K);
 }
 
 // Global union over the forward edges that leave a tile.  Threads enumerate
@@ -1495,7 +1504,9 @@ __global__ void __launch_bounds__(T, 2048 / T) k_labels_backfill(lseg_sensor sn,
                                                        const uint32_t* __restrict__ rbits,
                                                        const int32_t* __restrict__ rpre,
                                                        int32_t* __restrict__ node_labels, int32_t* __restrict__ out,
-                                                       int32_t* __restrict__ hist, int64_t K) {
+                                                       int32_t* __restrict__ hist, int64_t K,
+                                                       uint32_t* __restrict__ rbits_out, int32_t* __restrict__ n_labels,
+                                                       int32_t* __restrict__ rstat, int32_t* __restrict__ ticket) {
   extern __shared__ int s_dynrow[];
   const int S = sh.S, Sk = sh.Sk, k = sh.k, nwk = sh.Wk, nw = (S + 31) / 32;
   int* s_kv = s_dynrow;                                                 // per kept column
@@ -1510,9 +1521,23 @@ __global__ void __launch_bounds__(T, 2048 / T) k_labels_backfill(lseg_sensor sn,
   const uint32_t* rbf = rbits + (int64_t)f * sh.R * sh.Wk;
   const int32_t* rpf = rpre + (int64_t)f * sh.R * sh.Wk;
   const int64_t rb = (int64_t)row * S;
-  if (threadIdx.x == 0) s_any = 0;
+  // rbits_out != nullptr: k_root_flatten's work folded in (no node_labels
+  // output): each column chases its tile-local root to the final root
+  // itself, the row's final roots go to rbits_out and n_labels, and the
+  // pruning's per-row counters are reset here
+  const bool fold = rbits_out != nullptr;
+  __shared__ int s_nroot;
+  if (threadIdx.x == 0) {
+    s_any = 0;
+    s_nroot = 0;
+    if (fold) {
+      rstat[row] = 0;
+      if (row == 0) *ticket = 0;
+    }
+  }
   __syncthreads();
   bool any = false;
+  int nroot = 0;
   // classify the kept columns: donor label / target -2 / passive 0.  Chunks
   // of PF columns per thread with all loads of a chunk issued before they
   // are used (the two dependent parent loads would otherwise serialise).
@@ -1526,10 +1551,22 @@ __global__ void __launch_bounds__(T, 2048 / T) k_labels_backfill(lseg_sensor sn,
     }
 #pragma unroll
     for (int j = 0; j < PF; ++j) lv[j] = pv[j] >= 0 ? __ldcg(parf + pv[j]) : 0;  // its parent: the final root
+    if (fold) {
+#pragma unroll
+      for (int j = 0; j < PF; ++j)
+        if (pv[j] >= 0 && lv[j] != pv[j]) lv[j] = root_of(parf, lv[j]);  // merged across tiles
+    }
 #pragma unroll
     for (int j = 0; j < PF; ++j) {
       const int c = c0 + threadIdx.x + j * T;
       if (c >= nwk * 32) break;
+      if (fold) {
+        const uint32_t rm = __ballot_sync(0xffffffffu, pv[j] >= 0 && lv[j] == i * Sk + c);
+        if ((c & 31) == 0) {
+          rbits_out[(int64_t)row * nwk + (c >> 5)] = rm;
+          nroot += __popc(rm);
+        }
+      }
       int v = 0;
       if (pv[j] >= 0) v = lv[j] + 1;
       else if (c < Sk) v = ((__ldg(vbr + (c >> 5)) >> (c & 31)) & 1u) ? -2 : 0;  // valid, no normal
@@ -1540,7 +1577,9 @@ __global__ void __launch_bounds__(T, 2048 / T) k_labels_backfill(lseg_sensor sn,
     }
   }
   if (any && (threadIdx.x & 31) == 0) s_any = 1;
+  if (nroot) atomicAdd(&s_nroot, nroot);
   __syncthreads();
+  if (fold && threadIdx.x == 0 && s_nroot) atomicAdd(n_labels + f, s_nroot);
   const bool rany = s_any != 0;
   int32_t* hw = hist + (int64_t)f * K;
   // s / k as a multiply-high: exact for s < 2^32 / k (S <= 16384 here)
@@ -2081,9 +2120,9 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
         ws.fscal, n_labels);
     prof_mark("tile", st);
     if (nt < 148 * 16)  // one-wave batches: 256 threads per tile for latency
-      k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
+      k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
     else
-      k_tile_cc<TILE_R, TILE_C, LSEG_CC_TBIG><<<(unsigned)nt, LSEG_CC_TBIG, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
+      k_tile_cc<TILE_R, TILE_C, LSEG_CC_TBIG><<<(unsigned)nt, LSEG_CC_TBIG, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
     prof_mark("tile_cc", st);
     k_merge_cert<TILE_R, TILE_C><<<dim3((per + mt - 1) / mt, sh.F), mt, 0, st>>>(sn, sh, ranges, ws.vbits, bn4, cp,
                                                                                 ws.parent, ws.rank, ws.fscal);
@@ -2100,15 +2139,16 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
                                                                   ws.bnorm, ws.parent, ws.lroots, n_labels);
   prof_mark("tile", st);
   if (nt < 148 * 16)  // one-wave batches: 256 threads per tile for latency
-    k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
+    k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
   else
-    k_tile_cc<TILE_R, TILE_C, LSEG_CC_TBIG><<<(unsigned)nt, LSEG_CC_TBIG, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots);
+    k_tile_cc<TILE_R, TILE_C, LSEG_CC_TBIG><<<(unsigned)nt, LSEG_CC_TBIG, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
   prof_mark("tile_cc", st);
   k_merge<TILE_R, TILE_C><<<dim3((per + mt - 1) / mt, sh.F), mt, 0, st>>>(
       sh, ws.bnorm, thr[0], thr[1], thr[2], ws.parent);
   prof_mark("merge", st);
   }
-  {
+  const bool fold = !node_labels && LSEG_FOLD_FLATTEN;
+  if (!fold) {
     const int ft = (int64_t)sh.F * sh.R < 148 * 8 ? 256 : 128;  // one-wave batches: wider CTAs
     const int thr = sh.Wk >= ft / 32 ? ft : 32 * sh.Wk;
     k_root_flatten<<<sh.F * sh.R, thr, 0, st>>>(sh, ws.parent, ws.lroots, ws.rbits, ws.hist, ws.K, ws.fscal,
@@ -2127,10 +2167,12 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if ((int64_t)sh.F * sh.R < 148 * 8)  // one-wave batches: 256 threads per row for latency
     k_labels_backfill<256><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits,
-                                                           ws.rpre, node_labels, ws.lab_tmp, ws.hist, ws.K);
+                                                           ws.rpre, node_labels, ws.lab_tmp, ws.hist, ws.K,
+                                                           fold ? ws.rbits : nullptr, n_labels, ws.rcnt, ws.fscal + 3);
   else
     k_labels_backfill<128><<<sh.F * sh.R, 128, smem, st>>>(sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits,
-                                                           ws.rpre, node_labels, ws.lab_tmp, ws.hist, ws.K);
+                                                           ws.rpre, node_labels, ws.lab_tmp, ws.hist, ws.K,
+                                                           fold ? ws.rbits : nullptr, n_labels, ws.rcnt, ws.fscal + 3);
   prof_mark("labels_backfill", st);
 }
 
