@@ -56,8 +56,12 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_FOLD_FLATTEN
 #define LSEG_FOLD_FLATTEN 1
 #endif
-#ifndef LSEG_PF
-#define LSEG_PF 4
+// loads in flight per thread in the row kernels (measured: labels 2, pruning 8)
+#ifndef LSEG_PF_LAB
+#define LSEG_PF_LAB 2
+#endif
+#ifndef LSEG_PF_PRUNE
+#define LSEG_PF_PRUNE 8
 #endif
 #ifndef LSEG_CERT_MINB
 #define LSEG_CERT_MINB 4
@@ -1541,7 +1545,7 @@ __global__ void __launch_bounds__(T, 2048 / T) k_labels_backfill(lseg_sensor sn,
   // classify the kept columns: donor label / target -2 / passive 0.  Chunks
   // of PF columns per thread with all loads of a chunk issued before they
   // are used (the two dependent parent loads would otherwise serialise).
-  constexpr int PF = LSEG_PF;
+  constexpr int PF = LSEG_PF_LAB;
   for (int c0 = 0; c0 < nwk * 32; c0 += T * PF) {
     int pv[PF], lv[PF];
 #pragma unroll
@@ -2036,7 +2040,7 @@ __global__ void __launch_bounds__(T, 2048 / T) k_prune_rows(Shape sh, const int3
   __syncthreads();
   const int64_t rb = (int64_t)row * S;
   bool any = false;
-  constexpr int PF = LSEG_PF;
+  constexpr int PF = LSEG_PF_PRUNE;
   for (int s0 = 0; s0 < nw * 32; s0 += T * PF) {
     int lv[PF];
 #pragma unroll
