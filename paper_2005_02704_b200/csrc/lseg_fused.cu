@@ -57,6 +57,9 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #define LSEG_FOLD_FLATTEN 1
 #endif
 // loads in flight per thread in the row kernels (measured: labels 2, pruning 8)
+#ifndef LSEG_GEN_WARP_ROT
+#define LSEG_GEN_WARP_ROT 1
+#endif
 #ifndef LSEG_PF_LAB
 #define LSEG_PF_LAB 2
 #endif
@@ -303,7 +306,14 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       s_has[e] = 1;
     }
   }
+  // the general nodes start at the first warp after the last fan6 node's
+  // warp, i.e. on the warps with one fan6 node fewer per lane
+#if LSEG_GEN_WARP_ROT
+  const int gstart = (((nfan6 % T) + 31) & ~31) % T;
+  for (int i = (tid - gstart + T) % T; i < ngen; i += T) {
+#else
   for (int i = tid; i < ngen; i += T) {
+#endif
     const int e = s_list[NT - 1 - i];
     const int y = e / TC, x = e - y * TC;
     const unsigned m = s_m[e];
