@@ -770,7 +770,14 @@ __global__ void __launch_bounds__(T, LSEG_CERT_MINB) k_tile_cert(
     }
   };
   for (int i = tid; i < nfan6; i += T) node_normal(s_list[i], 0x3fu);  // straight-line: all six slots
+  // the rest from the first warp after the six-slot list's last partial warp
+  // (as in k_tile)
+#if LSEG_GEN_WARP_ROT
+  const int gstart = (((nfan6 % T) + 31) & ~31) % T;
+  for (int i = (tid - gstart + T) % T; i < ngen; i += T) {
+#else
   for (int i = tid; i < ngen; i += T) {
+#endif
     const int e = s_list[NT - 1 - i];
     node_normal(e, s_m[e]);
   }
