@@ -322,6 +322,8 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
       if (!((m >> s) & 1u)) continue;
+      // (row, column) through the flat index on purpose: the direct
+      // posyx(y + 1 + dr, x + 1 + dc) measured 1.3 % slower (register allocation)
       const int gq = (y + 1 + slot_dr(s)) * GC + x + 1 + slot_dc(s);
       const int yq = gq / GC;
       const Vec3 q = posyx(yq, gq - yq * GC);
