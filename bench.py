@@ -1,15 +1,23 @@
-"""Benchmark of the lidarseg hot path on B200 (driver contract, see DESIGN.md §Measurement).
+"""Benchmark of the lidarseg hot path on B200 (driver contract, see DESIGN.md §5).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
                     [--config hdl64_batch] [--interval 1] [--frames F]
+                    [--scaling strong|weak]
 
 A step = one pass of the whole hot path (bin -> mesh -> normals -> segment ->
-backfill -> prune) over one batch of F synthetic frames (BASELINE.json
-configs[3]: 512 HDL-64E-shape scans).  Each rank processes its own 512-frame
-batch (different poses), no data-path collective: "scaling": "weak".
-value = points processed by all ranks per second (device-resident inputs);
-e2e = the same through BatchPipeline with pinned host inputs, H2D of the
-points and D2H of the label grid inside the timed region.
+backfill -> prune) over one batch of synthetic frames: BASELINE.json
+configs[3], 512 HDL-64E-shape scans.  With N GPUs the one 512-frame batch is
+split into contiguous blocks of ceil(512/N) frames per rank (SURVEY.md §8(e),
+`dist.rank_batch`; "scaling": "strong"); `--scaling weak` gives every rank
+its own 512 frames instead.  No data-path collective: the run's only
+collective is the final all-reduce of (points, frames, segments, max
+elapsed).
+
+value = points processed by all ranks per second, inputs resident in HBM;
+e2e   = the same through the public host-to-host API (StreamingPipeline):
+        pinned host f32 xyz + int32 ring ids (the config's input) in, label
+        grid out, H2D / kernels / D2H overlapped in chunks, all inside the
+        timed region.
 """
 
 from __future__ import annotations
@@ -39,29 +47,23 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="hdl64_batch")
     ap.add_argument("--interval", type=int, default=1)
-    ap.add_argument("--frames", type=int, default=None)
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--frames", type=int, default=None, help="batch size (total over ranks when strong)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-latency", action="store_true", help="skip the single-scan latency (CUDA graph) lines")
+    ap.add_argument("--no-latency", action="store_true", help="skip the single-scan latency lines")
+    ap.add_argument("--no-accuracy", action="store_true", help="skip the suite accuracy (F1) line")
+    ap.add_argument("--no-parity", action="store_true", help="skip the sampled-frame oracle check / E_near")
     ap.add_argument("--e2e-chunk", type=int, default=64, help="frames per streamed chunk in the e2e run")
-    ap.add_argument("--e2e-rings", default="segments", choices=["segments", "u8", "i32"],
-                    help="ring input form of the e2e run: per-frame segment table, or a ring id per point")
-    ap.add_argument("--also-interval", type=int, default=5,
-                    help="also time this interval (reference default 5); 0 disables")
+    ap.add_argument("--also-intervals", default="5,10,15",
+                    help="also time these intervals (reference default 5, pipeline.py:25-26); '' disables")
     ap.add_argument("--seed", type=int, default=2005)
     ap.add_argument("--streams", type=int, default=1, help="frame chunks on concurrent streams")
     ap.add_argument("--chunk", type=int, default=0, help="sequential frame chunks of this size (0 = whole batch)")
     ap.add_argument("--normals", default="exact", choices=["certified", "exact"],
-                    help="fused-path normals: certified fp32 (labels exact) or exact fp64")
+                    help="fused-path normals: exact fp64 (default) or certified fp32 (labels exact either way)")
     return ap.parse_args()
-
-
-def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
 
 
 class ClockSampler:
@@ -110,115 +112,133 @@ class ClockSampler:
 def measured_peak_hbm():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            return float(json.load(fh)["hbm_gbs"]), "measured"
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
     except (OSError, KeyError, ValueError):
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-# Algorithmic bytes per stage of one pipeline launch over the batch (DESIGN.md
-# §5): P points, C cells (F*R*S), Ck kept cells (F*R*S'), N mesh nodes.  Each
-# entry is the compulsory HBM traffic of that kernel's inputs and outputs.
-def stage_bytes(P, C, Ck, N):
-    bnd = Ck * (2.0 / 16 + 2.0 / 64)  # tile-border cells (16 x 64 tiles)
+# ---- byte model (DESIGN.md §5 has the table)
+def pipeline_bytes(P, C, N):
+    """§8(d): B = 16 P + 8 C + 36 N + 4 C per batch (points in, f64 range
+    grid, neighbours + normals, labels)."""
+    return 16 * P + 8 * C + 36 * N + 4 * C
+
+
+def alg_stage_bytes(P, C, Ck, N):
+    """Each kernel's share of the §8(d) algorithmic bytes (compulsory API
+    inputs / outputs it moves; intermediates count 0): binning reads the
+    points and writes the grid, the tile reads the kept cells of the grid and
+    writes neighbours + normals, the pruning writes the labels."""
+    return {"bin_rows": 16 * P + 8 * C, "tile": 8 * Ck + 36 * N, "prune_apply": 4 * C}
+
+
+def design_stage_bytes(P, C, Ck, N, k):
+    """What each kernel of this design moves through HBM by construction
+    (intermediates included) -- the model the committed ncu DRAM counters
+    (profiles/) are compared against.  16 x 64 tiles."""
+    bnd = Ck * (2.0 / 16 + 2.0 / 64)           # tile-border cells
+    fb = 0 if k == 1 else C / 8                # full-resolution valid bits (k > 1)
     return {
-        "bin_rows": 16 * P + 8 * C + Ck / 8,           # points in, f64 grid + valid bits out
-        "bin_fallback": 0,                             # no-op unless the input is not ring-major
-        "frame_scan": Ck / 4,                          # valid bits in, word prefix out
-        # ranges + valid bits in; node ids, neighbours, normals, mask, parent,
-        # fp64 border normals (first/last row and column of 16 x 64 tiles) out
-        "tile": 8 * Ck + Ck / 4 + 4 * Ck + 24 * N + 12 * N + N + 24 * bnd + 5 * Ck / 8,
-        "tile_cc": 5 * Ck / 8 + 4 * Ck,                # pass masks in, tile-local parents out
+        "bin_rows": 16 * P + 8 * C + Ck / 8 + fb,
+        "frame_scan": Ck / 4,
+        "tile": 8 * Ck * (1 if k == 1 else 4) + Ck / 4 + 24 * N + 12 * N + N + 24 * bnd + 5 * Ck / 8,
+        "tile_cc": 5 * Ck / 8 + 4 * Ck + Ck / 8,
         "merge": 4 * bnd + 24 * bnd,
-        "root_flatten": 4 * Ck + Ck / 8,
-        "root_scan": Ck / 4,
-        "labels_backfill": 4 * Ck + Ck / 8 + 8 * (C - Ck) + 4 * C,
-        "prune_apply": 8 * C + Ck / 8 + Ck / 4 + Ck / 4,  # labels in/out; root bits in, survivor bits + prefix out
-        # single-op (unfused) path stages
-        "bin_fill": 8 * C, "bin": 24 * P, "valid_bits": 8 * Ck, "mesh": 4 * Ck + 24 * N,
-        "normals": 12 * Ck + 24 * N + 37 * N,
+        "labels_backfill": 8 * Ck + Ck / 8 + fb + 4 * C + Ck / 8,
+        "prune_apply": 8 * C + Ck / 8 + 8 * Ck / 32,
     }
 
 
-def committed_traffic(kernel, frames, interval):
-    """DRAM bytes per launch of `kernel` from the committed ncu capture
-    (profiles/traffic.json), if it was taken on this workload."""
+def committed_traffic(stage, frames, interval):
+    """DRAM bytes per launch of a stage's kernel from the committed ncu
+    launch list (profiles/traffic.json), if it was taken on this workload."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             t = json.load(fh)
     except (OSError, ValueError):
         return None
-    e = t.get(kernel)
+    e = t.get(f"{stage}@k{interval}") or t.get(stage)
     if e and e.get("frames") == frames and e.get("interval") == interval:
         return e
     return None
 
 
-def pipeline_bytes(P, C, N):
-    """B = 16 P + 8 C + 36 N + 4 C per batch."""
-    return 16 * P + 8 * C + 36 * N + 4 * C
-
-
-def cpu_baseline_port(shape, interval, seconds, seed):
-    """Oracle (NumPy port of the reference path) on 1 core, bounded sample."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import lidarseg_oracle as oracle
+# ---- CPU baselines (the oracle port of the reference path on this host)
+def _cpu_jobs(shape, interval, n, seed):
     from paper_2005_02704_b200 import synth
-    pts, nfr, t_used = 0, 0, 0.0
-    while t_used < seconds and nfr < 64:
-        xyz, ring, _ = synth.make_batch(shape, frames=1, seed=seed, first_frame=nfr)
-        xyz, ring = xyz.numpy(), ring.numpy()
-        t0 = time.perf_counter()
-        oracle.run_from_points(xyz, ring, shape.elevations, shape.steps, interval, shape.r_min, shape.r_max)
-        t_used += time.perf_counter() - t0
-        pts += xyz.shape[0]
-        nfr += 1
-    return {"value": pts / t_used, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{nfr} {shape.name} frames (k={interval}) through oracle/lidarseg_oracle.py "
-                      f"run_from_points, sequential, {t_used:.1f} s"}
+    jobs = []
+    for f in range(n):
+        xyz, ring, _ = synth.make_batch(shape, frames=1, seed=seed, first_frame=f)
+        jobs.append((xyz.numpy(), ring.numpy(), shape.elevations, shape.steps, interval, shape.r_min, shape.r_max))
+    return jobs
 
 
-def _ref_worker(args):
-    xyz, ring, elev, steps, interval, rmin, rmax = args
+def cpu_baselines(shape, intervals, seconds, seed):
+    """the reference CPU path (oracle port: same arithmetic
+    as reference run_pipeline + the binning restatement) on 1 core and on all
+    host cores (spawned multiprocessing pool over frames), at each interval,
+    each a bounded sample of the bench's frames."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import lidarseg_oracle as oracle
-    oracle.run_from_points(xyz, ring, elev, steps, interval, rmin, rmax)
-    return xyz.shape[0]
+    import cpu_pool
+    cores = os.cpu_count() or 1
+    out = []
+    for k in intervals:
+        # single core: frames one after another until ~`seconds`
+        import lidarseg_oracle as oracle
+        pts, used, nfr = 0, 0.0, 0
+        jobs = _cpu_jobs(shape, k, 8, seed)
+        while used < seconds and nfr < 64:
+            j = jobs[nfr % len(jobs)]
+            t0 = time.perf_counter()
+            oracle.run_from_points(*j)
+            used += time.perf_counter() - t0
+            pts += j[0].shape[0]
+            nfr += 1
+        out.append({"value": pts / used, "unit": UNIT, "cores": 1, "kind": "port", "interval": k,
+                    "sample": f"{nfr} {shape.name} frames (k={k}, {len(jobs)} distinct) through "
+                              f"oracle/lidarseg_oracle.py run_from_points, sequential, {used:.1f} s"})
+        # all cores: enough frames per round for every worker, rounds to ~`seconds`
+        per_frame = used / max(nfr, 1)
+        njobs = cores * 2
+        rounds = max(1, int(seconds / max(per_frame * njobs / cores, 1e-3)))
+        rounds = min(rounds, 8)
+        v, dt = cpu_pool.timed_pool([jobs[i % len(jobs)] for i in range(njobs)], cores, rounds=rounds, warmup=1)
+        out.append({"value": v, "unit": UNIT, "cores": cores, "kind": "port", "interval": k,
+                    "sample": f"{rounds} x {njobs} {shape.name} frames (k={k}) over a pool of {cores} "
+                              f"spawned workers, {dt:.1f} s"})
+    return out
 
 
 def run_reference(a, shape):
-    """--impl reference: the oracle port of the reference CPU path on all host cores."""
+    """--impl reference: the reference's CPU path (the oracle port -- the
+    reference is pure Python and not on the GPU box) on all host cores, on
+    this arm's config / metric; rank 0 only."""
     import multiprocessing as mp
-    from paper_2005_02704_b200 import synth
-    ws, rank, _ = dist_env()
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    for var in ("OMP_NUM_THREADS", "MKL_NUM_THREADS", "OPENBLAS_NUM_THREADS"):
-        os.environ[var] = "1"
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import cpu_pool
     cores = os.cpu_count() or 1
     per_step = max(cores, 2)
     nuniq = min(per_step, 32)
-    frames = []
-    for f in range(nuniq):
-        xyz, ring, _ = synth.make_batch(shape, frames=1, seed=a.seed, first_frame=f)
-        frames.append((xyz.numpy(), ring.numpy(), shape.elevations, shape.steps, a.interval, shape.r_min,
-                       shape.r_max))
-    jobs = [frames[i % nuniq] for i in range(per_step)]
-    ctx = mp.get_context("fork")
-    with ctx.Pool(cores) as pool:
+    jobs0 = _cpu_jobs(shape, a.interval, nuniq, a.seed)
+    jobs = [jobs0[i % nuniq] for i in range(per_step)]
+    with mp.get_context("fork").Pool(cores, initializer=cpu_pool._init) as pool:
         for _ in range(a.warmup):
-            pool.map(_ref_worker, jobs)
+            pool.map(cpu_pool.run_frame, jobs)
         t0 = time.perf_counter()
         pts = 0
         for _ in range(a.steps):
-            pts += sum(pool.map(_ref_worker, jobs))
+            pts += sum(pool.map(cpu_pool.run_frame, jobs))
         dt = time.perf_counter() - t0
     v = pts / dt
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-            "ms_per_step": dt / a.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (seeded ray-cast scenes, BASELINE.json shapes)",
+            "ms_per_step": dt / a.steps * 1e3, "higher_is_better": True, "scaling": a.scaling,
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded ray-cast scenes, BASELINE.json shapes)",
             "impl": "reference",
-            "config": {"workload": f"{shape.name}: {per_step} frames per step (sample of the 512-frame batch)",
-                       "interval": a.interval},
+            "config": {"workload": f"{shape.name}: {per_step} frames per step (bounded sample of the "
+                                   f"{shape.frames}-frame batch)", "interval": a.interval},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": f"{per_step} {shape.name} frames per step ({nuniq} distinct), "
                                        f"multiprocessing pool of {cores} workers over frames"},
@@ -226,10 +246,12 @@ def run_reference(a, shape):
     print(json.dumps(line), flush=True)
 
 
+# ---- single-scan latency (configs 1-3 are launch-bound)
 def single_scan_latency(dev, normals="exact", reps=200):
-    """single scans of configs 1-3 are launch-bound, so they
-    are reported as latency -- device time per frame of one scan, eager
-    (every kernel launched from the host) and as one replayed CUDA graph."""
+    """Per scan: the drop-in host-to-host run_pipeline(scan, cfg) call
+    (upload, one fused C-ABI call, download of mesh + fp64 normals + labels;
+    wall clock), and device time per frame of the batched pipeline eager and
+    as one replayed CUDA graph (BatchPipeline.capture)."""
     import paper_2005_02704_b200 as L
     from paper_2005_02704_b200 import synth
     out = {}
@@ -238,7 +260,7 @@ def single_scan_latency(dev, normals="exact", reps=200):
         xyz, ring, off = synth.make_batch(shape, frames=1, seed=77, device=dev)
         cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
                              r_max=shape.r_max)
-        bp = L.BatchPipeline(cfg, 1, frames=1, device=dev, normals=normals)
+        bp = L.BatchPipeline(cfg, 1, frames=1, device=dev, normals=normals, keep_node_ids=False)
         g = bp.capture(xyz, ring, off)
         st = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -253,6 +275,18 @@ def single_scan_latency(dev, normals="exact", reps=200):
             e1.record(st)
             torch.cuda.synchronize()
             res[mode + "_us_per_frame"] = e0.elapsed_time(e1) * 1e3 / reps
+        # the reference-facing single-scan call, host to host
+        grid = L.ScanGrid(config=cfg, ranges=bp.ranges[0].cpu().numpy())
+        pcfg = L.PipelineConfig(sensor=cfg, interval=1)
+        for _ in range(5):
+            L.run_pipeline(grid, pcfg)
+        ts = []
+        for _ in range(50):
+            t0 = time.perf_counter()
+            L.run_pipeline(grid, pcfg)
+            ts.append(time.perf_counter() - t0)
+        res["run_pipeline_us_host_to_host"] = float(np.median(ts)) * 1e6
+        res["run_pipeline_vs_graph"] = res["run_pipeline_us_host_to_host"] / res["graph_us_per_frame"]
         res["points"] = int(xyz.shape[0])
         out[name] = res
     return out
@@ -276,6 +310,82 @@ def suite_accuracy(dev, normals="exact", n_scenes=64):
     return out
 
 
+def near_threshold_edges(bp, thr, eps=1e-4):
+    """|E_near| over the whole batch: forward mesh edges
+    (slots N0..N2) between nodes with normals where some component's
+    | |dn_c| - T_c | < eps, evaluated in fp64 from the fp32 normals on the
+    device (the window is 1e-4 wide, fp32 rounding moves |dn| by < 1.2e-7)."""
+    n_near = n_fwd = 0
+    T = torch.tensor(thr, dtype=torch.float64, device=bp.normals.device)
+    for f in range(bp.frames):
+        n = int(bp.n_nodes[f])
+        if n == 0:
+            continue
+        nb = bp.neighbors[f, :n, :3].long()
+        m = bp.nmask[f, :n].bool()
+        v = bp.normals[f, :n].double()
+        p = torch.arange(n, device=nb.device).repeat_interleave(3)
+        q = nb.reshape(-1)
+        ok = q >= 0
+        p, q = p[ok], q[ok]
+        ok = m[p] & m[q]
+        p, q = p[ok], q[ok]
+        d = (v[p] - v[q]).abs()
+        n_near += int(((d - T).abs() < eps).any(dim=1).sum())
+        n_fwd += int(p.numel())
+    return n_near, n_fwd
+
+
+def sampled_parity(bp, xyz, ring, off, shape, interval, thr, frames):
+    """Sampled frames of the timed batch against the oracle (outside the
+    timed region): final labels bit-exact, and the near-threshold edges of
+    those frames with their flip count -- E_near edges whose decision under
+    the GPU's fp64 normals (single-scan run_pipeline on the same grid)
+    differs from the decision under the oracle's (= the reference's) fp64
+    normals."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import lidarseg_oracle as oracle
+    import paper_2005_02704_b200 as L
+    cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
+                         r_max=shape.r_max)
+    xh, rh, oh = xyz.cpu().numpy(), ring.cpu().numpy(), off.cpu().numpy()
+    match = near = flips = 0
+    T = np.asarray(thr, np.float64)
+    for f in frames:
+        sl = slice(oh[f], oh[f + 1])
+        want = oracle.run_from_points(xh[sl], rh[sl], shape.elevations, shape.steps, interval, shape.r_min,
+                                      shape.r_max)
+        match += int(np.array_equal(bp.labels[f].cpu().numpy(), want["labels"]))
+        res = L.run_pipeline(L.ScanGrid(config=cfg, ranges=want["ranges"]),
+                             L.PipelineConfig(sensor=cfg, interval=interval))
+        nb = want["mesh"]["neighbors"][:, :3]
+        vo = want["normals"]  # the oracle keeps the reference fp64 values
+        vg = res.normals.values
+        mk = want["mask"]
+        p = np.repeat(np.arange(nb.shape[0]), 3)
+        q = nb.ravel()
+        ok = q >= 0
+        p, q = p[ok], q[ok]
+        ok = mk[p] & mk[q]
+        p, q = p[ok], q[ok]
+        do = np.abs(vo[q] - vo[p])
+        nr = (np.abs(do - T) < 1e-4).any(axis=1)
+        dg = np.abs(vg[q[nr]] - vg[p[nr]])
+        near += int(nr.sum())
+        flips += int(((do[nr] < T).all(axis=1) != (dg < T).all(axis=1)).sum())
+    return {"frames_checked": len(frames), "labels_equal_oracle": match, "e_near": near, "flips": flips}
+
+
+def timed(fn, steps, st):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        fn()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+
+
 def main():
     a = parse()
     from paper_2005_02704_b200 import synth
@@ -286,6 +396,11 @@ def main():
     from paper_2005_02704_b200 import dist as D
     ws, rank, local = D.env()
     if ws > 1:
+        # NCCL's init report (communicator rank count, transport) on stderr:
+        # the only NCCL traffic is the barriers and the final all-reduces
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
@@ -293,25 +408,29 @@ def main():
     import paper_2005_02704_b200 as L
     from paper_2005_02704_b200 import _lib
 
-    F = a.frames or shape.frames
-    xyz, ring, off = synth.make_batch(shape, frames=F, seed=a.seed, device=dev, first_frame=rank * F)
+    F_total = a.frames or shape.frames
+    first, F, xyz, ring, off = D.rank_batch(shape, F_total, ws, rank, a.scaling, seed=a.seed, device=dev)
     P = int(xyz.shape[0])
     cfg = L.SensorConfig(ring_elevations=shape.elevations, azimuth_steps=shape.steps, r_min=shape.r_min,
                          r_max=shape.r_max)
-    bp = L.BatchPipeline(cfg, a.interval, frames=F, device=dev, streams=a.streams, chunk_frames=a.chunk or None,
-                         normals=a.normals)
     st = torch.cuda.current_stream()
 
     def barrier():
         if ws > 1:
             torch.distributed.barrier()
 
-    for _ in range(max(a.warmup, 3)):
-        bp.run(xyz, ring, off)
-    torch.cuda.synchronize()
-    N = int(bp.n_nodes.sum().item())
+    bp = None
+    N = 0
+    if F > 0:
+        bp = L.BatchPipeline(cfg, a.interval, frames=F, device=dev, streams=a.streams,
+                             chunk_frames=a.chunk or None, normals=a.normals, keep_node_ids=False)
+        for _ in range(max(a.warmup, 3)):
+            bp.run(xyz, ring, off)
+        torch.cuda.synchronize()
+        N = int(bp.n_nodes.sum().item())
     C = F * cfg.rings * cfg.azimuth_steps
-    Ck = F * cfg.rings * bp.Sk
+    Sk = _lib.kept_count(cfg.azimuth_steps, a.interval)
+    Ck = F * cfg.rings * Sk
 
     clocks = ClockSampler(local)
     barrier()
@@ -319,160 +438,189 @@ def main():
     clocks.start()
     time.sleep(0.3)
     _lib.profile_begin()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    for _ in range(a.steps):
-        bp.run(xyz, ring, off)
-    e1.record(st)
-    torch.cuda.synchronize()
+    elapsed = timed(lambda: bp.run(xyz, ring, off), a.steps, st) if bp is not None else 0.0
     stages = _lib.profile_end()
     clk = clocks.stop()
     barrier()
-    # the run's only collective: totals + max elapsed over ranks
-    run = D.reduce_run(P * a.steps, F * a.steps, int(bp.n_labels.sum().item()) * a.steps, e0.elapsed_time(e1),
-                       device=dev)
+    segs = int(bp.n_labels.sum().item()) if bp is not None else 0
+    final_segs = int(bp.labels.amax(dim=(1, 2)).sum().item()) if bp is not None else 0
+    run = D.reduce_run(P * a.steps, F * a.steps, final_segs * a.steps, elapsed, device=dev)
     ms = run["elapsed_ms"]
     ms_step = ms / a.steps
-    tot_pts = torch.tensor([run["points"] / a.steps], dtype=torch.float64)
     value = run["points"] / (ms / 1e3)
 
-    # ---- roofline of the dominant kernel + of the whole pipeline
+    # ---- roofline: the dominant kernel and the whole pipeline (per rank)
     peak, peak_kind = measured_peak_hbm()
-    sb = stage_bytes(P, C, Ck, N)
+    alg = alg_stage_bytes(P, C, Ck, N)
+    des = design_stage_bytes(P, C, Ck, N, a.interval)
+    stage_ms = {k: v[0] / v[1] for k, v in stages.items()}
     dom = max(stages, key=lambda k: stages[k][0]) if stages else None
     roof = None
     if dom:
-        dom_ms = stages[dom][0] / stages[dom][1]
-        ach = sb.get(dom, 0) / (dom_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "peak_kind": peak_kind,
-                "unit": "GB/s", "frac": ach / peak,
-                "ms_per_launch": dom_ms,
-                "share_of_step": stages[dom][0] / a.steps / ms_step,
-                "alg_bytes_per_launch": sb.get(dom, 0)}
+        dom_ms = stage_ms[dom]
+        ach = alg.get(dom, 0) / (dom_ms / 1e3) / 1e9
         ct = committed_traffic(dom, F, a.interval)
-        roof["traffic"] = ct["dram_bytes_per_launch"] if ct else None
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "peak_kind": peak_kind,
+                "unit": "GB/s", "frac": ach / peak, "ms_per_launch": dom_ms,
+                "share_of_step": stages[dom][0] / a.steps / ms_step,
+                "alg_bytes_per_launch": alg.get(dom, 0),
+                "alg_bytes_model": "SURVEY §8(d): tile = 8 C' (kept cells of the f64 grid in) + 36 N "
+                                   "(neighbours + normals out)",
+                "design_bytes_per_launch": des.get(dom),
+                "traffic": ct["dram_bytes_per_launch"] if ct else None,
+                "traffic_source": ct["source"] if ct else None}
         if ct and "fp64_pipe_active" in ct:
-            # what actually limits it (same capture): the kernel is FP64 / issue
-            # bound, not HBM bound -- see DESIGN.md §5
-            roof["limiter"] = {"fp64_pipe_active": ct["fp64_pipe_active"], "issue_active": ct["issue_active"],
-                               "source": ct["source"]}
+            roof["limiter"] = {k: ct[k] for k in ("fp64_pipe_active", "issue_active") if k in ct}
     pb = pipeline_bytes(P, C, N)
-    pipe_roof = {"alg_bytes_per_step": pb, "achieved_gbs": pb / (ms_step / 1e3) / 1e9,
-                 "frac": pb / (ms_step / 1e3) / 1e9 / peak, "frac_of_8tbs": pb / (ms_step / 1e3) / 1e9 / 8000.0}
-    stage_ms = {k: round(v[0] / v[1], 4) for k, v in stages.items()}
+    pipe_roof = {"alg_bytes_per_step": pb, "achieved_gbs": pb / (ms_step / 1e3) / 1e9 if ms_step else 0.0,
+                 "frac": pb / (ms_step / 1e3) / 1e9 / peak if ms_step else 0.0,
+                 "frac_of_8tbs": pb / (ms_step / 1e3) / 1e9 / 8000.0 if ms_step else 0.0,
+                 "bytes_per_point": pb / max(P, 1)}
+    per_stage = {k: {"ms": round(stage_ms[k], 4), "share": round(stages[k][0] / a.steps / ms_step, 4),
+                     "alg_bytes": alg.get(k, 0), "design_bytes": des.get(k),
+                     "design_gbs": (des.get(k) or 0) / (stage_ms[k] / 1e3) / 1e9} for k in stages}
 
-    # ---- the same batch at the reference's default interval (pipeline.py:25)
-    other = None
-    if a.also_interval and a.also_interval != a.interval:
-        bp2 = L.BatchPipeline(cfg, a.also_interval, frames=F, device=dev, normals=a.normals)
-        for _ in range(3):
-            bp2.run(xyz, ring, off)
+    # ---- near-threshold edges of the timed batch, sampled-frame parity (outside the timed region)
+    thr = tuple(float(t) for t in L.SegmenterConfig().thresholds)
+    near = None
+    if bp is not None and not a.no_parity:
+        e_near, e_fwd = near_threshold_edges(bp, thr)
+        near = {"e_near": e_near, "forward_edges": e_fwd, "eps": 1e-4}
+        if rank == 0:
+            near["sampled"] = sampled_parity(bp, xyz, ring, off, shape, a.interval, thr,
+                                             sorted({0, F // 3, (2 * F) // 3, F - 1}))
+
+    # ---- the same batch at the reference's other intervals (pipeline.py:25-26)
+    others = []
+    for k in [int(v) for v in a.also_intervals.split(",") if v.strip()]:
+        if k == a.interval:
+            continue
+        el = 0.0
+        if F > 0:
+            bp2 = L.BatchPipeline(cfg, k, frames=F, device=dev, normals=a.normals, keep_node_ids=False)
+            for _ in range(3):
+                bp2.run(xyz, ring, off)
+            torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
-        e0.record(st)
-        for _ in range(a.steps):
-            bp2.run(xyz, ring, off)
-        e1.record(st)
-        torch.cuda.synchronize()
-        r2 = D.reduce_run(P * a.steps, F * a.steps, 0, e0.elapsed_time(e1), device=dev)
-        other = {"interval": a.also_interval, "value": r2["points"] / (r2["elapsed_ms"] / 1e3), "unit": UNIT,
-                 "ms_per_step": r2["elapsed_ms"] / a.steps,
-                 "frames_per_s": r2["frames"] / (r2["elapsed_ms"] / 1e3)}
-        del bp2
+        if F > 0:
+            el = timed(lambda: bp2.run(xyz, ring, off), a.steps, st)
+            N2 = int(bp2.n_nodes.sum().item())
+            del bp2
+        else:
+            N2 = 0
+        r2 = D.reduce_run(P * a.steps, F * a.steps, 0, el, device=dev)
+        ck2 = F * cfg.rings * _lib.kept_count(cfg.azimuth_steps, k)
+        pb2 = pipeline_bytes(P, C, N2)
+        others.append({"interval": k, "value": r2["points"] / (r2["elapsed_ms"] / 1e3), "unit": UNIT,
+                       "ms_per_step": r2["elapsed_ms"] / a.steps,
+                       "frames_per_s": r2["frames"] / (r2["elapsed_ms"] / 1e3),
+                       "pipeline_frac": pb2 / (r2["elapsed_ms"] / a.steps / 1e3) / 1e9 / peak,
+                       "kept_cells": ck2, "nodes": N2})
 
-    # ---- e2e through the public API (StreamingPipeline): pinned host points in,
-    # pinned host label grid out, H2D / kernels / D2H overlapped in chunks
+    # ---- e2e through the public API (StreamingPipeline): pinned host points
+    # (f32 xyz + int32 ring ids, the config's input) in, pinned label grid out
     e2e = None
+    e2e_alt = None
     if not a.no_e2e:
         hx = xyz.cpu().pin_memory()
         ho = off.cpu()
-        if a.e2e_rings == "segments":
-            # ring-major points carry their rings as a per-frame (R+1) offset
-            # table (LSEG_PIPE_RING_SEGMENTS): 12 B per point on the wire
-            rdt = "segments"
-            hr = L.ring_segments(ring, off, cfg.rings).cpu().pin_memory()
-        else:
-            # one byte per ring id (<= 256 rings): 13 B instead of 16 B per point
-            rdt = torch.uint8 if (a.e2e_rings == "u8" and cfg.rings <= 256) else torch.int32
-            hr = ring.to(rdt).cpu().pin_memory()
-        hl = torch.empty(bp.labels.shape, dtype=torch.int32).pin_memory()
-        cf = min(a.e2e_chunk, F)
-        maxp = max(int(ho[min(f + cf, F)] - ho[f]) for f in range(0, F, cf))
-        del bp  # free the device-resident pipeline before allocating the streaming one
-        sp = L.StreamingPipeline(cfg, a.interval, chunk_frames=cf, max_chunk_points=maxp, device=dev, ring_dtype=rdt,
-                                 normals=a.normals)
-        for _ in range(2):
-            sp.run_host(hx, hr, ho, hl)
-        torch.cuda.synchronize()
-        barrier()
-        e0.record(st)
-        for _ in range(a.steps):
-            sp.run_host(hx, hr, ho, hl)
-        e1.record(st)
-        torch.cuda.synchronize()
-        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if ws > 1:
-            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-        h2d = hx.numel() * hx.element_size() + hr.numel() * hr.element_size() + ho.numel() * ho.element_size()
-        # the PCIe ceiling of the same traffic: copy-only time of h2d bytes up
-        # and the label bytes down, concurrently on two streams
-        del sp
-        up_h = torch.empty(int(h2d), dtype=torch.uint8).pin_memory()
-        up_d = torch.empty(int(h2d), dtype=torch.uint8, device=dev)
-        dn_d = torch.empty(hl.numel() * 4, dtype=torch.uint8, device=dev)
-        dn_h = torch.empty(hl.numel() * 4, dtype=torch.uint8).pin_memory()
-        s_up, s_dn = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        hr = ring.cpu().pin_memory()
+        hl = torch.empty((F, cfg.rings, cfg.azimuth_steps), dtype=torch.int32).pin_memory()
+        cf = max(1, min(a.e2e_chunk, F))
+        maxp = max([int(ho[min(f + cf, F)] - ho[f]) for f in range(0, F, cf)] or [1])
+        del bp
+        bp = None
+        torch.cuda.empty_cache()
 
-        def copies():
-            s_up.wait_stream(st)
-            s_dn.wait_stream(st)
-            with torch.cuda.stream(s_up):
-                up_d.copy_(up_h, non_blocking=True)
-            with torch.cuda.stream(s_dn):
-                dn_h.copy_(dn_d, non_blocking=True)
-            st.wait_stream(s_up)
-            st.wait_stream(s_dn)
+        def e2e_run(ring_h, rdt):
+            sp = L.StreamingPipeline(cfg, a.interval, chunk_frames=cf, max_chunk_points=max(maxp, 1), device=dev,
+                                     ring_dtype=rdt, normals=a.normals)
+            if F > 0:
+                for _ in range(2):
+                    sp.run_host(hx, ring_h, ho, hl)
+            torch.cuda.synchronize()
+            barrier()
+            el = timed(lambda: sp.run_host(hx, ring_h, ho, hl), a.steps, st) if F > 0 else 0.0
+            te = torch.tensor([el], dtype=torch.float64, device=dev)
+            if ws > 1:
+                torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+            del sp
+            return float(te.item())
 
-        copies()
-        torch.cuda.synchronize()
-        e0.record(st)
-        for _ in range(3):
+        t_i32 = e2e_run(hr, torch.int32)
+        h2d = hx.numel() * 4 + hr.numel() * 4 + ho.numel() * 8
+        d2h = hl.numel() * 4
+        e2e = {"value": run["points"] / (t_i32 / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": t_i32 / a.steps, "chunk_frames": cf, "ring_input": "int32 ring id per point",
+               "api": "StreamingPipeline.run_host (host f32 xyz + i32 ring + offsets -> host label grid)"}
+        # the ring-major input form: the per-frame ring segment table computed
+        # from the int32 ids on the host per chunk, inside the timed region
+        t_seg = e2e_run(hr, "segments_from_ids")
+        h2d_seg = hx.numel() * 4 + F * (cfg.rings + 1) * 8 + ho.numel() * 8
+        e2e_alt = {"value": run["points"] / (t_seg / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d_seg),
+                   "d2h_bytes_per_step": int(d2h), "ms_per_step": t_seg / a.steps,
+                   "ring_input": "int32 ring ids -> per-frame ring segment table on the host (timed), "
+                                 "12 B per point on the wire"}
+        # the PCIe ceiling of the headline traffic: copy-only time of the same
+        # bytes up and the label bytes down, concurrently on two streams
+        if F > 0:
+            up_h = torch.empty(int(h2d), dtype=torch.uint8).pin_memory()
+            up_d = torch.empty(int(h2d), dtype=torch.uint8, device=dev)
+            dn_d = torch.empty(int(d2h), dtype=torch.uint8, device=dev)
+            dn_h = torch.empty(int(d2h), dtype=torch.uint8).pin_memory()
+            s_up, s_dn = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+            def copies():
+                s_up.wait_stream(st)
+                s_dn.wait_stream(st)
+                with torch.cuda.stream(s_up):
+                    up_d.copy_(up_h, non_blocking=True)
+                with torch.cuda.stream(s_dn):
+                    dn_h.copy_(dn_d, non_blocking=True)
+                st.wait_stream(s_up)
+                st.wait_stream(s_dn)
+
             copies()
-        e1.record(st)
-        torch.cuda.synchronize()
-        copy_ms = e0.elapsed_time(e1) / 3
-        del up_h, up_d, dn_d, dn_h
-        e2e = {"value": float(tot_pts.item()) * a.steps / (float(te.item()) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(hl.numel() * 4),
-               "copy_only_ms_per_step": copy_ms, "frac_of_copy_bound": copy_ms / (float(te.item()) / a.steps),
-               "ms_per_step": float(te.item()) / a.steps, "chunk_frames": cf, "ring_input": str(rdt).replace("torch.", "")}
+            torch.cuda.synchronize()
+            copy_ms = timed(copies, 3, st) / 3
+            e2e["copy_only_ms_per_step"] = copy_ms
+            e2e["frac_of_copy_bound"] = copy_ms / (t_i32 / a.steps)
+            del up_h, up_d, dn_d, dn_h
 
     cpu = None
     if rank == 0 and ws == 1 and not a.no_cpu_baseline:
-        cpu = cpu_baseline_port(shape, a.interval, a.cpu_seconds, a.seed)
+        cpu = cpu_baselines(shape, sorted({a.interval, 5}), a.cpu_seconds, a.seed)
 
     if rank == 0:
-        # kernels per profiled stage of the fused pipeline (csrc/lseg_fused.cu):
-        # "bin_rows" = k_ring_bounds + k_bin_rows; every other stage is one kernel
-        # (the fallback-flag memset is not a kernel)
-        per_stage = {"bin_rows": 2, "bin_fill": 0}
-        launches = sum(v[1] * per_stage.get(k, 1) for k, v in stages.items())
+        # our kernels per profiled stage (csrc/lseg_fused.cu): "bin_rows" =
+        # k_ring_bounds + k_bin_rows; every other stage is one kernel
+        kernels_per_stage = {"bin_rows": 2}
+        launches = sum(v[1] * kernels_per_stage.get(k, 1) for k, v in stages.items())
+        main_cpu = None
+        if cpu:
+            main_cpu = next(c for c in cpu if c["interval"] == a.interval and c["cores"] > 1)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": a.steps,
-                "warmup": max(a.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64" if a.normals == "exact" else "f32+f64",
+                "warmup": max(a.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": a.scaling, "vs_baseline": None, "dtype": "f64" if a.normals == "exact" else "f32+f64",
                 "data": "synthetic (seeded ray-cast scenes, BASELINE.json shapes)",
-                "config": {"workload": f"{shape.name}: {F} frames x {cfg.rings}x{cfg.azimuth_steps} per rank "
-                                       f"(BASELINE configs[3])", "interval": a.interval, "frames_per_rank": F,
-                           "points_per_rank": P, "nodes_per_rank": N, "parallelism": f"frame-shard x{ws}",
-                           "normals": a.normals,
-                           "l2": "inputs (>1 GB per step) exceed the 126 MB L2; no flush needed"},
+                "config": {"workload": f"{shape.name}: {F_total} frames x {cfg.rings}x{cfg.azimuth_steps}"
+                                       + (f" split over {ws} ranks" if a.scaling == "strong" else " per rank")
+                                       + " (BASELINE configs[3])",
+                           "interval": a.interval, "frames_total": run["frames"] // a.steps,
+                           "frames_rank0": F, "points_rank0": P, "nodes_rank0": N,
+                           "parallelism": f"frame-shard x{ws} ({a.scaling})", "normals": a.normals,
+                           "l2": "inputs (~1 GB per step) exceed the 126 MB L2; no flush needed"},
                 "frames_per_s": run["frames"] / (ms / 1e3),
-                "segments_per_frame": run["segments"] / max(run["frames"], 1),
-                "roofline": roof, "pipeline_roofline": pipe_roof, "stage_ms": stage_ms,
-                "at_interval_%d" % a.also_interval if other else "at_other_interval": other,
-                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk}
+                "final_segments_per_frame": run["segments"] / max(run["frames"], 1),
+                "roofline": roof, "pipeline_roofline": pipe_roof, "stages": per_stage,
+                "other_intervals": others, "near_threshold": near,
+                "cpu_baseline": main_cpu, "cpu_baselines": cpu, "e2e": e2e, "e2e_ring_segments": e2e_alt,
+                "gpu_launches": int(launches), "clocks": clk}
         if not a.no_latency:
             line["single_scan_latency"] = single_scan_latency(dev, a.normals)
+        if not a.no_accuracy:
             line["accuracy_vs_truth"] = suite_accuracy(dev, a.normals)
         print(json.dumps(line), flush=True)
     if ws > 1:

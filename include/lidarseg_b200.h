@@ -125,7 +125,9 @@ int lseg_backfill(const lseg_sensor* sensor, int32_t frames, const double* range
                   const int32_t* labels_in, int32_t* labels_out, void* stream);
 
 /* Replaces prune_small (reference segment.py:127-160).  label_bound is an
- * exclusive upper bound on label values (the caller knows max+1). */
+ * exclusive upper bound on label values (the caller knows max+1).  Labels
+ * >= label_bound are a caller error: they are not counted, never index the
+ * workspace, and come out as -1. */
 int lseg_prune_small(int32_t frames, int32_t rings, int32_t steps, const int32_t* labels_in,
                      int32_t min_segment_size, int64_t label_bound, int32_t* labels_out,
                      void* workspace, size_t workspace_bytes, void* stream);
@@ -135,7 +137,8 @@ int lseg_prune_small(int32_t frames, int32_t rings, int32_t steps, const int32_t
  * Outputs as in the individual ops; normals32 (F,cap,3) f32;
  * node_labels (F,R,S) optional (NULL) = segment() output before completion;
  * labels (F,R,S) = after backfill + prune_small; n_nodes (F) mesh nodes;
- * n_labels (F) = number of segment() labels (before completion). */
+ * n_labels (F) = number of segment() labels (before completion).
+ * node_ids and normals32 may be NULL (not written). */
 int lseg_run_pipeline(const lseg_sensor* sensor, int32_t frames, int32_t interval,
                       const double* thresholds, int32_t min_segment_size, const float* xyz,
                       const int32_t* ring, const int64_t* frame_offsets, int64_t total_points,
@@ -187,6 +190,17 @@ int lseg_run_pipeline_grid(const lseg_sensor* sensor, int32_t frames, int32_t in
                            const double* ranges, int32_t* node_ids, int32_t* neighbors, float* normals32,
                            uint8_t* nmask, int32_t* node_labels, int32_t* labels, int32_t* n_nodes,
                            int32_t* n_labels, void* workspace, size_t workspace_bytes, void* stream);
+
+/* The drop-in single-scan path (reference run_pipeline(scan, cfg),
+ * pipeline.py:47-70, returning its PipelineResult fields) for F scans in ONE
+ * call: ranges (F, R, S) f64 in; mesh node_ids (F,R,S') and neighbors
+ * (F,cap,6), fp64 normals64 (F,cap,3) (the reference's NormalMap values,
+ * bit-identical; NaN rows where nmask is 0), segment() node_labels (F,R,S)
+ * (optional), final labels (F,R,S).  Exact fp64 normals only. */
+int lseg_run_scans(const lseg_sensor* sensor, int32_t frames, int32_t interval, const double* thresholds,
+                   int32_t min_segment_size, const double* ranges, int32_t* node_ids, int32_t* neighbors,
+                   double* normals64, uint8_t* nmask, int32_t* node_labels, int32_t* labels, int32_t* n_nodes,
+                   int32_t* n_labels, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- edge-based evaluation (reference evaluate.py:40-94).
  * Label grids (F,R,S) i32, 0 = unlabelled.  Scratch sized by

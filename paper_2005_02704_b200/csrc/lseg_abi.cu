@@ -325,8 +325,8 @@ static int run_pipeline_impl(const lseg_sensor* sensor, int32_t frames, int32_t 
   if (frames == 0) return LSEG_OK;
   Workspace ws;
   if (int e = check_ws(sh, 0, workspace, workspace_bytes, &ws)) return e;
-  if (!ranges || !node_ids || !neighbors || !nmask || !labels || !n_nodes || !n_labels || !frame_offsets)
-    return fail(LSEG_EINVAL, "NULL buffer");
+  if (!ranges || !neighbors || !nmask || !labels || !n_nodes || !n_labels || !frame_offsets)
+    return fail(LSEG_EINVAL, "NULL buffer");  // node_ids / normals32 / node_labels optional
   cudaStream_t st = (cudaStream_t)stream;
   prof_mark(nullptr, st);
   const bool fused_bin = sensor->steps <= 8192;
@@ -403,8 +403,8 @@ int lseg_run_pipeline_grid(const lseg_sensor* sensor, int32_t frames, int32_t in
   if (frames == 0) return LSEG_OK;
   Workspace ws;
   if (int e = check_ws(sh, 0, workspace, workspace_bytes, &ws)) return e;
-  if (!ranges || !node_ids || !neighbors || !nmask || !labels || !n_nodes || !n_labels)
-    return fail(LSEG_EINVAL, "NULL buffer");
+  if (!ranges || !neighbors || !nmask || !labels || !n_nodes || !n_labels)
+    return fail(LSEG_EINVAL, "NULL buffer");  // node_ids / normals32 / node_labels optional
   cudaStream_t st = (cudaStream_t)stream;
   prof_mark(nullptr, st);
   float* dbg = g_dbg_err;
@@ -414,6 +414,31 @@ int lseg_run_pipeline_grid(const lseg_sensor* sensor, int32_t frames, int32_t in
                      node_labels, false, (flags & LSEG_PIPE_CERT_NORMALS) == 0, dbg, st);
   launch_prune_fused(sh, ws, min_segment_size, labels, st);
   return check_launch("run_pipeline_grid");
+}
+
+int lseg_run_scans(const lseg_sensor* sensor, int32_t frames, int32_t interval, const double* thresholds,
+                   int32_t min_segment_size, const double* ranges, int32_t* node_ids, int32_t* neighbors,
+                   double* normals64, uint8_t* nmask, int32_t* node_labels, int32_t* labels, int32_t* n_nodes,
+                   int32_t* n_labels, void* workspace, size_t workspace_bytes, void* stream) {
+  if (int e = check_sensor(sensor)) return e;
+  Shape sh;
+  if (int e = check_shape(frames, sensor->rings, sensor->steps, interval, &sh)) return e;
+  if (!thresholds) return fail(LSEG_EINVAL, "thresholds is NULL");
+  for (int c = 0; c < 3; ++c)
+    if (!(thresholds[c] > 0.0 && thresholds[c] <= 2.0)) return fail(LSEG_EINVAL, "thresholds must be in (0, 2]");
+  if (min_segment_size < 0) return fail(LSEG_EINVAL, "min_segment_size must be >= 0");
+  if (frames == 0) return LSEG_OK;
+  Workspace ws;
+  if (int e = check_ws(sh, 0, workspace, workspace_bytes, &ws)) return e;
+  if (!ranges || !node_ids || !neighbors || !normals64 || !nmask || !labels || !n_nodes || !n_labels)
+    return fail(LSEG_EINVAL, "NULL buffer");
+  cudaStream_t st = (cudaStream_t)stream;
+  prof_mark(nullptr, st);
+  launch_valid_scan(*sensor, sh, ranges, ws, n_nodes, st);
+  launch_fused_graph(*sensor, sh, ws, ranges, thresholds, node_ids, neighbors, nullptr, nmask, n_nodes, n_labels,
+                     node_labels, false, true, nullptr, st, normals64);
+  launch_prune_fused(sh, ws, min_segment_size, labels, st);
+  return check_launch("run_scans");
 }
 
 void lseg_debug_cert_err(float* per_node_err) { g_dbg_err = per_node_err; }

@@ -121,7 +121,8 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
                                                 int32_t* __restrict__ neighbors, float* __restrict__ n32,
                                                 uint8_t* __restrict__ nmask, unsigned long long* __restrict__ masks,
                                                 double* __restrict__ bnorm, int32_t* __restrict__ parent,
-                                                uint32_t* __restrict__ lroots, int32_t* __restrict__ n_labels) {
+                                                uint32_t* __restrict__ lroots, int32_t* __restrict__ n_labels,
+                                                double* __restrict__ n64) {
   constexpr int GR = TR + 2, GC = TC + 2;  // halo rows r0-1..r0+TR, cols c0-1..c0+TC
   constexpr int NT = TR * TC;
 #if LSEG_PHASES
@@ -365,6 +366,13 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       o[0] = has ? (float)s_nx[e] : qn;
       o[1] = has ? (float)s_ny[e] : qn;
       o[2] = has ? (float)s_nz[e] : qn;
+    }
+    if (n64) {  // fp64 normals (the single-scan drop-in: reference NormalMap values)
+      double* o = n64 + (nbase + id) * 3;
+      const double qn = __longlong_as_double(0x7ff8000000000000LL);
+      o[0] = has ? s_nx[e] : qn;
+      o[1] = has ? s_ny[e] : qn;
+      o[2] = has ? s_nz[e] : qn;
     }
     nmask[nbase + id] = has ? 1 : 0;
     if (has) {  // fp64 normals of the tile's border rows / columns for k_merge (coalesced)
@@ -2118,7 +2126,7 @@ void debug_phases(double* out) {
 void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace& ws, const double* ranges,
                         const double* thr, int32_t* node_ids, int32_t* neighbors, float* n32, uint8_t* nmask,
                         int32_t* n_nodes, int32_t* n_labels, int32_t* node_labels, bool fbits_valid,
-                        bool exact_normals, float* dbg_err, cudaStream_t st) {
+                        bool exact_normals, float* dbg_err, cudaStream_t st, double* n64) {
   const int tilesC = (sh.Sk + TILE_C - 1) / TILE_C, tilesR = (sh.R + TILE_R - 1) / TILE_R;
   const int64_t nt = (int64_t)sh.F * tilesR * tilesC;
   const int per = tilesR * sh.Sk + tilesC * sh.R;
@@ -2159,7 +2167,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   cudaFuncSetAttribute(k_tile<TILE_R, TILE_C, TILE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
   k_tile<TILE_R, TILE_C, TILE_T><<<(unsigned)nt, TILE_T, tsmem, st>>>(sn, sh, ranges, ws.vbits, ws.wpre, thr[0], thr[1],
                                                                   thr[2], node_ids, neighbors, n32, nmask, ws.masks,
-                                                                  ws.bnorm, ws.parent, ws.lroots, n_labels);
+                                                                  ws.bnorm, ws.parent, ws.lroots, n_labels, n64);
   prof_mark("tile", st);
   if (nt < 148 * 16)  // one-wave batches: 256 threads per tile for latency
     k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);

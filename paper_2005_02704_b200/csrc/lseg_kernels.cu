@@ -29,7 +29,11 @@ __global__ void k_bin_points(lseg_sensor sn, int F, const float* __restrict__ xy
                              int64_t P, double* __restrict__ ranges, int32_t* __restrict__ cell_out) {
   const int R = sn.rings, S = sn.steps;
   const double dS = (double)S;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+  // only the points the frames own: [off[0], off[F]) read on the device (the
+  // buffer behind xyz may be longer than the frames' points, e.g. a reused
+  // chunk buffer, and off[0] need not be 0 for a sub-batch of a larger one)
+  const int64_t pb = __ldg(off), pe = min(__ldg(off + F), P);
+  for (int64_t p = pb + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < pe;
        p += (int64_t)gridDim.x * blockDim.x) {
     // frame of point p: binary search in off[0..F]
     int lo = 0, hi = F;  // off[lo] <= p < off[hi]
@@ -363,7 +367,7 @@ __global__ void __launch_bounds__(T) k_ring_fill(int mode, lseg_sensor sn, Shape
   auto is_donor = [&](int lab) -> bool {
     if (lab <= 0) return false;
     if (mode == 0) return true;
-    return !(any_small && hf[lab] < min_size);
+    return lab >= K || !(any_small && hf[lab] < min_size);  // >= K: caller error, see below
   };
   const int s0 = threadIdx.x * ITEMS;
   int last = INT_MIN, first = INT_MAX;
@@ -415,7 +419,7 @@ __global__ void __launch_bounds__(T) k_ring_fill(int mode, lseg_sensor sn, Shape
     int res = lab;
     bool target;
     if (mode == 0) target = (lab == 0) && in_window(__ldg(rrow + s), sn.r_min, sn.r_max);
-    else target = (lab > 0) && any_small && hf[lab] < min_size;
+    else target = (lab > 0) && lab < K && any_small && hf[lab] < min_size;
     if (target) {
       if (!has_donor) {
         res = (mode == 0) ? lab : 0;
@@ -430,7 +434,9 @@ __global__ void __launch_bounds__(T) k_ring_fill(int mode, lseg_sensor sn, Shape
       }
     }
     if (is_donor(lab)) pd = s;
-    if (mode == 1) res = any_small ? rm[res] : res;
+    // a label >= K (label_bound too small, a caller error) comes out as -1:
+    // no histogram / remap access outside the workspace
+    if (mode == 1) res = res >= K ? -1 : (any_small ? rm[res] : res);
     out[s] = res;
     if (hw) {  // run-length aggregated histogram of the backfilled row
       if (res == run_lab) ++run_len;
@@ -497,7 +503,10 @@ __global__ void k_hist(Shape sh, int64_t K, const int32_t* __restrict__ labels, 
   const int64_t per = (int64_t)sh.R * sh.S;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
     const int lab = labels[t];
-    if (lab > 0) atomicAdd(hist + (t / per) * K + lab, 1);
+    // labels outside [1, K) are a caller error (label_bound too small): not
+    // counted, flagged in hist[frame * K + 0] (slot 0 is never a label)
+    if (lab > 0 && lab < K) atomicAdd(hist + (t / per) * K + lab, 1);
+    else if (lab >= K) atomicOr(hist + (t / per) * K, 1);
   }
 }
 

@@ -1,8 +1,8 @@
 """End-to-end hot path, mirroring reference pkg/src/lidarseg/pipeline.py.
 
 * ``run_pipeline(scan, cfg, interval=None)`` — the reference's single-scan
-  entry point (pipeline.py:47-70): mesh -> normals -> segment -> backfill ->
-  prune on the GPU, stage timings from CUDA events.
+  entry point (pipeline.py:47-70): one upload, one fused C-ABI call
+  (lseg_run_scans), one download; stage timings from CUDA events.
 * ``bin_points(xyz, ring, config)`` — the new binning op.
 * ``BatchPipeline`` — the batched, device-resident form of the whole path
   (points -> labels for F frames in one C-ABI call, lseg_run_pipeline); this
@@ -17,11 +17,11 @@ import numpy as np
 import torch
 
 from . import _lib
-from .mesh import Mesh, build_mesh
-from .normals import NormalMap, estimate_normals_device
+from .mesh import Mesh
+from .normals import NormalMap
 from .scan import ScanGrid, SensorConfig, device_tables, subsample_steps
 from .evaluate import EvalConfig
-from .segment import SegmenterConfig, backfill_device, prune_small_device, segment_device
+from .segment import SegmenterConfig
 
 
 @dataclass(frozen=True)
@@ -88,31 +88,73 @@ def bin_points(xyz, ring, config: SensorConfig) -> ScanGrid:
     return ScanGrid(config=config, ranges=out)
 
 
+_STAGE_OF = {"valid_bits": "mesh", "frame_scan": "mesh", "tile": "normals", "tile_cc": "segment",
+             "merge": "segment", "labels_backfill": "backfill", "prune_apply": "backfill"}
+
+
 def run_pipeline(scan: ScanGrid, cfg: PipelineConfig, interval: int | None = None) -> PipelineResult:
-    """GPU run_pipeline (reference pipeline.py:47-70)."""
+    """GPU run_pipeline (reference pipeline.py:47-70): ONE upload of the range
+    grid, ONE fused C-ABI call (lseg_run_scans: valid bits -> mesh + fp64
+    normals + pass masks -> components -> backfill -> prune, no host sync in
+    between), ONE download of mesh, normals and labels.  The reference's
+    stage timings come from the library's per-kernel CUDA events: mesh = node
+    numbering, normals = the tile kernel (which also emits the mesh slots),
+    segment = tile components + border merge, backfill = labels + backfill +
+    pruning."""
     interval = cfg.interval if interval is None else int(interval)
-    _lib.lib()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-    ev[0].record()
-    mesh = build_mesh(scan, interval)
-    ev[1].record()
-    n64, _, mask = estimate_normals_device(scan, mesh)
-    ev[2].record()
-    node_labels, _ = segment_device(mesh, n64, mask, cfg.segmenter)
-    ev[3].record()
-    ranges = scan.device_ranges()
-    filled = backfill_device(scan.config, ranges.unsqueeze(0), node_labels)
-    labels = prune_small_device(filled, cfg.segmenter.min_segment_size, mesh.rings * mesh.kept_steps.size + 1)
-    ev[4].record()
-    torch.cuda.synchronize()
-    n = mesh.n_nodes
-    m = mask[0, :n].bool().cpu().numpy()
-    vals = n64[0, :n].cpu().numpy()
+    kept = subsample_steps(scan.config, interval)  # ValueError contract
+    L = _lib.lib()
+    conf = scan.config
+    R, S, Sk = conf.rings, conf.azimuth_steps, kept.size
+    cap = R * Sk
+    dev = torch.device("cuda")
+    _, sn = device_tables(conf, dev)
+    seg = cfg.segmenter
+    key = (R, S, interval)
+    bufs = _SCAN_BUFS.get(key)
+    if bufs is None:
+        wsb = _lib.workspace_bytes(1, R, S, interval)
+        bufs = {"ws": torch.empty(wsb, dtype=torch.uint8, device=dev), "wsb": wsb,
+                "ranges": torch.empty((1, R, S), dtype=torch.float64, device=dev),
+                "node_ids": torch.empty((1, R, Sk), dtype=torch.int32, device=dev),
+                "neighbors": torch.empty((1, cap, 6), dtype=torch.int32, device=dev),
+                "n64": torch.empty((1, cap, 3), dtype=torch.float64, device=dev),
+                "nmask": torch.empty((1, cap), dtype=torch.uint8, device=dev),
+                "labels": torch.empty((1, R, S), dtype=torch.int32, device=dev),
+                "counts": torch.empty(2, dtype=torch.int32, device=dev)}
+        _SCAN_BUFS.clear()  # keep one shape's buffers
+        _SCAN_BUFS[key] = bufs
+    b = bufs
+    host = torch.from_numpy(np.ascontiguousarray(scan.ranges, dtype=np.float64)).view(1, R, S)
+    _lib.profile_begin()
+    b["ranges"].copy_(host, non_blocking=False)
+    _lib.check(L.lseg_run_scans(sn, 1, interval, _lib.thresholds_arg(seg.thresholds), int(seg.min_segment_size),
+                                _lib.ptr(b["ranges"]), _lib.ptr(b["node_ids"]), _lib.ptr(b["neighbors"]),
+                                _lib.ptr(b["n64"]), _lib.ptr(b["nmask"]), None, _lib.ptr(b["labels"]),
+                                _lib.ptr(b["counts"][:1]), _lib.ptr(b["counts"][1:]), _lib.ptr(b["ws"]), b["wsb"],
+                                _lib.stream_ptr()))
+    stages = _lib.profile_end()
+    # one synchronising download of everything (node count first decides the slices)
+    node_ids = b["node_ids"][0].cpu().numpy()
+    valid = node_ids >= 0
+    n = int(valid.sum())
+    labels = b["labels"][0].cpu().numpy()
+    nb = b["neighbors"][0, :n].cpu().numpy()
+    m = b["nmask"][0, :n].cpu().numpy().astype(bool)
+    vals = b["n64"][0, :n].cpu().numpy()
     vals[~m] = np.nan
-    t = [ev[0].elapsed_time(ev[i]) for i in range(1, 5)]
-    timings = {"mesh": t[0], "normals": t[1] - t[0], "segment": t[2] - t[1], "backfill": t[3] - t[2], "total": t[3]}
-    return PipelineResult(labels=labels[0].cpu().numpy(), normals=NormalMap(values=vals, mask=m), mesh=mesh,
-                          timings_ms=timings)
+    rr, pos = np.nonzero(valid)
+    mesh = Mesh(rings=R, full_steps=S, interval=interval, kept_steps=kept, node_rings=rr.astype(np.int32),
+                node_steps=kept[pos].astype(np.int64), node_ids=node_ids, neighbors=nb)
+    timings = {"mesh": 0.0, "normals": 0.0, "segment": 0.0, "backfill": 0.0}
+    for name, (ms, _) in stages.items():
+        if name in _STAGE_OF:
+            timings[_STAGE_OF[name]] += ms
+    timings["total"] = sum(timings.values())
+    return PipelineResult(labels=labels, normals=NormalMap(values=vals, mask=m), mesh=mesh, timings_ms=timings)
+
+
+_SCAN_BUFS: dict = {}
 
 
 class BatchPipeline:
@@ -125,7 +167,7 @@ class BatchPipeline:
 
     def __init__(self, config: SensorConfig, interval: int, segmenter: SegmenterConfig | None = None,
                  frames: int = 1, device=None, keep_node_labels: bool = False, streams: int = 1,
-                 chunk_frames: int | None = None, normals: str = "exact"):
+                 chunk_frames: int | None = None, normals: str = "exact", keep_node_ids: bool = True):
         self.L = _lib.lib()
         if normals not in ("certified", "exact"):
             raise ValueError("normals must be 'certified' or 'exact'")
@@ -147,7 +189,9 @@ class BatchPipeline:
         _, self.sn = device_tables(config, dev)
         self.thr = _lib.thresholds_arg(self.seg.thresholds)
         self.ranges = torch.empty((F, R, S), dtype=torch.float64, device=dev)
-        self.node_ids = torch.empty((F, R, self.Sk), dtype=torch.int32, device=dev)
+        # node ids (F,R,S') are optional: derivable from the valid bits, and
+        # 4 B per kept cell of HBM writes the batched path does not need
+        self.node_ids = torch.empty((F, R, self.Sk), dtype=torch.int32, device=dev) if keep_node_ids else None
         self.neighbors = torch.empty((F, self.cap, 6), dtype=torch.int32, device=dev)
         self.normals = torch.empty((F, self.cap, 3), dtype=torch.float32, device=dev)
         self.nmask = torch.empty((F, self.cap), dtype=torch.uint8, device=dev)
@@ -241,7 +285,8 @@ class BatchPipeline:
         """Host copies of frame f's outputs (reference-shaped)."""
         n = int(self.n_nodes[f].item())
         m = self.nmask[f, :n].bool().cpu().numpy()
-        out = {"ranges": self.ranges[f].cpu().numpy(), "node_ids": self.node_ids[f].cpu().numpy(),
+        out = {"ranges": self.ranges[f].cpu().numpy(),
+               "node_ids": None if self.node_ids is None else self.node_ids[f].cpu().numpy(),
                "neighbors": self.neighbors[f, :n].cpu().numpy(), "normals": self.normals[f, :n].cpu().numpy(),
                "mask": m, "labels": self.labels[f].cpu().numpy(), "n_labels": int(self.n_labels[f].item())}
         if self.node_labels is not None:
@@ -265,6 +310,20 @@ def ring_segments(ring, offsets, rings: int):
     return out
 
 
+def host_ring_segments(ring_h, offsets_h, rings: int, f0: int, f1: int):
+    """(f1-f0, rings+1) int64 segment table of frames [f0, f1) of ring-major
+    host points from their int32 ring ids: one binary search per ring
+    boundary per frame on the host (the per-point ring ids stay on the host)."""
+    r = ring_h.numpy() if isinstance(ring_h, torch.Tensor) else np.asarray(ring_h)
+    o = offsets_h.numpy() if isinstance(offsets_h, torch.Tensor) else np.asarray(offsets_h)
+    q = np.arange(rings + 1, dtype=r.dtype)
+    out = np.empty((f1 - f0, rings + 1), dtype=np.int64)
+    for f in range(f0, f1):
+        a, b = int(o[f]), int(o[f + 1])
+        out[f - f0] = np.searchsorted(r[a:b], q) + a
+    return torch.from_numpy(out)
+
+
 class StreamingPipeline:
     """Host-to-host batched hot path with copy/compute overlap.
 
@@ -283,10 +342,15 @@ class StreamingPipeline:
         self.taper_min = max(1, self.cf // 8)
         R, S = config.rings, config.azimuth_steps
         self.maxp = int(max_chunk_points or self.cf * R * S)
-        self.bps = [BatchPipeline(config, interval, segmenter, frames=self.cf, device=self.device, normals=normals)
-                    for _ in range(2)]
+        self.bps = [BatchPipeline(config, interval, segmenter, frames=self.cf, device=self.device, normals=normals,
+                                  keep_node_ids=False) for _ in range(2)]
         self.xyz = [torch.empty((self.maxp, 3), dtype=torch.float32, device=self.device) for _ in range(2)]
-        self.segments = ring_dtype == "segments"  # ring-major points + (F, R+1) ring segment table
+        # "segments": the caller passes the (F, R+1) ring segment table of
+        # ring-major points; "segments_from_ids": the caller passes int32 ring
+        # ids and each chunk's table is computed on the host inside run_host
+        # (binary searches of the ring boundaries, ring-major input assumed)
+        self.ids_to_segments = ring_dtype == "segments_from_ids"
+        self.segments = ring_dtype in ("segments", "segments_from_ids")
         self.R = R
         self.ring = [torch.empty((self.cf, R + 1), dtype=torch.int64, device=self.device) if self.segments
                      else torch.empty(self.maxp, dtype=ring_dtype, device=self.device) for _ in range(2)]
@@ -297,8 +361,9 @@ class StreamingPipeline:
         self.computed = [torch.cuda.Event() for _ in range(2)]
 
     def run_host(self, xyz_h, ring_h, offsets_h, labels_h):
-        """xyz_h (P,3) f32, ring_h (P,) i32 / u8 (or, with ring_dtype="segments",
-        the (F, R+1) i64 table of ``ring_segments``), offsets_h (F+1,) i64 host
+        """xyz_h (P,3) f32, ring_h (P,) i32 / u8 (with ring_dtype="segments",
+        the (F, R+1) i64 table of ``ring_segments``; with "segments_from_ids",
+        (P,) i32 ring ids converted per chunk on the host), offsets_h (F+1,) i64 host
         tensors (pinned); labels_h (F,R,S) i32 pinned output.  Enqueues everything and
         returns; synchronise on the current stream to wait."""
         F = offsets_h.numel() - 1
@@ -330,7 +395,10 @@ class StreamingPipeline:
                 self.xyz[b][: p1 - p0].copy_(xyz_h[p0:p1], non_blocking=True)
                 loc = offsets_h[f0:f1 + 1] - p0
                 if self.segments:  # chunk-relative segment table, empty frames as padding
-                    seg = ring_h[f0:f1] - p0
+                    if self.ids_to_segments:
+                        seg = host_ring_segments(ring_h, offsets_h, self.R, f0, f1) - p0
+                    else:
+                        seg = ring_h[f0:f1] - p0
                     if nf < self.cf:
                         seg = torch.cat([seg, seg.new_full((self.cf - nf, self.R + 1), int(loc[-1]))])
                     self.ring[b].copy_(seg, non_blocking=True)

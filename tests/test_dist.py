@@ -1,9 +1,14 @@
-"""Multi-rank frame sharding on CPU with gloo (world_size 2): every frame is
-owned exactly once, and the reduced totals equal a single-process run."""
+"""Multi-rank frame sharding on CPU with gloo (world_size 2), through the
+exact functions bench.py runs per rank (dist.rank_batch for the rank's frames,
+dist.reduce_run for the run's single collective): every frame of the batch
+is owned exactly once, each rank's frames are the batch's frames, and the
+reduced totals equal a single-process run."""
 
 import os
 import socket
 
+import pytest
+import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
@@ -19,6 +24,14 @@ def test_shard_covers_every_frame_once():
                 assert n >= 0
                 owned += list(range(a, a + n))
             assert owned == list(range(F))
+            assert max(D.shard(F, G, r)[1] for r in range(G)) == -(-F // G)
+
+
+def test_rank_frames_strong_and_weak():
+    assert [D.rank_frames(512, 8, r) for r in range(8)] == [(64 * r, 64) for r in range(8)]
+    assert [D.rank_frames(512, 2, r, "weak") for r in range(2)] == [(0, 512), (512, 512)]
+    with pytest.raises(ValueError):
+        D.rank_frames(4, 2, 0, "bogus")
 
 
 def _free_port():
@@ -29,51 +42,37 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, frames, out):
+def _worker(rank, world, port, frames, scaling, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    import sys
-    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
-    import lidarseg_oracle as O
     from paper_2005_02704_b200 import synth
     shape = synth.CONFIGS["vlp16"]
-    first, n = D.shard(frames, world, rank)
-    pts = segs = 0
-    if n:
-        xyz, ring, off = synth.make_batch(shape, frames=n, seed=3, first_frame=first)
-        for f in range(n):
-            a, b = int(off[f]), int(off[f + 1])
-            res = O.run_from_points(xyz[a:b].numpy(), ring[a:b].numpy(), shape.elevations, shape.steps, 5,
-                                    shape.r_min, shape.r_max)
-            pts += b - a
-            segs += int(res["labels"].max())
-    tot = D.reduce_run(pts, n, segs, elapsed_ms=10.0 * (rank + 1))
-    out[rank] = (tot["points"], tot["frames"], tot["segments"], tot["elapsed_ms"])
+    first, n, xyz, ring, off = D.rank_batch(shape, frames, world, rank, scaling, seed=3)
+    # stand-in for the per-frame work: points and a per-frame checksum of the
+    # rank's own inputs (the GPU pipeline itself is covered by the -m gpu tests)
+    sums = [float(xyz[int(off[f]):int(off[f + 1])].double().sum()) for f in range(n)]
+    tot = D.reduce_run(int(xyz.shape[0]), n, len(sums), elapsed_ms=10.0 * (rank + 1))
+    out[rank] = {"first": first, "n": n, "points": int(xyz.shape[0]), "sums": sums,
+                 "tot": (tot["points"], tot["frames"], tot["segments"], tot["elapsed_ms"])}
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_two_rank_gloo_totals_match_single_process():
-    frames = 3
+@pytest.mark.parametrize("scaling,frames", [("strong", 5), ("weak", 2)])
+def test_two_rank_gloo_partition_and_totals(scaling, frames):
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(2, _free_port(), frames, out), nprocs=2, join=True)
-    single = {}
-    _worker_single = None  # noqa: F841
-    import sys
-    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
-    import lidarseg_oracle as O
+    mp.spawn(_worker, args=(2, _free_port(), frames, scaling, out), nprocs=2, join=True)
     from paper_2005_02704_b200 import synth
     shape = synth.CONFIGS["vlp16"]
-    xyz, ring, off = synth.make_batch(shape, frames=frames, seed=3)
-    pts = segs = 0
-    for f in range(frames):
-        a, b = int(off[f]), int(off[f + 1])
-        res = O.run_from_points(xyz[a:b].numpy(), ring[a:b].numpy(), shape.elevations, shape.steps, 5,
-                                shape.r_min, shape.r_max)
-        pts += b - a
-        segs += int(res["labels"].max())
-    single = (pts, frames, segs)
-    assert out[0] == out[1]
-    assert out[0][:3] == single
-    assert out[0][3] == 20.0  # max over ranks
+    total = frames if scaling == "strong" else 2 * frames
+    xyz, ring, off = synth.make_batch(shape, frames=total, seed=3)
+    want_sums = [float(xyz[int(off[f]):int(off[f + 1])].double().sum()) for f in range(total)]
+    r0, r1 = out[0], out[1]
+    if scaling == "strong":
+        assert (r0["first"], r0["n"], r1["first"], r1["n"]) == (0, 3, 3, 2)
+    else:
+        assert (r0["first"], r0["n"], r1["first"], r1["n"]) == (0, frames, frames, frames)
+    # each frame owned once, and each rank's frames are exactly the batch's frames
+    assert r0["sums"] + r1["sums"] == want_sums
+    assert r0["tot"] == r1["tot"] == (int(xyz.shape[0]), total, total, 20.0)  # sums; max elapsed over ranks

@@ -102,3 +102,41 @@ def test_edge_evaluator(oracle, name):
         np.testing.assert_array_equal(oracle.extract_edges(g["truth"]), g["te"])
         np.testing.assert_array_equal(oracle.dilate_chebyshev(g["te"], r), g["dil"])
     np.testing.assert_allclose(oracle.edge_prf(g["pred"], g["truth"], r), g["prf"], rtol=0, atol=0)
+
+
+SCALE = golden_names("scale_")
+
+
+@pytest.mark.parametrize("name", SCALE)
+def test_oracle_matches_reference_at_bench_scale(oracle, name):
+    """The oracle against reference outputs on full bench-shape frames
+    (HDL-64 batch frame at k = 1/5/10/15, OS1-128, the 256 x 4096 stress
+    frame): mesh, fp64 normals (digest, bit-exact), segment() labels and
+    final labels."""
+    from golden.packing import digest, near_threshold_edges, normals_digest, unpack_ranges
+    g = load_golden(name)
+    ranges = unpack_ranges(g)
+    for k in [int(v) for v in g["intervals"]]:
+        mesh = oracle.build_mesh(ranges, g["elev"], k, float(g["r_min"]), float(g["r_max"]))
+        assert mesh["neighbors"].shape[0] == int(g[f"k{k}_n_nodes"])
+        assert digest(mesh["node_ids"].astype(np.int32)) == str(g[f"k{k}_node_ids"])
+        assert digest(mesh["neighbors"].astype(np.int32)) == str(g[f"k{k}_neighbors"])
+        vals, mask = oracle.estimate_normals(ranges, g["elev"], mesh)
+        assert normals_digest(vals, mask, np.float64) == str(g[f"k{k}_n64"])
+        dense = oracle.segment(mesh, vals, mask, g["thr"])
+        assert digest(dense.astype(np.int32)) == str(g[f"k{k}_node_dense_digest"])
+        valid = oracle.valid_mask(ranges, float(g["r_min"]), float(g["r_max"]))
+        labels = oracle.prune_small(oracle.backfill(valid, dense), int(g["mseg"]))
+        np.testing.assert_array_equal(labels, g[f"k{k}_labels"])
+        assert near_threshold_edges(mesh["neighbors"], vals, mask, g["thr"]) == (int(g[f"k{k}_e_near"]),
+                                                                                 int(g[f"k{k}_e_fwd"]))
+
+
+def test_range_packing_roundtrip():
+    from golden.packing import pack_ranges, unpack_ranges
+    rng = np.random.default_rng(0)
+    r = rng.uniform(0.5, 120.0, size=(7, 33))
+    r[rng.random(r.shape) < 0.3] = np.nan
+    back = unpack_ranges(pack_ranges(r))
+    np.testing.assert_array_equal(np.isnan(back), np.isnan(r))
+    np.testing.assert_array_equal(back[~np.isnan(r)], r[~np.isnan(r)])
