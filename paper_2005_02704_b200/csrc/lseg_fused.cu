@@ -92,26 +92,6 @@ __device__ __forceinline__ bool edge_internal(int r, int c, int s, int Sk) {
   return (tr / TR == r / TR) && (tc / TC == c / TC);
 }
 
-// Column (0..63) of the run start of tile column x in a row with run starts
-// `st` (x must hold a normal, i.e. lie inside a run).
-__device__ __forceinline__ int run_col(unsigned long long st, int x) {
-  const unsigned long long m = st & (x == 63 ? ~0ull : ((2ull << x) - 1ull));
-  return 63 - __clzll((long long)m);
-}
-
-// Frame-local kept-cell index of the run start of kept cell (r, c), or -1 if
-// the cell has no normal; masks_f = the frame's pass masks.
-template <int TR, int TC>
-__device__ __forceinline__ int run_start_of(const Shape& sh, const unsigned long long* __restrict__ masks_f,
-                                            int tilesC, int r, int c) {
-  const int tr = r / TR, tc = c / TC, y = r - tr * TR, x = c - tc * TC;
-  const unsigned long long* m = masks_f + ((int64_t)tr * tilesC + tc) * (TR * 5) + y * 5;
-  const unsigned long long HS = __ldg(m + 3);
-  if (!((HS >> x) & 1ull)) return -1;
-  const unsigned long long H = __ldg(m);
-  return r * sh.Sk + tc * TC + run_col(HS & ~(H << 1), x);
-}
-
 // Border-normal store of one frame: for each tile row, its first and last
 // ring rows (all S' columns), then for each tile column its first and last
 // columns (all R rows); 3 doubles per cell, so every write run is contiguous.
@@ -1021,11 +1001,10 @@ __global__ void __launch_bounds__(T, LSEG_CERT_MINB) k_tile_cert(
 template <int TR, int TC>
 __device__ __forceinline__ void merge_cert_frame(const lseg_sensor& sn, const Shape& sh, const double* ranges,
                                                  const uint32_t* vbits, const float4* bn4, const CertParams& cp,
-                                                 const unsigned long long* masks, int32_t* parent, int32_t* unc,
-                                                 int32_t* fscal, int f, int u0, int ustep, bool overflow_pass) {
+                                                 int32_t* parent, int32_t* unc, int32_t* fscal, int f, int u0,
+                                                 int ustep, bool overflow_pass) {
   const int nbr = (sh.R + TR - 1) / TR;
   const int nbc = (sh.Sk + TC - 1) / TC;
-  const unsigned long long* mf = masks + (int64_t)f * nbr * nbc * (TR * 5);
   const int per = nbr * sh.Sk + nbc * sh.R;
   const int64_t capp = sh.cap / 2;  // undecided-list capacity (pairs) per frame
   int32_t* par = parent + (int64_t)f * sh.cap;
@@ -1042,9 +1021,9 @@ __device__ __forceinline__ void merge_cert_frame(const lseg_sensor& sn, const Sh
       c = min(bc * TC + TC - 1, sh.Sk - 1);
       r = v - bc * sh.R;
     }
-    const int p = run_start_of<TR, TC>(sh, mf, nbc, r, c);
-    if (p < 0) continue;  // no normal
+    const int p = r * sh.Sk + c;
     const int pp = __ldcg(par + p);
+    if (pp < 0) continue;  // no normal
     const int tr = r / TR;
     const bool last_row = (r == min(tr * TR + TR - 1, sh.R - 1));
 #pragma unroll
@@ -1052,9 +1031,9 @@ __device__ __forceinline__ void merge_cert_frame(const lseg_sensor& sn, const Sh
       if (r + slot_dr(s) >= sh.R) continue;
       if (edge_internal<TR, TC>(r, c, s, sh.Sk)) continue;
       const int rq = r + slot_dr(s), cq = wrapc(c + slot_dc(s), sh.Sk);
-      const int q = run_start_of<TR, TC>(sh, mf, nbc, rq, cq);
-      if (q < 0) continue;
+      const int q = rq * sh.Sk + cq;
       const int pq = __ldcg(par + q);
+      if (pq < 0) continue;
       float4 a, bq;
       if (slot_dr(s) == 1 && last_row) {
         a = __ldcg(bn + bn4_row(sh, 2 * tr + 1, c));
@@ -1074,9 +1053,9 @@ __device__ __forceinline__ void merge_cert_frame(const lseg_sensor& sn, const Sh
           d = (ha && hq && normals_pass(na, nq, cp.t[0], cp.t[1], cp.t[2])) ? 1 : 0;
         } else {
           const int idx = atomicAdd(fscal + f * 4 + 2, 1);
-          if (idx < capp) {  // the cells (for their exact normals) -- run starts are recomputed
-            unc[(int64_t)f * sh.cap + 2 * idx] = r * sh.Sk + c;
-            unc[(int64_t)f * sh.cap + 2 * idx + 1] = rq * sh.Sk + cq;
+          if (idx < capp) {
+            unc[(int64_t)f * sh.cap + 2 * idx] = p;
+            unc[(int64_t)f * sh.cap + 2 * idx + 1] = q;
           }
         }
       }
@@ -1088,9 +1067,8 @@ __device__ __forceinline__ void merge_cert_frame(const lseg_sensor& sn, const Sh
 template <int TR, int TC>
 __global__ void k_merge_cert(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
                              const uint32_t* __restrict__ vbits, const float4* __restrict__ bn4, CertParams cp,
-                             const unsigned long long* __restrict__ masks, int32_t* __restrict__ parent,
-                             int32_t* __restrict__ unc, int32_t* __restrict__ fscal) {
-  merge_cert_frame<TR, TC>(sn, sh, ranges, vbits, bn4, cp, masks, parent, unc, fscal, blockIdx.y,
+                             int32_t* __restrict__ parent, int32_t* __restrict__ unc, int32_t* __restrict__ fscal) {
+  merge_cert_frame<TR, TC>(sn, sh, ranges, vbits, bn4, cp, parent, unc, fscal, blockIdx.y,
                            blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, false);
 }
 
@@ -1098,18 +1076,16 @@ __global__ void k_merge_cert(lseg_sensor sn, Shape sh, const double* __restrict_
 template <int TR, int TC>
 __global__ void k_merge_exact(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
                               const uint32_t* __restrict__ vbits, const float4* __restrict__ bn4, CertParams cp,
-                              const unsigned long long* __restrict__ masks, int32_t* __restrict__ parent,
-                              const int32_t* __restrict__ unc, int32_t* __restrict__ fscal) {
+                              int32_t* __restrict__ parent, const int32_t* __restrict__ unc,
+                              int32_t* __restrict__ fscal) {
   const int f = blockIdx.y;
   const int n = fscal[f * 4 + 2];
   if (n == 0) return;
   if (n > sh.cap / 2) {  // list overflowed: redo the frame's border edges inline
-    merge_cert_frame<TR, TC>(sn, sh, ranges, vbits, bn4, cp, masks, parent, nullptr, fscal, f, threadIdx.x,
-                             blockDim.x, true);
+    merge_cert_frame<TR, TC>(sn, sh, ranges, vbits, bn4, cp, parent, nullptr, fscal, f, threadIdx.x, blockDim.x,
+                             true);
     return;
   }
-  const int nbc = (sh.Sk + TC - 1) / TC;
-  const unsigned long long* mf = masks + (int64_t)f * ((sh.R + TR - 1) / TR) * nbc * (TR * 5);
   const double* rf = ranges + (int64_t)f * sh.R * sh.S;
   const uint32_t* vbf = vbits + (int64_t)f * sh.R * sh.Wk;
   int32_t* par = parent + (int64_t)f * sh.cap;
@@ -1119,147 +1095,199 @@ __global__ void k_merge_exact(lseg_sensor sn, Shape sh, const double* __restrict
     double na[3], nq[3];
     const bool ha = exact_normal_at(sn, sh, rf, vbf, r, c, na);
     const bool hq = exact_normal_at(sn, sh, rf, vbf, rq, cq, nq);
-    if (ha && hq && normals_pass(na, nq, cp.t[0], cp.t[1], cp.t[2]))
-      uf_union(par, run_start_of<TR, TC>(sh, mf, nbc, r, c), run_start_of<TR, TC>(sh, mf, nbc, rq, cq));
+    if (ha && hq && normals_pass(na, nq, cp.t[0], cp.t[1], cp.t[2])) uf_union(par, p, q);
   }
 }
 
-// ---------------------------------------------------------------- tile components (run level)
-// Runs: maximal horizontal chains of a tile row's passing H edges.  A cell
-// starts a run iff it has a normal and the edge from its left neighbour does
-// not pass: starts = HS & ~(H << 1).  Every cell's tile-local component is
-// its run's, so components are computed over runs only and the per-cell
-// tile-local root is never stored: parent[run start] = root, and a cell's run
-// start comes from its row's H / HS masks (run_start_of).
+// Tile-local connected components from the tile's pass masks (the body of
+// k_tile_cc, one small CTA per tile): each node's parent starts as the first
+// cell of its horizontal run (bit arithmetic); vertical / diagonal edges --
+// minus those whose parallel edge one column to the left already joins the
+// same two runs -- join runs by union-find in shared memory; each
+// labelled cell gets parent[cell] = minimum cell of its tile-local component
+// (-1 without a normal).
+template <int TR, int TC, int T>
+__device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int c0, int TRe, int TCe,
+                                             const unsigned long long* s_m, int* s_par, int32_t* __restrict__ parent,
+                                             uint32_t* __restrict__ lroots, int32_t* __restrict__ hist, int64_t K) {
+  constexpr int NT = TR * TC;
+  // run starts: parent of every cell = first cell of its horizontal run
+  for (int e = threadIdx.x; e < NT; e += T) {
+    const int y = e / TC, x = e - y * TC;
+    const unsigned long long Z = ~s_m[y * 5] & ((1ull << x) - 1ull);
+    s_par[e] = y * TC + (Z ? 64 - __clzll((long long)Z) : 0);
+  }
+  __syncthreads();
+  // vertical / diagonal unions: edges whose parallel edge one column to the
+  // left already joins the same two runs are dropped with 64-bit mask
+  // arithmetic (one thread per row pair), the rest are unioned cell-parallel
+  __shared__ unsigned long long s_U[TR * 2];
+  for (int y = threadIdx.x; y < TR; y += T) {
+    unsigned long long U0 = 0, U1 = 0;
+    if (y + 1 < TRe) {
+      const unsigned long long Hy = s_m[y * 5], V0 = s_m[y * 5 + 1], V1 = s_m[y * 5 + 2];
+      const unsigned long long Hn = s_m[(y + 1) * 5];
+      U0 = V0 & ~((Hy << 1) & (Hn << 1) & (V0 << 1));
+      U1 = V1 & ~((V0 & Hn) | ((Hy << 1) & Hn & (V1 << 1)));
+    }
+    s_U[2 * y] = U0;
+    s_U[2 * y + 1] = U1;
+  }
+  __syncthreads();
+  // Union-find over runs: labels live at run starts (every other cell keeps
+  // s_par = its run start throughout).  The tile's run-to-run edges are
+  // gathered into one dense shared-memory list (packed per thread first as
+  // a | b0 << 10 | b1 << 20 | valid bits << 30, 10-bit tile cell indices);
+  // all threads then union them lock-free (atomicCAS, larger root hooked
+  // under the smaller, so each root is its component's minimum run start)
+  // and compress the run starts -- two barriers, no rounds.
+  static_assert(NT <= 1024, "10-bit cell indices");
+  constexpr int NJ = (NT + T - 1) / T;
+  static_assert(NT % T == 0 && TC % 32 == 0, "each warp step covers a 32-cell chunk of one row");
+  // each warp's edges as a dense list (a | b << 10) in its own shared-memory
+  // segment (appended without atomics), then unioned by the same warp:
+  // no block barrier between gathering and union.  At step j the warp's
+  // lanes are one 32-cell chunk of a row, so the chunk's edge bits are read
+  // straight from the row masks and chunks without edges are skipped.
+  constexpr int SEG = 2 * NT / (T / 32);  // >= 2 edges per cell of the warp (+ the wraps, see below)
+  __shared__ unsigned s_el[2 * NT];
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned* el = s_el + (threadIdx.x >> 5) * SEG;
+  int ne = 0;
+  unsigned starts = 0;  // which of this thread's cells are run starts
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int e0 = (threadIdx.x & ~31) + j * T;
+    const int y = e0 / TC, x0 = e0 - y * TC;
+    const int e = e0 + lane;
+    if (((~(s_m[y * 5] << 1) >> x0) >> lane) & 1ull) starts |= 1u << j;  // x = 0 or no run edge from x - 1
+    const unsigned c0 = (unsigned)(s_U[2 * y] >> x0), c1 = (unsigned)(s_U[2 * y + 1] >> x0);
+    if (c0 | c1) {  // warp-uniform
+      const unsigned a = (unsigned)s_par[e];
+      if ((c0 >> lane) & 1u) el[ne + __popc(c0 & lt)] = a | (unsigned)s_par[e + TC] << 10;
+      ne += __popc(c0);
+      if ((c1 >> lane) & 1u) el[ne + __popc(c1 & lt)] = a | (unsigned)s_par[e + TC + 1] << 10;
+      ne += __popc(c1);
+    }
+  }
+  // full-width column wrap (x = S'-1 -> 0), added by the last warp (fewest
+  // edges: it holds row TR-1)
+  if (threadIdx.x >= T - 32) {
+    const int y = lane;
+    const unsigned W = (y < TRe) ? (unsigned)s_m[y * 5 + 4] : 0u;
+    const bool w0 = W & 1u, w1 = (W & 2u) && (y + 1 < TRe);
+    const unsigned b0 = __ballot_sync(0xffffffffu, w0), b1 = __ballot_sync(0xffffffffu, w1);
+    if (b0 | b1) {
+      const unsigned a = (y < TRe) ? (unsigned)s_par[y * TC + TCe - 1] : 0u;
+      if (w0) el[ne + __popc(b0 & lt)] = a | (unsigned)(y * TC) << 10;
+      ne += __popc(b0);
+      // (y + 1) * TC is 1024 on the last row: only when that edge exists
+      if (w1) el[ne + __popc(b1 & lt)] = a | (unsigned)((y + 1) * TC) << 10;
+      ne += __popc(b1);
+    }
+  }
+  __syncwarp();
+  const int any_edge = __syncthreads_or(ne);
+  if (any_edge) {
+    // lock-free union-find over the run-start labels (larger root hooked
+    // under the smaller: root = component minimum; path halving on the way),
+    // then full compression at run starts
+    auto find = [&](int x) -> int {  // with path halving: unions only
+      int p = s_par[x];
+      while (p != x) {
+        const int g = s_par[p];
+        if (g != p) s_par[x] = g;  // x is not a root: only ever points further up
+        x = p;
+        p = g;
+      }
+      return x;
+    };
+    // read-only find for the compression (a halving store there could
+    // overwrite a run start another thread has already compressed)
+    auto root = [&](int x) -> int {
+      int p = s_par[x];
+      while (p != x) {
+        x = p;
+        p = s_par[x];
+      }
+      return x;
+    };
+    for (int k = lane; k < ne; k += 32) {
+      const unsigned v = el[k];
+      int ra = find(v & 1023u), rb = find(v >> 10);
+      while (ra != rb) {
+        if (ra < rb) { const int t = ra; ra = rb; rb = t; }
+        const int old = atomicCAS(s_par + ra, ra, rb);
+        if (old == ra) break;
+        ra = find(old);
+        rb = find(rb);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+      if ((starts >> j) & 1u) s_par[threadIdx.x + j * T] = root(threadIdx.x + j * T);
+    __syncthreads();
+  }
+  // ... and give every labelled cell its run start's root; tile-local roots
+  // (cells that are their own root) also get a bit in `lroots`, so the global
+  // flatten only has to chase those
+  const int64_t nbase = (int64_t)f * sh.cap;
+  for (int e = threadIdx.x; e < NT; e += T) {  // NT is a multiple of T: whole warps
+    const int y = e / TC, x = e - y * TC;
+    const bool in = (y < TRe && x < TCe);
+    int pc = -1;
+    if (in && ((s_m[y * 5 + 3] >> x) & 1ull)) {
+      const int lr = s_par[s_par[e]];  // run start -> its label
+      pc = (r0 + lr / TC) * sh.Sk + c0 + lr % TC;
+    }
+    const int cell = (r0 + y) * sh.Sk + c0 + x;
+    if (in) parent[nbase + cell] = pc;
+    // histogram slot of every tile-local root zeroed here (a superset of the
+    // final roots k_labels_backfill counts into)
+    if (hist && in && pc == cell) hist[(int64_t)f * K + cell + 1] = 0;
+    const uint32_t b = __ballot_sync(0xffffffffu, in && pc == cell);
+    const int word = (c0 + x) >> 5;
+    if ((threadIdx.x & 31) == 0 && y < TRe && word < sh.Wk) lroots[((int64_t)f * sh.R + r0 + y) * sh.Wk + word] = b;
+  }
+}
 
-// One warp per (frame, TR x TC tile).  Lane y owns tile row y: it creates the
-// row's runs, then unions over the non-redundant vertical / diagonal edges of
-// rows (y, y+1) -- an edge is dropped when the parallel edge one column to
-// the left joins the same two runs -- and the column-wrap edges of
-// full-width tiles; lock-free union-find on the run starts in shared memory
-// (CAS, larger root hooked under the smaller, so the root is the component's
-// minimum cell, path halving).  Outputs per run: parent[run start] = its
-// tile-local root; per tile-local root: its lroots bit and a zeroed
-// histogram slot (a superset of the final roots, counted into later).
-// Work is O(runs + edges) per tile instead of O(cells).
-template <int TR, int TC, int WPB>
-__global__ void __launch_bounds__(32 * WPB) k_runs(Shape sh, const unsigned long long* __restrict__ masks,
-                                                   int32_t* __restrict__ parent, uint32_t* __restrict__ lroots,
-                                                   int32_t* __restrict__ hist, int64_t K, int64_t ntiles) {
-  static_assert(TR <= 32 && TC == 64, "one lane per tile row, 64-bit rows");
-  __shared__ int s_par[WPB][TR * TC];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t b = (int64_t)blockIdx.x * WPB + warp;
-  if (b >= ntiles) return;  // warp-uniform
+// Test hook (lseg_debug_tile_cc): the tile CC body on given pass masks, one
+// 16 x 64 tile per "frame" (tests/test_gpu_math.py checks it against a CPU
+// union-find over the same edges).
+template <int TR, int TC, int T>
+__global__ void k_tile_cc_dbg(Shape sh, const unsigned long long* __restrict__ masks, int32_t* parent,
+                              uint32_t* lroots) {
+  __shared__ int s_par[TR * TC];
+  __shared__ unsigned long long s_m[TR * 5];
+  const int f = blockIdx.x;
+  for (int j = threadIdx.x; j < TR * 5; j += T) s_m[j] = masks[(int64_t)f * TR * 5 + j];
+  __syncthreads();
+  tile_cc_body<TR, TC, T>(sh, f, 0, 0, TR, TC, s_m, s_par, parent, lroots, nullptr, 0);
+}
+void debug_tile_cc(int n, const unsigned long long* masks, int32_t* parent, uint32_t* lroots) {
+  const Shape sh = make_shape(n, TILE_R, TILE_C, 1);
+  k_tile_cc_dbg<TILE_R, TILE_C, 256><<<n, 256>>>(sh, masks, parent, lroots);
+}
+
+template <int TR, int TC, int T>
+__global__ void __launch_bounds__(T, 2048 / T) k_tile_cc(Shape sh, const unsigned long long* __restrict__ masks,
+                                               int32_t* __restrict__ parent, uint32_t* __restrict__ lroots,
+                                               int32_t* __restrict__ hist, int64_t K) {
+  __shared__ int s_par[TR * TC];
+  __shared__ unsigned long long s_m[TR * 5];
   const int tilesC = (sh.Sk + TC - 1) / TC;
   const int tilesR = (sh.R + TR - 1) / TR;
+  const int64_t b = blockIdx.x;
   const int f = (int)(b / ((int64_t)tilesR * tilesC));
   const int rem = (int)(b - (int64_t)f * tilesR * tilesC);
   const int r0 = (rem / tilesC) * TR, c0 = (rem % tilesC) * TC;
   const int TRe = min(TR, sh.R - r0), TCe = min(TC, sh.Sk - c0);
-  int* par = s_par[warp];
-  const unsigned long long* mt = masks + b * (TR * 5);
-  unsigned long long H = 0, V0 = 0, V1 = 0, HS = 0;
-  unsigned W = 0;
-  if (lane < TRe) {
-    H = __ldg(mt + lane * 5);
-    V0 = __ldg(mt + lane * 5 + 1);
-    V1 = __ldg(mt + lane * 5 + 2);
-    HS = __ldg(mt + lane * 5 + 3);
-    W = (unsigned)__ldg(mt + lane * 5 + 4);
-  }
-  const unsigned long long st = HS & ~(H << 1);
-  const unsigned long long Hn = __shfl_down_sync(0xffffffffu, H, 1);
-  const unsigned long long stn = __shfl_down_sync(0xffffffffu, st, 1);
-  const int yb = lane * TC;
-  for (unsigned long long m = st; m; m &= m - 1ull) {
-    const int x = __ffsll((long long)m) - 1;
-    par[yb + x] = yb + x;
-  }
-  __syncwarp();
-  auto find = [&](int x) -> int {  // path halving: a non-root only ever points further up
-    int p = par[x];
-    while (p != x) {
-      const int g = par[p];
-      if (g != p) par[x] = g;
-      x = p;
-      p = g;
-    }
-    return x;
-  };
-  auto unite = [&](int a, int c) {
-    int ra = find(a), rb = find(c);
-    while (ra != rb) {
-      if (ra < rb) { const int t = ra; ra = rb; rb = t; }
-      const int old = atomicCAS(par + ra, ra, rb);
-      if (old == ra) break;
-      ra = find(old);
-      rb = find(rb);
-    }
-  };
-  if (lane + 1 < TRe) {
-    const unsigned long long U0 = V0 & ~((H << 1) & (Hn << 1) & (V0 << 1));
-    const unsigned long long U1 = V1 & ~((V0 & Hn) | ((H << 1) & Hn & (V1 << 1)));
-    for (unsigned long long m = U0; m; m &= m - 1ull) {
-      const int x = __ffsll((long long)m) - 1;
-      unite(yb + run_col(st, x), yb + TC + run_col(stn, x));
-    }
-    for (unsigned long long m = U1; m; m &= m - 1ull) {
-      const int x = __ffsll((long long)m) - 1;
-      unite(yb + run_col(st, x), yb + TC + run_col(stn, x + 1));
-    }
-  }
-  // column wrap of a full-width tile (S' <= TC): (y, S'-1) -> (y, 0) and
-  // (y, S'-1) -> (y+1, 0); column 0 always starts its run
-  if (lane < TRe && (W & 1u)) unite(yb + run_col(st, TCe - 1), yb);
-  if (lane + 1 < TRe && (W & 2u)) unite(yb + run_col(st, TCe - 1), yb + TC);
-  __syncwarp();
-  const int64_t nbase = (int64_t)f * sh.cap;
-  unsigned long long lr = 0;
-  for (unsigned long long m = st; m; m &= m - 1ull) {
-    const int x = __ffsll((long long)m) - 1;
-    int rt = yb + x, p = par[rt];
-    while (p != rt) {  // read-only root chase
-      rt = p;
-      p = par[rt];
-    }
-    const int ry = rt / TC;
-    const int root = (r0 + ry) * sh.Sk + c0 + (rt - ry * TC);
-    const int cell = (r0 + lane) * sh.Sk + c0 + x;
-    parent[nbase + cell] = root;
-    if (root == cell) {
-      lr |= 1ull << x;
-      if (hist) hist[(int64_t)f * K + cell + 1] = 0;
-    }
-  }
-  if (lane < TRe) {
-    uint32_t* lw = lroots + ((int64_t)f * sh.R + r0 + lane) * sh.Wk + (c0 >> 5);
-    lw[0] = (uint32_t)lr;
-    if ((c0 >> 5) + 1 < sh.Wk) lw[1] = (uint32_t)(lr >> 32);
-  }
-}
-
-// Test hook (lseg_debug_tile_cc): k_runs on given pass masks, one 16 x 64
-// tile per "frame", then every cell's tile-local root (-1 without a normal)
-// expanded from its run start (tests/test_gpu_math.py checks it against a CPU
-// union-find over the same edges).
-template <int TR, int TC>
-__global__ void k_runs_expand_dbg(Shape sh, const unsigned long long* __restrict__ masks,
-                                  const int32_t* __restrict__ par_runs, int32_t* __restrict__ parent) {
-  const int f = blockIdx.x;
-  for (int e = threadIdx.x; e < TR * TC; e += blockDim.x) {
-    const int y = e / TC, x = e - y * TC;
-    const int s = run_start_of<TR, TC>(sh, masks + (int64_t)f * TR * 5, 1, y, x);
-    parent[(int64_t)f * TR * TC + e] = s < 0 ? -1 : par_runs[(int64_t)f * sh.cap + s];
-  }
-}
-void debug_tile_cc(int n, const unsigned long long* masks, int32_t* parent, uint32_t* lroots) {
-  const Shape sh = make_shape(n, TILE_R, TILE_C, 1);
-  int32_t* tmp = nullptr;
-  cudaMalloc(&tmp, sizeof(int32_t) * (size_t)n * TILE_R * TILE_C);
-  k_runs<TILE_R, TILE_C, 4><<<(n + 3) / 4, 128>>>(sh, masks, tmp, lroots, nullptr, 0, n);
-  k_runs_expand_dbg<TILE_R, TILE_C><<<n, 256>>>(sh, masks, tmp, parent);
-  cudaFree(tmp);
+  const unsigned long long* mrow = masks + b * (TR * 5);
+  for (int j = threadIdx.x; j < TR * 5; j += T) s_m[j] = __ldg(mrow + j);
+  __syncthreads();
+  tile_cc_body<TR, TC, T>(sh, f, r0, c0, TRe, TCe, s_m, s_par, parent, lroots, hist, K);
 }
 
 // Global union over the forward edges that leave a tile.  Threads enumerate
@@ -1271,7 +1299,7 @@ void debug_tile_cc(int n, const unsigned long long* masks, int32_t* parent, uint
 // on the few large roots.
 template <int TR, int TC>
 __global__ void k_merge(Shape sh, const double* __restrict__ bnorm, double t0, double t1, double t2,
-                        const unsigned long long* __restrict__ masks, int32_t* __restrict__ parent) {
+                        int32_t* __restrict__ parent) {
   // blockIdx.y = frame; threads enumerate the frame's border cells
   const int f = blockIdx.y;
   const int nbr = (sh.R + TR - 1) / TR;
@@ -1279,13 +1307,11 @@ __global__ void k_merge(Shape sh, const double* __restrict__ bnorm, double t0, d
   const int per = nbr * sh.Sk + nbc * sh.R;
   int32_t* par = parent + (int64_t)f * sh.cap;
   const double* bn = bnorm + (int64_t)f * bn_frame(sh, TR, TC);
-  const int tilesC = (sh.Sk + TC - 1) / TC;
-  const unsigned long long* mf = masks + (int64_t)f * nbr * tilesC * (TR * 5);
   const int lane = threadIdx.x & 31;
   // warp-uniform trip count (the dedup below needs whole warps)
   for (int u0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); u0 < per; u0 += gridDim.x * blockDim.x) {
     const int u = u0 + lane;
-    int r = 0, c = 0, pp = -1, p = 0;
+    int r = 0, c = 0, pp = -1;
     if (u < per) {
       if (u < nbr * sh.Sk) {
         const int br = u / sh.Sk;
@@ -1297,9 +1323,9 @@ __global__ void k_merge(Shape sh, const double* __restrict__ bnorm, double t0, d
         c = min(bc * TC + TC - 1, sh.Sk - 1);
         r = v - bc * sh.R;
       }
-      p = run_start_of<TR, TC>(sh, mf, tilesC, r, c);  // -1: no normal
-      if (p >= 0) pp = __ldcg(par + p);
+      pp = __ldcg(par + r * sh.Sk + c);  // -1: no normal
     }
+    const int p = r * sh.Sk + c;
     const int tr = r / TR, tc = c / TC;
     const bool last_row = (r == min(tr * TR + TR - 1, sh.R - 1));
 #pragma unroll
@@ -1308,8 +1334,8 @@ __global__ void k_merge(Shape sh, const double* __restrict__ bnorm, double t0, d
       int q = 0, pq = -1;
       if (pp >= 0 && r + slot_dr(s) < sh.R && !edge_internal<TR, TC>(r, c, s, sh.Sk)) {
         const int rq = r + slot_dr(s), cq = wrapc(c + slot_dc(s), sh.Sk);
-        q = run_start_of<TR, TC>(sh, mf, tilesC, rq, cq);
-        if (q >= 0) pq = __ldcg(par + q);
+        q = rq * sh.Sk + cq;
+        pq = __ldcg(par + q);
         if (pq >= 0) {
           // an edge that crosses a tile-row boundary reads both normals from
           // the row border store, one that only crosses a column boundary
@@ -1506,7 +1532,6 @@ __global__ void __launch_bounds__(T, 2048 / T) k_labels_backfill(lseg_sensor sn,
                                                        const uint32_t* __restrict__ vbits,
                                                        const uint32_t* __restrict__ fbits,
                                                        const int32_t* __restrict__ parent,
-                                                       const unsigned long long* __restrict__ masks,
                                                        const uint32_t* __restrict__ rbits,
                                                        const int32_t* __restrict__ rpre,
                                                        int32_t* __restrict__ node_labels, int32_t* __restrict__ out,
@@ -1517,27 +1542,13 @@ __global__ void __launch_bounds__(T, 2048 / T) k_labels_backfill(lseg_sensor sn,
   const int S = sh.S, Sk = sh.Sk, k = sh.k, nwk = sh.Wk, nw = (S + 31) / 32;
   int* s_kv = s_dynrow;                                                 // per kept column
   uint32_t* s_kdm = reinterpret_cast<uint32_t*>(s_dynrow + nwk * 32);  // donor columns
-  const int tilesC = (sh.Sk + kTileC - 1) / kTileC;
-  // the row's run starts / normal bits per tile (k_tile's pass masks)
-  unsigned long long* s_st = reinterpret_cast<unsigned long long*>(s_dynrow + (nwk * 33 + 1) / 2 * 2);
-  unsigned long long* s_hs = s_st + tilesC;
   __shared__ int s_any;
   const int row = blockIdx.x;
   const int f = row / sh.R, i = row - f * sh.R;
-  {
-    const int tr = i / kTileR, y = i - tr * kTileR;
-    const unsigned long long* mr =
-        masks + ((int64_t)f * ((sh.R + kTileR - 1) / kTileR) + tr) * tilesC * (kTileR * 5) + y * 5;
-    for (int t = threadIdx.x; t < tilesC; t += T) {
-      const unsigned long long H = __ldg(mr + (int64_t)t * kTileR * 5), HS = __ldg(mr + (int64_t)t * kTileR * 5 + 3);
-      s_st[t] = HS & ~(H << 1);
-      s_hs[t] = HS;
-    }
-  }
   const uint32_t* vbr = vbits + (int64_t)row * sh.Wk;
   const uint32_t* fbr = fbits ? fbits + (int64_t)row * nw : nullptr;
   const int32_t* parf = parent + (int64_t)f * sh.cap;
-  const int rowc = i * sh.Sk;
+  const int32_t* par = parf + (int64_t)i * sh.Sk;
   const uint32_t* rbf = rbits + (int64_t)f * sh.R * sh.Wk;
   const int32_t* rpf = rpre + (int64_t)f * sh.R * sh.Wk;
   const int64_t rb = (int64_t)row * S;
@@ -1565,13 +1576,9 @@ __global__ void __launch_bounds__(T, 2048 / T) k_labels_backfill(lseg_sensor sn,
   for (int c0 = 0; c0 < nwk * 32; c0 += T * PF) {
     int pv[PF], lv[PF];
 #pragma unroll
-    for (int j = 0; j < PF; ++j) {  // tile-local root = parent of the cell's run start
+    for (int j = 0; j < PF; ++j) {
       const int c = c0 + threadIdx.x + j * T;
-      pv[j] = -1;
-      if (c < Sk) {
-        const int t = c / kTileC, x = c - t * kTileC;
-        if ((s_hs[t] >> x) & 1ull) pv[j] = __ldcg(parf + rowc + t * kTileC + run_col(s_st[t], x));
-      }
+      pv[j] = (c < Sk) ? __ldcg(par + c) : -1;  // tile-local root
     }
 #pragma unroll
     for (int j = 0; j < PF; ++j) lv[j] = pv[j] >= 0 ? __ldcg(parf + pv[j]) : 0;  // its parent: the final root
@@ -2105,13 +2112,6 @@ void launch_prune_fused(const Shape& sh, const Workspace& ws, int32_t min_size, 
 }
 
 // ---------------------------------------------------------------- launchers
-static void launch_runs(const Shape& sh, const Workspace& ws, int64_t nt, cudaStream_t st) {
-  constexpr int WPB = 4;  // tiles (warps) per CTA
-  k_runs<TILE_R, TILE_C, WPB><<<(unsigned)((nt + WPB - 1) / WPB), 32 * WPB, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots,
-                                                                                    ws.hist, ws.K, nt);
-  prof_mark("tile_cc", st);
-}
-
 void debug_phases(double* out) {
 #if LSEG_PHASES
   unsigned long long h[8];
@@ -2150,12 +2150,15 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
         sn, sh, ranges, ws.vbits, ws.wpre, cp, node_ids, neighbors, n32, nmask, ws.masks, bn4, ws.normals64, dbg_err,
         ws.fscal, n_labels);
     prof_mark("tile", st);
-    launch_runs(sh, ws, nt, st);
+    if (nt < 148 * 16)  // one-wave batches: 256 threads per tile for latency
+      k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
+    else
+      k_tile_cc<TILE_R, TILE_C, LSEG_CC_TBIG><<<(unsigned)nt, LSEG_CC_TBIG, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
+    prof_mark("tile_cc", st);
     k_merge_cert<TILE_R, TILE_C><<<dim3((per + mt - 1) / mt, sh.F), mt, 0, st>>>(sn, sh, ranges, ws.vbits, bn4, cp,
-                                                                                ws.masks, ws.parent, ws.rank,
-                                                                                ws.fscal);
-    k_merge_exact<TILE_R, TILE_C><<<dim3(1, sh.F), 128, 0, st>>>(sn, sh, ranges, ws.vbits, bn4, cp, ws.masks,
-                                                                 ws.parent, ws.rank, ws.fscal);
+                                                                                ws.parent, ws.rank, ws.fscal);
+    k_merge_exact<TILE_R, TILE_C><<<dim3(1, sh.F), 128, 0, st>>>(sn, sh, ranges, ws.vbits, bn4, cp, ws.parent,
+                                                                 ws.rank, ws.fscal);
     prof_mark("merge", st);
   } else {
   const size_t tsmem =
@@ -2166,9 +2169,13 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
                                                                   thr[2], node_ids, neighbors, n32, nmask, ws.masks,
                                                                   ws.bnorm, ws.parent, ws.lroots, n_labels, n64);
   prof_mark("tile", st);
-  launch_runs(sh, ws, nt, st);
+  if (nt < 148 * 16)  // one-wave batches: 256 threads per tile for latency
+    k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
+  else
+    k_tile_cc<TILE_R, TILE_C, LSEG_CC_TBIG><<<(unsigned)nt, LSEG_CC_TBIG, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
+  prof_mark("tile_cc", st);
   k_merge<TILE_R, TILE_C><<<dim3((per + mt - 1) / mt, sh.F), mt, 0, st>>>(
-      sh, ws.bnorm, thr[0], thr[1], thr[2], ws.masks, ws.parent);
+      sh, ws.bnorm, thr[0], thr[1], thr[2], ws.parent);
   prof_mark("merge", st);
   }
   const bool fold = !node_labels && LSEG_FOLD_FLATTEN;
@@ -2184,17 +2191,17 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
     }
   }
   // labels + backfill -> lab_tmp (+ histogram)
-  const size_t smem = sizeof(int) * (((size_t)sh.Wk * 33 + 1) / 2 * 2) + 16 * (size_t)tilesC;
+  const size_t smem = sizeof(int) * (size_t)sh.Wk * 33;
   const uint32_t* fb = (sh.k > 1 && fbits_valid) ? ws.fbits : nullptr;
   if (smem > 48 * 1024)
     for (auto fn : {k_labels_backfill<128>, k_labels_backfill<256>})
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if ((int64_t)sh.F * sh.R < 148 * 8)  // one-wave batches: 256 threads per row for latency
-    k_labels_backfill<256><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, ranges, ws.vbits, fb, ws.parent, ws.masks, ws.rbits,
+    k_labels_backfill<256><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits,
                                                            ws.rpre, node_labels, ws.lab_tmp, ws.hist, ws.K,
                                                            fold ? ws.rbits : nullptr, n_labels, ws.rcnt, ws.fscal + 3);
   else
-    k_labels_backfill<128><<<sh.F * sh.R, 128, smem, st>>>(sn, sh, ranges, ws.vbits, fb, ws.parent, ws.masks, ws.rbits,
+    k_labels_backfill<128><<<sh.F * sh.R, 128, smem, st>>>(sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits,
                                                            ws.rpre, node_labels, ws.lab_tmp, ws.hist, ws.K,
                                                            fold ? ws.rbits : nullptr, n_labels, ws.rcnt, ws.fscal + 3);
   prof_mark("labels_backfill", st);
