@@ -125,25 +125,29 @@ def run_pipeline(scan: ScanGrid, cfg: PipelineConfig, interval: int | None = Non
         _SCAN_BUFS.clear()  # keep one shape's buffers
         _SCAN_BUFS[key] = bufs
     b = bufs
-    host = torch.from_numpy(np.ascontiguousarray(scan.ranges, dtype=np.float64)).view(1, R, S)
+    b["ranges"].copy_(torch.from_numpy(np.array(scan.ranges, dtype=np.float64, copy=True)).view(1, R, S))
     _lib.profile_begin()
-    b["ranges"].copy_(host, non_blocking=False)
     _lib.check(L.lseg_run_scans(sn, 1, interval, _lib.thresholds_arg(seg.thresholds), int(seg.min_segment_size),
                                 _lib.ptr(b["ranges"]), _lib.ptr(b["node_ids"]), _lib.ptr(b["neighbors"]),
                                 _lib.ptr(b["n64"]), _lib.ptr(b["nmask"]), None, _lib.ptr(b["labels"]),
                                 _lib.ptr(b["counts"][:1]), _lib.ptr(b["counts"][1:]), _lib.ptr(b["ws"]), b["wsb"],
                                 _lib.stream_ptr()))
-    stages = _lib.profile_end()
-    # one synchronising download of everything (node count first decides the slices)
-    node_ids = b["node_ids"][0].cpu().numpy()
+    # every output downloaded asynchronously into fresh pinned host tensors
+    # (torch's caching host allocator: no pinning cost per call), one
+    # synchronisation; the returned arrays are views of those tensors
+    pin = lambda t: torch.empty(t.shape[1:], dtype=t.dtype, pin_memory=True).copy_(t[0], non_blocking=True)
+    h = {k: pin(b[k]) for k in ("node_ids", "labels", "neighbors", "n64", "nmask")}
+    stages = _lib.profile_end()  # synchronises on the last event (after the copies were enqueued)
+    torch.cuda.current_stream().synchronize()
+    node_ids = h["node_ids"].numpy()
     valid = node_ids >= 0
-    n = int(valid.sum())
-    labels = b["labels"][0].cpu().numpy()
-    nb = b["neighbors"][0, :n].cpu().numpy()
-    m = b["nmask"][0, :n].cpu().numpy().astype(bool)
-    vals = b["n64"][0, :n].cpu().numpy()
-    vals[~m] = np.nan
     rr, pos = np.nonzero(valid)
+    n = int(rr.size)
+    labels = h["labels"].numpy()
+    nb = h["neighbors"].numpy()[:n]
+    m = h["nmask"].numpy()[:n].astype(bool)
+    vals = h["n64"].numpy()[:n]
+    vals[~m] = np.nan
     mesh = Mesh(rings=R, full_steps=S, interval=interval, kept_steps=kept, node_rings=rr.astype(np.int32),
                 node_steps=kept[pos].astype(np.int64), node_ids=node_ids, neighbors=nb)
     timings = {"mesh": 0.0, "normals": 0.0, "segment": 0.0, "backfill": 0.0}
