@@ -202,6 +202,22 @@ int lseg_run_scans(const lseg_sensor* sensor, int32_t frames, int32_t interval, 
                    double* normals64, uint8_t* nmask, int32_t* node_labels, int32_t* labels, int32_t* n_nodes,
                    int32_t* n_labels, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- streaming mesh builder (reference MeshBuilder, mesh.py:139-170;
+ * streaming contract SPEC.md:200).  Columns are fed in sweep order; when
+ * kept column j arrives (its R ranges, device f64), the valid bits and
+ * per-ring ranks of column j are recorded and every slot of column j-1 is
+ * emitted (slots reference (ring, rank) pairs).  State: runcnt (R) i32,
+ * zeroed before column 0; colrank (R, kept) i32; slots (R, kept, 6) i32. */
+int lseg_mb_column(int32_t rings, int32_t kept, int32_t column, double r_min, double r_max, const double* ranges,
+                   int32_t* runcnt, int32_t* colrank, int32_t* slots, void* stream);
+
+/* Closes the wrap (slots of columns 0 and kept-1), scans the per-ring
+ * counts into row offsets (rowoff (R) i32) and resolves every slot to the
+ * reference's row-major node ids: node_ids (R, kept), neighbors
+ * (n_nodes, 6), n_nodes (1) -- identical to lseg_build_mesh on the grid. */
+int lseg_mb_finish(int32_t rings, int32_t kept, const int32_t* runcnt, const int32_t* colrank, int32_t* slots,
+                   int32_t* rowoff, int32_t* node_ids, int32_t* neighbors, int32_t* n_nodes, void* stream);
+
 /* ---- edge-based evaluation (reference evaluate.py:40-94).
  * Label grids (F,R,S) i32, 0 = unlabelled.  Scratch sized by
  * lseg_eval_workspace_bytes. */

@@ -15,7 +15,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC]
-SOURCES = ["lseg_kernels.cu", "lseg_fused.cu", "lseg_eval.cu", "lseg_sim.cu", "lseg_format.cpp", "lseg_abi.cu"]
+SOURCES = ["lseg_kernels.cu", "lseg_fused.cu", "lseg_eval.cu", "lseg_sim.cu", "lseg_stream.cu", "lseg_format.cpp",
+           "lseg_abi.cu"]
 
 
 def _deps():

@@ -58,6 +58,8 @@ _SIGS = {
                                          _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
     "lseg_run_scans": (C.c_int, [C.POINTER(lseg_sensor), _I32, _I32, C.POINTER(C.c_double), _I32, _P, _P, _P, _P,
                                  _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
+    "lseg_mb_column": (C.c_int, [_I32, _I32, _I32, C.c_double, C.c_double, _P, _P, _P, _P, _P]),
+    "lseg_mb_finish": (C.c_int, [_I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P]),
     "lseg_format_rows": (C.c_int64, [C.c_int64, _I32, _P, _P, _P, C.c_int64, _I32]),
     "lseg_cast_grid": (C.c_int, [C.POINTER(lseg_sensor), _I32, _P, _I32, _P, _P, _P, _P]),
     "lseg_cast_rays": (C.c_int, [_P, _I32, _I64, _P, _P, _P, _P, _P]),

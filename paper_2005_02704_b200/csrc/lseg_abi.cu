@@ -441,6 +441,24 @@ int lseg_run_scans(const lseg_sensor* sensor, int32_t frames, int32_t interval, 
   return check_launch("run_scans");
 }
 
+int lseg_mb_column(int32_t rings, int32_t kept, int32_t column, double r_min, double r_max, const double* ranges,
+                   int32_t* runcnt, int32_t* colrank, int32_t* slots, void* stream) {
+  if (rings < 1 || kept < 2 || kept > 65535 || rings > 32767) return fail(LSEG_EINVAL, "bad shape");
+  if (column < 0 || column >= kept) return fail(LSEG_EINVAL, "column out of range");
+  if (!ranges || !runcnt || !colrank || !slots) return fail(LSEG_EINVAL, "NULL buffer");
+  launch_mb_column(rings, kept, column, r_min, r_max, ranges, runcnt, colrank, slots, (cudaStream_t)stream);
+  return check_launch("mb_column");
+}
+
+int lseg_mb_finish(int32_t rings, int32_t kept, const int32_t* runcnt, const int32_t* colrank, int32_t* slots,
+                   int32_t* rowoff, int32_t* node_ids, int32_t* neighbors, int32_t* n_nodes, void* stream) {
+  if (rings < 1 || kept < 2 || kept > 65535 || rings > 32767) return fail(LSEG_EINVAL, "bad shape");
+  if (!runcnt || !colrank || !slots || !rowoff || !node_ids || !neighbors || !n_nodes)
+    return fail(LSEG_EINVAL, "NULL buffer");
+  launch_mb_finish(rings, kept, runcnt, colrank, slots, rowoff, node_ids, neighbors, n_nodes, (cudaStream_t)stream);
+  return check_launch("mb_finish");
+}
+
 void lseg_debug_cert_err(float* per_node_err) { g_dbg_err = per_node_err; }
 
 void lseg_debug_tile_cc(int n, const unsigned long long* masks, int32_t* parent, uint32_t* lroots) {

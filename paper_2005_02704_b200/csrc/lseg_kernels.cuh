@@ -50,4 +50,9 @@ void launch_apply_scan(int64_t n, double r_min, double r_max, const double* t, c
 void launch_scene_normals(const lseg_sensor& sn, const double* prims, int n_prims, const double* ranges,
                           const int32_t* labels, double* out, cudaStream_t st);
 void launch_selftest_math(int64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t st);
+void launch_mb_column(int R, int Sk, int j, double r_min, double r_max, const double* col, int32_t* runcnt,
+                      int32_t* colrank, int32_t* slots, cudaStream_t st);
+void launch_mb_finish(int R, int Sk, const int32_t* runcnt, const int32_t* colrank, int32_t* slots, int32_t* rowoff,
+                      int32_t* node_ids, int32_t* neighbors, int32_t* n_nodes, cudaStream_t st);
+
 }  // namespace lseg

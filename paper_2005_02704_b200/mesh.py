@@ -109,12 +109,18 @@ def build_mesh(grid: ScanGrid, interval: int, max_edge_length: float | None = No
 
 class MeshBuilder:
     """Incremental mesh construction, one kept azimuth column at a time
-    (reference mesh.py:139-170).
+    (reference mesh.py:139-170; streaming contract SPEC.md:200; SURVEY.md
+    §8(f) F2).
 
-    Columns arrive in sweep order while the sensor spins; each is copied to its
-    slot of a device range grid as it arrives (asynchronously, from pinned
-    memory), so ``finish()`` only runs the GPU mesh build on data already
-    resident in HBM.  The result equals ``build_mesh`` on the assembled grid.
+    Columns arrive in sweep order while the sensor spins.  Each
+    ``add_column`` uploads the column and launches one small kernel
+    (lseg_mb_column) that records the column's valid cells and their per-ring
+    ranks and emits every slot of the PREVIOUS column -- all of its
+    neighbours exist once the next column is in.  ``finish()`` closes the
+    wrap (columns 0 and S'-1), scans the per-ring counts (O(R)) and resolves
+    the emitted (ring, rank) references to the reference's row-major node
+    ids in one parallel pass (lseg_mb_finish).  The result equals
+    ``build_mesh`` on the assembled grid.
     """
 
     def __init__(self, grid_config, interval: int):
@@ -122,29 +128,51 @@ class MeshBuilder:
         self.interval = int(interval)
         self.kept = subsample_steps(grid_config, interval)
         self._n = 0
-        _lib.lib()
-        R, S = grid_config.rings, grid_config.azimuth_steps
-        self._dev = torch.full((R, S), float("nan"), dtype=torch.float64, device="cuda")
-        self._host = torch.empty((self.kept.size, R), dtype=torch.float64).pin_memory()
-        self._cols = []
+        self._L = _lib.lib()
+        R, Sk = grid_config.rings, self.kept.size
+        dev = torch.device("cuda")
+        self._col = torch.empty((Sk, R), dtype=torch.float64, device=dev)  # one slot per column: no reuse race
+        self._runcnt = torch.zeros(R, dtype=torch.int32, device=dev)
+        self._colrank = torch.empty((R, Sk), dtype=torch.int32, device=dev)
+        self._slots = torch.empty((R, Sk, 6), dtype=torch.int32, device=dev)
+        self._host = torch.empty((Sk, R), dtype=torch.float64).pin_memory()
 
     def add_column(self, ranges) -> None:
+        """Feed the range column for the next kept azimuth step."""
         col = np.asarray(ranges, dtype=float).reshape(-1)
-        if col.size != self.config.rings:
-            raise ValueError(f"column length {col.size} != ring count {self.config.rings}")
+        R = self.config.rings
+        if col.size != R:
+            raise ValueError(f"column length {col.size} != ring count {R}")
         if self._n >= self.kept.size:
             raise ValueError("all kept columns already supplied")
-        self._host[self._n].copy_(torch.from_numpy(col))
-        self._dev[:, int(self.kept[self._n])].copy_(self._host[self._n], non_blocking=True)
-        self._cols.append(col)
+        j = self._n
+        self._host[j].copy_(torch.from_numpy(col))
+        self._col[j].copy_(self._host[j], non_blocking=True)
+        _lib.check(self._L.lseg_mb_column(R, int(self.kept.size), j, float(self.config.r_min),
+                                          float(self.config.r_max), _lib.ptr(self._col[j]), _lib.ptr(self._runcnt),
+                                          _lib.ptr(self._colrank), _lib.ptr(self._slots), _lib.stream_ptr()))
         self._n += 1
 
     def finish(self) -> Mesh:
-        if self._n != self.kept.size:
-            raise ValueError(f"expected {self.kept.size} kept columns, got {self._n}")
-        full = np.full((self.config.rings, self.config.azimuth_steps), np.nan)
-        full[:, self.kept] = np.stack(self._cols, axis=1)
-        return build_mesh(ScanGrid(config=self.config, ranges=full), self.interval, _device_ranges=self._dev)
+        Sk = self.kept.size
+        if self._n != Sk:
+            raise ValueError(f"expected {Sk} kept columns, got {self._n}")
+        R, S = self.config.rings, self.config.azimuth_steps
+        dev = self._runcnt.device
+        node_ids = torch.empty((1, R, Sk), dtype=torch.int32, device=dev)
+        nbrs = torch.empty((1, R * Sk, 6), dtype=torch.int32, device=dev)
+        rowoff = torch.empty(R, dtype=torch.int32, device=dev)
+        n_nodes = torch.empty(1, dtype=torch.int32, device=dev)
+        _lib.check(self._L.lseg_mb_finish(R, int(Sk), _lib.ptr(self._runcnt), _lib.ptr(self._colrank),
+                                          _lib.ptr(self._slots), _lib.ptr(rowoff), _lib.ptr(node_ids),
+                                          _lib.ptr(nbrs), _lib.ptr(n_nodes), _lib.stream_ptr()))
+        ids = node_ids[0].cpu().numpy()
+        rr, pos = np.nonzero(ids >= 0)
+        n = int(rr.size)
+        return Mesh(rings=R, full_steps=S, interval=self.interval, kept_steps=self.kept,
+                    node_rings=rr.astype(np.int32), node_steps=self.kept[pos].astype(np.int64), node_ids=ids,
+                    neighbors=nbrs[0, :n].cpu().numpy(),
+                    _dev={"node_ids": node_ids, "neighbors": nbrs, "n_nodes": n_nodes})
 
 
 def mesh_triangles(mesh: Mesh) -> np.ndarray:
