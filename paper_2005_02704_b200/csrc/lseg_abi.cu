@@ -109,6 +109,7 @@ static int check_sensor(const lseg_sensor* sn) {
 
 static int check_shape(int F, int R, int S, int k, Shape* out) {
   if (F < 0) return fail(LSEG_EINVAL, "frames must be >= 0");
+  if (F > 65535) return fail(LSEG_EINVAL, "at most 65535 frames per call");
   if (kept_count(S, k) < 0)
     return fail(LSEG_EINVAL, "interval " + std::to_string(k) + " not in [1, " + std::to_string(S - 1) + "]");
   *out = make_shape(F, R, S, k);

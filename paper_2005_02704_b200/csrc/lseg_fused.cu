@@ -66,6 +66,9 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_PF_PRUNE
 #define LSEG_PF_PRUNE 8
 #endif
+#ifndef LSEG_BN_SEP
+#define LSEG_BN_SEP 1  // border fp64 normals written by a separate border-cell pass
+#endif
 #ifndef LSEG_CERT_MINB
 #define LSEG_CERT_MINB 4
 #endif
@@ -167,10 +170,12 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
 
   const int tilesC = (sh.Sk + TC - 1) / TC;
   const int tilesR = (sh.R + TR - 1) / TR;
-  const int64_t b = blockIdx.x;
-  const int f = (int)(b / ((int64_t)tilesR * tilesC));
-  const int rem = (int)(b - (int64_t)f * tilesR * tilesC);
-  const int r0 = (rem / tilesC) * TR, c0 = (rem % tilesC) * TC;
+  // grid (tile column, tile row, frame): per-CTA values straight from the
+  // block index (uniform registers, no division)
+  const int f = blockIdx.z;
+  const int rem = blockIdx.y * tilesC + blockIdx.x;  // tile within the frame
+  const int64_t b = (int64_t)f * tilesR * tilesC + rem;
+  const int r0 = blockIdx.y * TR, c0 = blockIdx.x * TC;
   const int TRe = min(TR, sh.R - r0), TCe = min(TC, sh.Sk - c0);
   const double* rf = ranges + (int64_t)f * sh.R * sh.S;
   const uint32_t* vbf = vbits + (int64_t)f * sh.R * sh.Wk;
@@ -375,6 +380,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       o[2] = has ? s_nz[e] : qn;
     }
     nmask[nbase + id] = has ? 1 : 0;
+#if !LSEG_BN_SEP
     if (has) {  // fp64 normals of the tile's border rows / columns for k_merge (coalesced)
       double* bf = bnorm + (int64_t)f * bn_frame(sh, TR, TC);
       const int tr = r0 / TR, tc = c0 / TC;
@@ -383,7 +389,36 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       if (x == 0) bn_put(bf + bn_col(sh, TR, 2 * tc, rr), s_nx[e], s_ny[e], s_nz[e]);
       if (x == TCe - 1) bn_put(bf + bn_col(sh, TR, 2 * tc + 1, rr), s_nx[e], s_ny[e], s_nz[e]);
     }
+#endif
   }
+#if LSEG_BN_SEP
+  // fp64 normals of the tile's border rows / columns for k_merge: only the
+  // 2 TC + 2 TR border cells, one thread each (row stores coalesced)
+  {
+    double* bf = bnorm + (int64_t)f * bn_frame(sh, TR, TC);
+    const int tr = r0 / TR, tc = c0 / TC;
+    for (int u = tid; u < 2 * TC + 2 * TR; u += T) {
+      int y, x, slot;
+      bool rowside;
+      if (u < 2 * TC) {
+        rowside = true;
+        slot = u / TC;
+        x = u - slot * TC;
+        y = slot ? TRe - 1 : 0;
+      } else {
+        rowside = false;
+        slot = (u - 2 * TC) / TR;
+        y = u - 2 * TC - slot * TR;
+        x = slot ? TCe - 1 : 0;
+      }
+      if (y >= TRe || x >= TCe) continue;
+      const int e = y * TC + x;
+      if (!s_has[e]) continue;
+      double* o = rowside ? bf + bn_row(sh, 2 * tr + slot, c0 + x) : bf + bn_col(sh, TR, 2 * tc + slot, r0 + y);
+      bn_put(o, s_nx[e], s_ny[e], s_nz[e]);
+    }
+  }
+#endif
 
 #if LSEG_PHASES
   __syncthreads();
@@ -644,10 +679,12 @@ __global__ void __launch_bounds__(T, LSEG_CERT_MINB) k_tile_cert(
 
   const int tilesC = (sh.Sk + TC - 1) / TC;
   const int tilesR = (sh.R + TR - 1) / TR;
-  const int64_t b = blockIdx.x;
-  const int f = (int)(b / ((int64_t)tilesR * tilesC));
-  const int rem = (int)(b - (int64_t)f * tilesR * tilesC);
-  const int r0 = (rem / tilesC) * TR, c0 = (rem % tilesC) * TC;
+  // grid (tile column, tile row, frame): per-CTA values straight from the
+  // block index (uniform registers, no division)
+  const int f = blockIdx.z;
+  const int rem = blockIdx.y * tilesC + blockIdx.x;  // tile within the frame
+  const int64_t b = (int64_t)f * tilesR * tilesC + rem;
+  const int r0 = blockIdx.y * TR, c0 = blockIdx.x * TC;
   const int TRe = min(TR, sh.R - r0), TCe = min(TC, sh.Sk - c0);
   const double* rf = ranges + (int64_t)f * sh.R * sh.S;
   const uint32_t* vbf = vbits + (int64_t)f * sh.R * sh.Wk;
@@ -1279,10 +1316,12 @@ __global__ void __launch_bounds__(T, 2048 / T) k_tile_cc(Shape sh, const unsigne
   __shared__ unsigned long long s_m[TR * 5];
   const int tilesC = (sh.Sk + TC - 1) / TC;
   const int tilesR = (sh.R + TR - 1) / TR;
-  const int64_t b = blockIdx.x;
-  const int f = (int)(b / ((int64_t)tilesR * tilesC));
-  const int rem = (int)(b - (int64_t)f * tilesR * tilesC);
-  const int r0 = (rem / tilesC) * TR, c0 = (rem % tilesC) * TC;
+  // grid (tile column, tile row, frame): per-CTA values straight from the
+  // block index (uniform registers, no division)
+  const int f = blockIdx.z;
+  const int rem = blockIdx.y * tilesC + blockIdx.x;  // tile within the frame
+  const int64_t b = (int64_t)f * tilesR * tilesC + rem;
+  const int r0 = blockIdx.y * TR, c0 = blockIdx.x * TC;
   const int TRe = min(TR, sh.R - r0), TCe = min(TC, sh.Sk - c0);
   const unsigned long long* mrow = masks + b * (TR * 5);
   for (int j = threadIdx.x; j < TR * 5; j += T) s_m[j] = __ldg(mrow + j);
@@ -2129,6 +2168,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
                         bool exact_normals, float* dbg_err, cudaStream_t st, double* n64) {
   const int tilesC = (sh.Sk + TILE_C - 1) / TILE_C, tilesR = (sh.R + TILE_R - 1) / TILE_R;
   const int64_t nt = (int64_t)sh.F * tilesR * tilesC;
+  const dim3 tgrid(tilesC, tilesR, sh.F);  // frames <= 65535 (check_shape)
   const int per = tilesR * sh.Sk + tilesC * sh.R;
   const int mt = sh.F < 8 ? 64 : 128;  // border-merge threads per CTA (more CTAs for single scans)
   if (!exact_normals) {
@@ -2146,14 +2186,14 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
     cudaFuncSetAttribute(k_tile_cert<TILE_R, TILE_C, TILE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)csmem);
     float4* bn4 = reinterpret_cast<float4*>(ws.bnorm);
-    k_tile_cert<TILE_R, TILE_C, TILE_T><<<(unsigned)nt, TILE_T, csmem, st>>>(
+    k_tile_cert<TILE_R, TILE_C, TILE_T><<<tgrid, TILE_T, csmem, st>>>(
         sn, sh, ranges, ws.vbits, ws.wpre, cp, node_ids, neighbors, n32, nmask, ws.masks, bn4, ws.normals64, dbg_err,
         ws.fscal, n_labels);
     prof_mark("tile", st);
     if (nt < 148 * 16)  // one-wave batches: 256 threads per tile for latency
-      k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
+      k_tile_cc<TILE_R, TILE_C, 256><<<tgrid, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
     else
-      k_tile_cc<TILE_R, TILE_C, LSEG_CC_TBIG><<<(unsigned)nt, LSEG_CC_TBIG, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
+      k_tile_cc<TILE_R, TILE_C, LSEG_CC_TBIG><<<tgrid, LSEG_CC_TBIG, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
     prof_mark("tile_cc", st);
     k_merge_cert<TILE_R, TILE_C><<<dim3((per + mt - 1) / mt, sh.F), mt, 0, st>>>(sn, sh, ranges, ws.vbits, bn4, cp,
                                                                                 ws.parent, ws.rank, ws.fscal);
@@ -2165,14 +2205,14 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
       (size_t)((TILE_R + 2) * (TILE_C + 2) + 2 * (TILE_R + 2) + 2 * (TILE_C + 2) + 3 * TILE_R * TILE_C) * 8 +
       (size_t)(TILE_R + 2) * (TILE_C + 2) * 4 + (size_t)TILE_R * TILE_C * 4;
   cudaFuncSetAttribute(k_tile<TILE_R, TILE_C, TILE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
-  k_tile<TILE_R, TILE_C, TILE_T><<<(unsigned)nt, TILE_T, tsmem, st>>>(sn, sh, ranges, ws.vbits, ws.wpre, thr[0], thr[1],
+  k_tile<TILE_R, TILE_C, TILE_T><<<tgrid, TILE_T, tsmem, st>>>(sn, sh, ranges, ws.vbits, ws.wpre, thr[0], thr[1],
                                                                   thr[2], node_ids, neighbors, n32, nmask, ws.masks,
                                                                   ws.bnorm, ws.parent, ws.lroots, n_labels, n64);
   prof_mark("tile", st);
   if (nt < 148 * 16)  // one-wave batches: 256 threads per tile for latency
-    k_tile_cc<TILE_R, TILE_C, 256><<<(unsigned)nt, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
+    k_tile_cc<TILE_R, TILE_C, 256><<<tgrid, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
   else
-    k_tile_cc<TILE_R, TILE_C, LSEG_CC_TBIG><<<(unsigned)nt, LSEG_CC_TBIG, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
+    k_tile_cc<TILE_R, TILE_C, LSEG_CC_TBIG><<<tgrid, LSEG_CC_TBIG, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
   prof_mark("tile_cc", st);
   k_merge<TILE_R, TILE_C><<<dim3((per + mt - 1) / mt, sh.F), mt, 0, st>>>(
       sh, ws.bnorm, thr[0], thr[1], thr[2], ws.parent);
