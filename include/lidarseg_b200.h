@@ -195,12 +195,14 @@ int lseg_run_pipeline_grid(const lseg_sensor* sensor, int32_t frames, int32_t in
  * pipeline.py:47-70, returning its PipelineResult fields) for F scans in ONE
  * call: ranges (F, R, S) f64 in; mesh node_ids (F,R,S') and neighbors
  * (F,cap,6), fp64 normals64 (F,cap,3) (the reference's NormalMap values,
- * bit-identical; NaN rows where nmask is 0), segment() node_labels (F,R,S)
- * (optional), final labels (F,R,S).  Exact fp64 normals only. */
+ * bit-identical; NaN rows where nmask is 0), node_cells (F,cap,2) i32
+ * optional (ring, step) of each node = Mesh.node_rings / node_steps,
+ * segment() node_labels (F,R,S) optional, final labels (F,R,S).  Exact
+ * fp64 normals only. */
 int lseg_run_scans(const lseg_sensor* sensor, int32_t frames, int32_t interval, const double* thresholds,
                    int32_t min_segment_size, const double* ranges, int32_t* node_ids, int32_t* neighbors,
-                   double* normals64, uint8_t* nmask, int32_t* node_labels, int32_t* labels, int32_t* n_nodes,
-                   int32_t* n_labels, void* workspace, size_t workspace_bytes, void* stream);
+                   double* normals64, uint8_t* nmask, int32_t* node_cells, int32_t* node_labels, int32_t* labels,
+                   int32_t* n_nodes, int32_t* n_labels, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- streaming mesh builder (reference MeshBuilder, mesh.py:139-170;
  * streaming contract SPEC.md:200).  Columns are fed in sweep order; when

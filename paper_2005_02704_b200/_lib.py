@@ -57,7 +57,7 @@ _SIGS = {
     "lseg_run_pipeline_grid": (C.c_int, [C.POINTER(lseg_sensor), _I32, _I32, C.POINTER(C.c_double), _I32, C.c_uint32,
                                          _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
     "lseg_run_scans": (C.c_int, [C.POINTER(lseg_sensor), _I32, _I32, C.POINTER(C.c_double), _I32, _P, _P, _P, _P,
-                                 _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
+                                 _P, _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
     "lseg_mb_column": (C.c_int, [_I32, _I32, _I32, C.c_double, C.c_double, _P, _P, _P, _P, _P]),
     "lseg_mb_finish": (C.c_int, [_I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P]),
     "lseg_format_rows": (C.c_int64, [C.c_int64, _I32, _P, _P, _P, C.c_int64, _I32]),

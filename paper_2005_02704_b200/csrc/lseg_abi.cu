@@ -419,8 +419,8 @@ int lseg_run_pipeline_grid(const lseg_sensor* sensor, int32_t frames, int32_t in
 
 int lseg_run_scans(const lseg_sensor* sensor, int32_t frames, int32_t interval, const double* thresholds,
                    int32_t min_segment_size, const double* ranges, int32_t* node_ids, int32_t* neighbors,
-                   double* normals64, uint8_t* nmask, int32_t* node_labels, int32_t* labels, int32_t* n_nodes,
-                   int32_t* n_labels, void* workspace, size_t workspace_bytes, void* stream) {
+                   double* normals64, uint8_t* nmask, int32_t* node_cells, int32_t* node_labels, int32_t* labels,
+                   int32_t* n_nodes, int32_t* n_labels, void* workspace, size_t workspace_bytes, void* stream) {
   if (int e = check_sensor(sensor)) return e;
   Shape sh;
   if (int e = check_shape(frames, sensor->rings, sensor->steps, interval, &sh)) return e;
@@ -437,7 +437,7 @@ int lseg_run_scans(const lseg_sensor* sensor, int32_t frames, int32_t interval, 
   prof_mark(nullptr, st);
   launch_valid_scan(*sensor, sh, ranges, ws, n_nodes, st);
   launch_fused_graph(*sensor, sh, ws, ranges, thresholds, node_ids, neighbors, nullptr, nmask, n_nodes, n_labels,
-                     node_labels, false, true, nullptr, st, normals64);
+                     node_labels, false, true, nullptr, st, normals64, node_cells);
   launch_prune_fused(sh, ws, min_segment_size, labels, st);
   return check_launch("run_scans");
 }

@@ -66,8 +66,21 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_PF_PRUNE
 #define LSEG_PF_PRUNE 8
 #endif
+#ifndef LSEG_POS_SMEM
+#define LSEG_POS_SMEM 0  // halo positions in shared memory (3 CTAs / SM) instead of rebuilt per use
+#endif
 #ifndef LSEG_BN_SEP
 #define LSEG_BN_SEP 1  // border fp64 normals written by a separate border-cell pass
+#endif
+// resident threads per SM the row kernels are compiled for (2048: 32 registers)
+#ifndef LSEG_CC_TSM
+#define LSEG_CC_TSM 2048
+#endif
+#ifndef LSEG_LAB_TSM
+#define LSEG_LAB_TSM 2048
+#endif
+#ifndef LSEG_PRUNE_TSM
+#define LSEG_PRUNE_TSM 2048
 #endif
 #ifndef LSEG_CERT_MINB
 #define LSEG_CERT_MINB 4
@@ -125,7 +138,9 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
                                                 uint8_t* __restrict__ nmask, unsigned long long* __restrict__ masks,
                                                 double* __restrict__ bnorm, int32_t* __restrict__ parent,
                                                 uint32_t* __restrict__ lroots, int32_t* __restrict__ n_labels,
-                                                double* __restrict__ n64) {
+                                                double* __restrict__ n64, int32_t* __restrict__ node_rc) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int GR = TR + 2, GC = TC + 2;  // halo rows r0-1..r0+TR, cols c0-1..c0+TC
   constexpr int NT = TR * TC;
 #if LSEG_PHASES
@@ -145,6 +160,17 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   extern __shared__ __align__(16) unsigned char s_dyn[];
   // ranges + separable direction tables; positions are rebuilt on use
   // (5 multiplies) -- 19 KB less shared memory buys a 4th CTA per SM
+#if LSEG_POS_SMEM
+  // halo positions computed once per halo cell (reference product order)
+  double* s_px = reinterpret_cast<double*>(s_dyn);
+  double* s_py = s_px + GR * GC;
+  double* s_pz = s_py + GR * GC;
+  double* s_nx = s_pz + GR * GC;
+  auto posyx = [&](int yy, int xx) -> Vec3 {
+    const int i = yy * GC + xx;
+    return Vec3{s_px[i], s_py[i], s_pz[i]};
+  };
+#else
   double* s_r = reinterpret_cast<double*>(s_dyn);
   double* s_ct = s_r + GR * GC;   // cos(elev) per halo row
   double* s_st = s_ct + GR;       // sin(elev) per halo row
@@ -161,6 +187,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     q.z = __dmul_rn(s_st[yy], r);
     return q;
   };
+#endif
   double* s_ny = s_nx + NT;
   double* s_nz = s_ny + NT;
   int* s_id = reinterpret_cast<int*>(s_nz + NT);
@@ -216,9 +243,19 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       const int cc = wrapc(c0 - 1 + x, sh.Sk);
       const uint32_t bit = 1u << (cc & 31);
       const int id = (wv[j] & bit) ? pv[j] + __popc(wv[j] & (bit - 1u)) : -1;
+#if LSEG_POS_SMEM
+      Vec3 q = {0.0, 0.0, 0.0};
+      if (id >= 0) q = cell_pos(sn, rr, cc * sh.k, rv[j]);
+      s_px[e] = q.x;
+      s_py[e] = q.y;
+      s_pz[e] = q.z;
+#else
+      (void)rr;
       s_r[e] = id >= 0 ? rv[j] : 0.0;
+#endif
       s_id[e] = id;
     }
+#if !LSEG_POS_SMEM
     for (int e = tid; e < GR + GC; e += T) {
       if (e < GR) {
         const int rr = min(max(r0 - 1 + e, 0), sh.R - 1);
@@ -230,6 +267,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
         s_sp[e - GR] = __ldg(sn.sin_az + cc);
       }
     }
+#endif
   }
   __syncthreads();
   PH_MARK(1);
@@ -356,6 +394,10 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     const int64_t cell = (int64_t)rr * sh.Sk + cc;
     if (node_ids) node_ids[nbase + cell] = id;
     if (id < 0) continue;
+    if (node_rc) {  // the single-scan Mesh's node_rings / node_steps (mesh.py:115-117)
+      node_rc[(nbase + id) * 2] = rr;
+      node_rc[(nbase + id) * 2 + 1] = cc * sh.k;
+    }
     int nb[6];
 #pragma unroll
     for (int s = 0; s < 6; ++s) nb[s] = s_id[g + slot_dr(s) * GC + slot_dc(s)];
@@ -653,6 +695,8 @@ __global__ void __launch_bounds__(T, LSEG_CERT_MINB) k_tile_cert(
     float* __restrict__ n32, uint8_t* __restrict__ nmask, unsigned long long* __restrict__ masks,
     float4* __restrict__ bn4, double* __restrict__ xn, float* __restrict__ dbg_err, int32_t* __restrict__ fscal,
     int32_t* __restrict__ n_labels) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int GR = TR + 2, GC = TC + 2, NH = GR * GC;
   constexpr int NT = TR * TC;
   static_assert(TC == 64, "row masks assume 64-column tiles");
@@ -1105,6 +1149,8 @@ template <int TR, int TC>
 __global__ void k_merge_cert(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
                              const uint32_t* __restrict__ vbits, const float4* __restrict__ bn4, CertParams cp,
                              int32_t* __restrict__ parent, int32_t* __restrict__ unc, int32_t* __restrict__ fscal) {
+  pdl_trigger();
+  pdl_wait();
   merge_cert_frame<TR, TC>(sn, sh, ranges, vbits, bn4, cp, parent, unc, fscal, blockIdx.y,
                            blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, false);
 }
@@ -1115,6 +1161,8 @@ __global__ void k_merge_exact(lseg_sensor sn, Shape sh, const double* __restrict
                               const uint32_t* __restrict__ vbits, const float4* __restrict__ bn4, CertParams cp,
                               int32_t* __restrict__ parent, const int32_t* __restrict__ unc,
                               int32_t* __restrict__ fscal) {
+  pdl_trigger();
+  pdl_wait();
   const int f = blockIdx.y;
   const int n = fscal[f * 4 + 2];
   if (n == 0) return;
@@ -1309,9 +1357,11 @@ void debug_tile_cc(int n, const unsigned long long* masks, int32_t* parent, uint
 }
 
 template <int TR, int TC, int T>
-__global__ void __launch_bounds__(T, 2048 / T) k_tile_cc(Shape sh, const unsigned long long* __restrict__ masks,
+__global__ void __launch_bounds__(T, LSEG_CC_TSM / T) k_tile_cc(Shape sh, const unsigned long long* __restrict__ masks,
                                                int32_t* __restrict__ parent, uint32_t* __restrict__ lroots,
                                                int32_t* __restrict__ hist, int64_t K) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ int s_par[TR * TC];
   __shared__ unsigned long long s_m[TR * 5];
   const int tilesC = (sh.Sk + TC - 1) / TC;
@@ -1339,6 +1389,8 @@ __global__ void __launch_bounds__(T, 2048 / T) k_tile_cc(Shape sh, const unsigne
 template <int TR, int TC>
 __global__ void k_merge(Shape sh, const double* __restrict__ bnorm, double t0, double t1, double t2,
                         int32_t* __restrict__ parent) {
+  pdl_trigger();
+  pdl_wait();
   // blockIdx.y = frame; threads enumerate the frame's border cells
   const int f = blockIdx.y;
   const int nbr = (sh.R + TR - 1) / TR;
@@ -1414,6 +1466,8 @@ __global__ void k_root_flatten(Shape sh, int32_t* __restrict__ parent, const uin
                                uint32_t* __restrict__ rbits, int32_t* __restrict__ hist, int64_t K,
                                int32_t* __restrict__ fscal, int32_t* __restrict__ rstat,
                                int32_t* __restrict__ n_labels) {
+  pdl_trigger();
+  pdl_wait();
   // after k_merge: point every tile-local root straight at its final root
   // (the only cells whose chains can be long; every other cell points at its
   // tile-local root, so its final root is parent[parent[cell]]), mark final
@@ -1567,7 +1621,7 @@ __device__ __forceinline__ void hist_add(int32_t* hw, int lab) {
 // its value: a non-kept valid cell between two donor columns picks the nearer
 // one directly, the rest search the donor-column bits.
 template <int T>
-__global__ void __launch_bounds__(T, 2048 / T) k_labels_backfill(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
+__global__ void __launch_bounds__(T, LSEG_LAB_TSM / T) k_labels_backfill(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
                                                        const uint32_t* __restrict__ vbits,
                                                        const uint32_t* __restrict__ fbits,
                                                        const int32_t* __restrict__ parent,
@@ -1577,6 +1631,8 @@ __global__ void __launch_bounds__(T, 2048 / T) k_labels_backfill(lseg_sensor sn,
                                                        int32_t* __restrict__ hist, int64_t K,
                                                        uint32_t* __restrict__ rbits_out, int32_t* __restrict__ n_labels,
                                                        int32_t* __restrict__ rstat, int32_t* __restrict__ ticket) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ int s_dynrow[];
   const int S = sh.S, Sk = sh.Sk, k = sh.k, nwk = sh.Wk, nw = (S + 31) / 32;
   int* s_kv = s_dynrow;                                                 // per kept column
@@ -1774,6 +1830,8 @@ __global__ void __launch_bounds__(T, LSEG_BIN_MINB) k_bin_rows(lseg_sensor sn, S
                                                 const int64_t* __restrict__ seg, double* __restrict__ ranges,
                                                 uint32_t* __restrict__ vbits, uint32_t* __restrict__ fbits,
                                                 int32_t* __restrict__ fallback) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ unsigned long long s_cell[];
   __shared__ int s_bad;
   const int64_t row = blockIdx.x;
@@ -1861,6 +1919,8 @@ __global__ void __launch_bounds__(T, LSEG_BIN_MINB) k_bin_rows(lseg_sensor sn, S
 template <typename RT>
 __global__ void k_ring_bounds(Shape sh, const RT* __restrict__ ring, const int64_t* __restrict__ off,
                              int64_t* __restrict__ seg) {
+  pdl_trigger();
+  pdl_wait();
   const int f = blockIdx.y;
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // one warp per bound
@@ -1880,6 +1940,8 @@ __global__ void __launch_bounds__(T) k_bin_finish(lseg_sensor sn, Shape sh, cons
                                                   const int32_t* __restrict__ fallback, double* __restrict__ ranges,
                                                   uint32_t* __restrict__ vbits, uint32_t* __restrict__ fbits,
                                                   int32_t* __restrict__ wpre, int32_t* __restrict__ n_nodes) {
+  pdl_trigger();
+  pdl_wait();
   const int f = blockIdx.x;
   if (ring && fallback[f]) {
     const int Wf = (sh.S + 31) / 32;
@@ -1940,8 +2002,8 @@ static void bin_fused_t(const lseg_sensor& sn, const Shape& sh, const float* xyz
   const size_t smem = sizeof(unsigned long long) * sh.S;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_bin_rows<256, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_ring_bounds<RT><<<dim3((sh.R + 1 + 7) / 8, sh.F), 256, 0, st>>>(sh, ring, off, ws.seg);
-  k_bin_rows<256, RT><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, xyz, ring, off, ws.seg, ranges, ws.vbits, ws.fbits,
+  launch_pdl(k_ring_bounds<RT>, dim3((sh.R + 1 + 7) / 8, sh.F), 256, 0, st, sh, ring, off, ws.seg);
+  launch_pdl(k_bin_rows<256, RT>, sh.F * sh.R, 256, smem, st, sn, sh, xyz, ring, off, ws.seg, ranges, ws.vbits, ws.fbits,
                                                      ws.fallback);
   prof_mark("bin_rows", st);
 }
@@ -1954,7 +2016,7 @@ static void bin_fused_seg(const lseg_sensor& sn, const Shape& sh, const float* x
   const size_t smem = sizeof(unsigned long long) * sh.S;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_bin_rows<256, uint8_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_bin_rows<256, uint8_t, false><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, xyz, nullptr, off, segs, ranges, ws.vbits,
+  launch_pdl(k_bin_rows<256, uint8_t, false>, sh.F * sh.R, 256, smem, st, sn, sh, xyz, nullptr, off, segs, ranges, ws.vbits,
                                                                   ws.fbits, ws.fallback);
   prof_mark("bin_rows", st);
 }
@@ -1963,17 +2025,17 @@ void launch_bin_fused(const lseg_sensor& sn, const Shape& sh, const float* xyz, 
                       const int64_t* off, const Workspace& ws, double* ranges, int32_t* n_nodes, cudaStream_t st) {
   if (ring_bytes == 0) {  // caller-given ring segments: nothing can fall back
     bin_fused_seg(sn, sh, xyz, static_cast<const int64_t*>(ring), off, ws, ranges, st);
-    k_bin_finish<1024, 4, uint8_t><<<sh.F, 1024, 0, st>>>(sn, sh, xyz, nullptr, off, ws.fallback, ranges, ws.vbits,
+    launch_pdl(k_bin_finish<1024, 4, uint8_t>, sh.F, 1024, 0, st, sn, sh, xyz, nullptr, off, ws.fallback, ranges, ws.vbits,
                                                           ws.fbits, ws.wpre, n_nodes);
   } else if (ring_bytes == 1) {
     const uint8_t* r8 = static_cast<const uint8_t*>(ring);
     bin_fused_t(sn, sh, xyz, r8, off, ws, ranges, st);
-    k_bin_finish<1024, 4, uint8_t><<<sh.F, 1024, 0, st>>>(sn, sh, xyz, r8, off, ws.fallback, ranges, ws.vbits,
+    launch_pdl(k_bin_finish<1024, 4, uint8_t>, sh.F, 1024, 0, st, sn, sh, xyz, r8, off, ws.fallback, ranges, ws.vbits,
                                                           ws.fbits, ws.wpre, n_nodes);
   } else {
     const int32_t* r32 = static_cast<const int32_t*>(ring);
     bin_fused_t(sn, sh, xyz, r32, off, ws, ranges, st);
-    k_bin_finish<1024, 4, int32_t><<<sh.F, 1024, 0, st>>>(sn, sh, xyz, r32, off, ws.fallback, ranges, ws.vbits,
+    launch_pdl(k_bin_finish<1024, 4, int32_t>, sh.F, 1024, 0, st, sn, sh, xyz, r32, off, ws.fallback, ranges, ws.vbits,
                                                           ws.fbits, ws.wpre, n_nodes);
   }
   prof_mark("frame_scan", st);
@@ -1997,11 +2059,13 @@ void launch_bin_fused(const lseg_sensor& sn, const Shape& sh, const float* xyz, 
 // publishing its ids, so no wait chain forms and nothing deadlocks.
 // rstat and the ticket are zeroed by k_root_flatten.
 template <int T>
-__global__ void __launch_bounds__(T, 2048 / T) k_prune_rows(Shape sh, const int32_t* __restrict__ lab_in,
+__global__ void __launch_bounds__(T, LSEG_PRUNE_TSM / T) k_prune_rows(Shape sh, const int32_t* __restrict__ lab_in,
                                                   int32_t* __restrict__ out, const int32_t* __restrict__ hist,
                                                   int64_t K, int32_t min_size, const uint32_t* __restrict__ rbits,
                                                   int32_t* __restrict__ remap, int32_t* __restrict__ rstat,
                                                   int32_t* __restrict__ ticket) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int NW = T / 32;
   constexpr int kReady = 1 << 30, kIds = 1 << 29;
   extern __shared__ int s_dynrow[];
@@ -2142,10 +2206,10 @@ void launch_prune_fused(const Shape& sh, const Workspace& ws, int32_t min_size, 
     for (auto fn : {k_prune_rows<128>, k_prune_rows<256>})
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (wide)
-    k_prune_rows<256><<<sh.F * sh.R, 256, smem, st>>>(sh, ws.lab_tmp, labels, ws.hist, ws.K, min_size, ws.rbits,
+    launch_pdl(k_prune_rows<256>, sh.F * sh.R, 256, smem, st, sh, ws.lab_tmp, labels, ws.hist, ws.K, min_size, ws.rbits,
                                                       ws.remap, ws.rcnt, ws.fscal + 3);
   else
-    k_prune_rows<128><<<sh.F * sh.R, 128, smem, st>>>(sh, ws.lab_tmp, labels, ws.hist, ws.K, min_size, ws.rbits,
+    launch_pdl(k_prune_rows<128>, sh.F * sh.R, 128, smem, st, sh, ws.lab_tmp, labels, ws.hist, ws.K, min_size, ws.rbits,
                                                       ws.remap, ws.rcnt, ws.fscal + 3);
   prof_mark("prune_apply", st);
 }
@@ -2165,7 +2229,7 @@ void debug_phases(double* out) {
 void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace& ws, const double* ranges,
                         const double* thr, int32_t* node_ids, int32_t* neighbors, float* n32, uint8_t* nmask,
                         int32_t* n_nodes, int32_t* n_labels, int32_t* node_labels, bool fbits_valid,
-                        bool exact_normals, float* dbg_err, cudaStream_t st, double* n64) {
+                        bool exact_normals, float* dbg_err, cudaStream_t st, double* n64, int32_t* node_rc) {
   const int tilesC = (sh.Sk + TILE_C - 1) / TILE_C, tilesR = (sh.R + TILE_R - 1) / TILE_R;
   const int64_t nt = (int64_t)sh.F * tilesR * tilesC;
   const dim3 tgrid(tilesC, tilesR, sh.F);  // frames <= 65535 (check_shape)
@@ -2186,35 +2250,40 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
     cudaFuncSetAttribute(k_tile_cert<TILE_R, TILE_C, TILE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)csmem);
     float4* bn4 = reinterpret_cast<float4*>(ws.bnorm);
-    k_tile_cert<TILE_R, TILE_C, TILE_T><<<tgrid, TILE_T, csmem, st>>>(
+    launch_pdl(k_tile_cert<TILE_R, TILE_C, TILE_T>, tgrid, TILE_T, csmem, st, 
         sn, sh, ranges, ws.vbits, ws.wpre, cp, node_ids, neighbors, n32, nmask, ws.masks, bn4, ws.normals64, dbg_err,
         ws.fscal, n_labels);
     prof_mark("tile", st);
     if (nt < 148 * 16)  // one-wave batches: 256 threads per tile for latency
-      k_tile_cc<TILE_R, TILE_C, 256><<<tgrid, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
+      launch_pdl(k_tile_cc<TILE_R, TILE_C, 256>, tgrid, 256, 0, st, sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
     else
-      k_tile_cc<TILE_R, TILE_C, LSEG_CC_TBIG><<<tgrid, LSEG_CC_TBIG, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
+      launch_pdl(k_tile_cc<TILE_R, TILE_C, LSEG_CC_TBIG>, tgrid, LSEG_CC_TBIG, 0, st, sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
     prof_mark("tile_cc", st);
-    k_merge_cert<TILE_R, TILE_C><<<dim3((per + mt - 1) / mt, sh.F), mt, 0, st>>>(sn, sh, ranges, ws.vbits, bn4, cp,
+    launch_pdl(k_merge_cert<TILE_R, TILE_C>, dim3((per + mt - 1) / mt, sh.F), mt, 0, st, sn, sh, ranges, ws.vbits, bn4, cp,
                                                                                 ws.parent, ws.rank, ws.fscal);
-    k_merge_exact<TILE_R, TILE_C><<<dim3(1, sh.F), 128, 0, st>>>(sn, sh, ranges, ws.vbits, bn4, cp, ws.parent,
+    launch_pdl(k_merge_exact<TILE_R, TILE_C>, dim3(1, sh.F), 128, 0, st, sn, sh, ranges, ws.vbits, bn4, cp, ws.parent,
                                                                  ws.rank, ws.fscal);
     prof_mark("merge", st);
   } else {
+#if LSEG_POS_SMEM
+  const size_t tsmem = (size_t)(3 * (TILE_R + 2) * (TILE_C + 2) + 3 * TILE_R * TILE_C) * 8 +
+                       (size_t)(TILE_R + 2) * (TILE_C + 2) * 4 + (size_t)TILE_R * TILE_C * 4;
+#else
   const size_t tsmem =
       (size_t)((TILE_R + 2) * (TILE_C + 2) + 2 * (TILE_R + 2) + 2 * (TILE_C + 2) + 3 * TILE_R * TILE_C) * 8 +
       (size_t)(TILE_R + 2) * (TILE_C + 2) * 4 + (size_t)TILE_R * TILE_C * 4;
+#endif
   cudaFuncSetAttribute(k_tile<TILE_R, TILE_C, TILE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
-  k_tile<TILE_R, TILE_C, TILE_T><<<tgrid, TILE_T, tsmem, st>>>(sn, sh, ranges, ws.vbits, ws.wpre, thr[0], thr[1],
+  launch_pdl(k_tile<TILE_R, TILE_C, TILE_T>, tgrid, TILE_T, tsmem, st, sn, sh, ranges, ws.vbits, ws.wpre, thr[0], thr[1],
                                                                   thr[2], node_ids, neighbors, n32, nmask, ws.masks,
-                                                                  ws.bnorm, ws.parent, ws.lroots, n_labels, n64);
+                                                                  ws.bnorm, ws.parent, ws.lroots, n_labels, n64, node_rc);
   prof_mark("tile", st);
   if (nt < 148 * 16)  // one-wave batches: 256 threads per tile for latency
-    k_tile_cc<TILE_R, TILE_C, 256><<<tgrid, 256, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
+    launch_pdl(k_tile_cc<TILE_R, TILE_C, 256>, tgrid, 256, 0, st, sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
   else
-    k_tile_cc<TILE_R, TILE_C, LSEG_CC_TBIG><<<tgrid, LSEG_CC_TBIG, 0, st>>>(sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
+    launch_pdl(k_tile_cc<TILE_R, TILE_C, LSEG_CC_TBIG>, tgrid, LSEG_CC_TBIG, 0, st, sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
   prof_mark("tile_cc", st);
-  k_merge<TILE_R, TILE_C><<<dim3((per + mt - 1) / mt, sh.F), mt, 0, st>>>(
+  launch_pdl(k_merge<TILE_R, TILE_C>, dim3((per + mt - 1) / mt, sh.F), mt, 0, st, 
       sh, ws.bnorm, thr[0], thr[1], thr[2], ws.parent);
   prof_mark("merge", st);
   }
@@ -2222,7 +2291,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   if (!fold) {
     const int ft = (int64_t)sh.F * sh.R < 148 * 8 ? 256 : 128;  // one-wave batches: wider CTAs
     const int thr = sh.Wk >= ft / 32 ? ft : 32 * sh.Wk;
-    k_root_flatten<<<sh.F * sh.R, thr, 0, st>>>(sh, ws.parent, ws.lroots, ws.rbits, ws.hist, ws.K, ws.fscal,
+    launch_pdl(k_root_flatten, sh.F * sh.R, thr, 0, st, sh, ws.parent, ws.lroots, ws.rbits, ws.hist, ws.K, ws.fscal,
                                                 ws.rcnt, n_labels);
     prof_mark("root_flatten", st);
     if (node_labels) {  // frame-level root ranks: only the segment() output needs them
@@ -2237,11 +2306,11 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
     for (auto fn : {k_labels_backfill<128>, k_labels_backfill<256>})
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if ((int64_t)sh.F * sh.R < 148 * 8)  // one-wave batches: 256 threads per row for latency
-    k_labels_backfill<256><<<sh.F * sh.R, 256, smem, st>>>(sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits,
+    launch_pdl(k_labels_backfill<256>, sh.F * sh.R, 256, smem, st, sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits,
                                                            ws.rpre, node_labels, ws.lab_tmp, ws.hist, ws.K,
                                                            fold ? ws.rbits : nullptr, n_labels, ws.rcnt, ws.fscal + 3);
   else
-    k_labels_backfill<128><<<sh.F * sh.R, 128, smem, st>>>(sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits,
+    launch_pdl(k_labels_backfill<128>, sh.F * sh.R, 128, smem, st, sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits,
                                                            ws.rpre, node_labels, ws.lab_tmp, ws.hist, ws.K,
                                                            fold ? ws.rbits : nullptr, n_labels, ws.rcnt, ws.fscal + 3);
   prof_mark("labels_backfill", st);

@@ -65,6 +65,8 @@ __global__ void k_bin_points(lseg_sensor sn, int F, const float* __restrict__ xy
 // --------------------------------------------------------------------------
 __global__ void k_valid_bits(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
                              uint32_t* __restrict__ vbits) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t nwords = (int64_t)sh.F * sh.R * sh.Wk;
   const int lane = threadIdx.x & 31;
   for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nwords;
@@ -87,6 +89,8 @@ template <int T, int ITEMS>
 __global__ void __launch_bounds__(T) k_frame_scan(Shape sh, const uint32_t* __restrict__ vbits,
                                                   int32_t* __restrict__ wpre, int32_t* __restrict__ n_nodes,
                                                   int32_t* __restrict__ hist, int64_t K) {
+  pdl_trigger();
+  pdl_wait();
   using Scan = cub::BlockScan<int, T>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int carry;
@@ -600,9 +604,9 @@ void launch_mesh(const lseg_sensor& sn, const Shape& sh, double max_edge, const 
                  const Workspace& ws, int32_t* node_ids, int32_t* neighbors, int32_t* node_rings,
                  int32_t* node_steps, int32_t* n_nodes, cudaStream_t st) {
   const int64_t nwords = (int64_t)sh.F * sh.R * sh.Wk;
-  k_valid_bits<<<grid_for(nwords * 32, 256), 256, 0, st>>>(sn, sh, ranges, ws.vbits);
+  launch_pdl(k_valid_bits, grid_for(nwords * 32, 256), 256, 0, st, sn, sh, ranges, ws.vbits);
   prof_mark("valid_bits", st);
-  k_frame_scan<1024, 4><<<sh.F, 1024, 0, st>>>(sh, ws.vbits, ws.wpre, n_nodes, nullptr, 0);
+  launch_pdl(k_frame_scan<1024, 4>, sh.F, 1024, 0, st, sh, ws.vbits, ws.wpre, n_nodes, nullptr, 0);
   prof_mark("frame_scan", st);
   const int64_t ncell = (int64_t)sh.F * sh.R * sh.Sk;
   k_mesh<<<grid_for(ncell, 256), 256, 0, st>>>(sn, sh, max_edge, ranges, ws.vbits, ws.wpre, node_ids,
@@ -613,20 +617,20 @@ void launch_mesh(const lseg_sensor& sn, const Shape& sh, double max_edge, const 
 void launch_valid_scan(const lseg_sensor& sn, const Shape& sh, const double* ranges, const Workspace& ws,
                        int32_t* n_nodes, cudaStream_t st) {
   const int64_t nwords = (int64_t)sh.F * sh.R * sh.Wk;
-  k_valid_bits<<<grid_for(nwords * 32, 256), 256, 0, st>>>(sn, sh, ranges, ws.vbits);
+  launch_pdl(k_valid_bits, grid_for(nwords * 32, 256), 256, 0, st, sn, sh, ranges, ws.vbits);
   prof_mark("valid_bits", st);
-  k_frame_scan<1024, 4><<<sh.F, 1024, 0, st>>>(sh, ws.vbits, ws.wpre, n_nodes, nullptr, 0);
+  launch_pdl(k_frame_scan<1024, 4>, sh.F, 1024, 0, st, sh, ws.vbits, ws.wpre, n_nodes, nullptr, 0);
   prof_mark("frame_scan", st);
 }
 
 void launch_frame_scan(const Shape& sh, const Workspace& ws, int32_t* n_nodes, cudaStream_t st) {
-  k_frame_scan<1024, 4><<<sh.F, 1024, 0, st>>>(sh, ws.vbits, ws.wpre, n_nodes, nullptr, 0);
+  launch_pdl(k_frame_scan<1024, 4>, sh.F, 1024, 0, st, sh, ws.vbits, ws.wpre, n_nodes, nullptr, 0);
   prof_mark("frame_scan", st);
 }
 
 void launch_scan_bits(const Shape& sh, const uint32_t* bits, int32_t* pre, int32_t* counts, int32_t* hist, int64_t K,
                       cudaStream_t st) {
-  k_frame_scan<1024, 4><<<sh.F, 1024, 0, st>>>(sh, bits, pre, counts, hist, K);
+  launch_pdl(k_frame_scan<1024, 4>, sh.F, 1024, 0, st, sh, bits, pre, counts, hist, K);
 }
 
 void launch_root_rank(const Shape& sh, const int32_t* n_nodes, const int32_t* parent, const uint8_t* nmask,

@@ -28,7 +28,8 @@ void launch_root_rank(const Shape& sh, const int32_t* n_nodes, const int32_t* pa
 void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace& ws, const double* ranges,
                         const double* thr, int32_t* node_ids, int32_t* neighbors, float* n32, uint8_t* nmask,
                         int32_t* n_nodes, int32_t* n_labels, int32_t* node_labels, bool fbits_valid,
-                        bool exact_normals, float* dbg_err, cudaStream_t st, double* n64 = nullptr);
+                        bool exact_normals, float* dbg_err, cudaStream_t st, double* n64 = nullptr,
+                        int32_t* node_rc = nullptr);
 void launch_bin_fused(const lseg_sensor& sn, const Shape& sh, const float* xyz, const void* ring, int ring_bytes,
                       const int64_t* off, const Workspace& ws, double* ranges, int32_t* n_nodes, cudaStream_t st);
 void launch_frame_scan(const Shape& sh, const Workspace& ws, int32_t* n_nodes, cudaStream_t st);

@@ -120,8 +120,9 @@ def run_pipeline(scan: ScanGrid, cfg: PipelineConfig, interval: int | None = Non
                 "neighbors": torch.empty((1, cap, 6), dtype=torch.int32, device=dev),
                 "n64": torch.empty((1, cap, 3), dtype=torch.float64, device=dev),
                 "nmask": torch.empty((1, cap), dtype=torch.uint8, device=dev),
+                "cells": torch.empty((1, cap, 2), dtype=torch.int32, device=dev),
                 "labels": torch.empty((1, R, S), dtype=torch.int32, device=dev),
-                "counts": torch.empty(2, dtype=torch.int32, device=dev)}
+                "counts": torch.empty((1, 2), dtype=torch.int32, device=dev)}
         _SCAN_BUFS.clear()  # keep one shape's buffers
         _SCAN_BUFS[key] = bufs
     b = bufs
@@ -129,27 +130,27 @@ def run_pipeline(scan: ScanGrid, cfg: PipelineConfig, interval: int | None = Non
     _lib.profile_begin()
     _lib.check(L.lseg_run_scans(sn, 1, interval, _lib.thresholds_arg(seg.thresholds), int(seg.min_segment_size),
                                 _lib.ptr(b["ranges"]), _lib.ptr(b["node_ids"]), _lib.ptr(b["neighbors"]),
-                                _lib.ptr(b["n64"]), _lib.ptr(b["nmask"]), None, _lib.ptr(b["labels"]),
-                                _lib.ptr(b["counts"][:1]), _lib.ptr(b["counts"][1:]), _lib.ptr(b["ws"]), b["wsb"],
+                                _lib.ptr(b["n64"]), _lib.ptr(b["nmask"]), _lib.ptr(b["cells"]), None,
+                                _lib.ptr(b["labels"]),
+                                _lib.ptr(b["counts"][0, :1]), _lib.ptr(b["counts"][0, 1:]), _lib.ptr(b["ws"]), b["wsb"],
                                 _lib.stream_ptr()))
     # every output downloaded asynchronously into fresh pinned host tensors
     # (torch's caching host allocator: no pinning cost per call), one
     # synchronisation; the returned arrays are views of those tensors
     pin = lambda t: torch.empty(t.shape[1:], dtype=t.dtype, pin_memory=True).copy_(t[0], non_blocking=True)
-    h = {k: pin(b[k]) for k in ("node_ids", "labels", "neighbors", "n64", "nmask")}
+    h = {k: pin(b[k]) for k in ("counts", "node_ids", "labels", "neighbors", "n64", "nmask", "cells")}
     stages = _lib.profile_end()  # synchronises on the last event (after the copies were enqueued)
     torch.cuda.current_stream().synchronize()
+    n = int(h["counts"][0])
     node_ids = h["node_ids"].numpy()
-    valid = node_ids >= 0
-    rr, pos = np.nonzero(valid)
-    n = int(rr.size)
     labels = h["labels"].numpy()
     nb = h["neighbors"].numpy()[:n]
-    m = h["nmask"].numpy()[:n].astype(bool)
+    m = h["nmask"].numpy()[:n].view(np.bool_)
     vals = h["n64"].numpy()[:n]
     vals[~m] = np.nan
-    mesh = Mesh(rings=R, full_steps=S, interval=interval, kept_steps=kept, node_rings=rr.astype(np.int32),
-                node_steps=kept[pos].astype(np.int64), node_ids=node_ids, neighbors=nb)
+    cells = h["cells"].numpy()[:n]
+    mesh = Mesh(rings=R, full_steps=S, interval=interval, kept_steps=kept, node_rings=cells[:, 0],
+                node_steps=cells[:, 1].astype(np.int64), node_ids=node_ids, neighbors=nb)
     timings = {"mesh": 0.0, "normals": 0.0, "segment": 0.0, "backfill": 0.0}
     for name, (ms, _) in stages.items():
         if name in _STAGE_OF:
