@@ -480,9 +480,13 @@ def main():
                  "frac": pb / (ms_step / 1e3) / 1e9 / peak if ms_step else 0.0,
                  "frac_of_8tbs": pb / (ms_step / 1e3) / 1e9 / 8000.0 if ms_step else 0.0,
                  "bytes_per_point": pb / max(P, 1)}
-    per_stage = {k: {"ms": round(stage_ms[k], 4), "share": round(stages[k][0] / a.steps / ms_step, 4),
-                     "alg_bytes": alg.get(k, 0), "design_bytes": des.get(k),
-                     "design_gbs": (des.get(k) or 0) / (stage_ms[k] / 1e3) / 1e9} for k in stages}
+    per_stage = {}
+    for k in stages:
+        ct_k = committed_traffic(k, F, a.interval)
+        per_stage[k] = {"ms": round(stage_ms[k], 4), "share": round(stages[k][0] / a.steps / ms_step, 4),
+                        "alg_bytes": alg.get(k, 0), "design_bytes": des.get(k),
+                        "design_gbs": (des.get(k) or 0) / (stage_ms[k] / 1e3) / 1e9,
+                        "ncu_dram_bytes": ct_k["dram_bytes_per_launch"] if ct_k else None}
 
     # ---- near-threshold edges of the timed batch, sampled-frame parity (outside the timed region)
     thr = tuple(float(t) for t in L.SegmenterConfig().thresholds)
