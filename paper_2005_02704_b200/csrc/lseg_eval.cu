@@ -128,7 +128,7 @@ __global__ void k_dilate_bytes(EvalShape e, const uint32_t* __restrict__ bits, i
 
 static int grid_of(int64_t n) {
   int64_t b = (n + 255) / 256;
-  return (int)(b > 148 * 32 ? 148 * 32 : (b < 1 ? 1 : b));
+  return (int)(b > num_sms() * 32 ? num_sms() * 32 : (b < 1 ? 1 : b));
 }
 
 size_t eval_workspace_bytes(int F, int R, int S) {

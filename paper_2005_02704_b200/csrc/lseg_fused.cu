@@ -2199,7 +2199,7 @@ __global__ void __launch_bounds__(T, LSEG_PRUNE_TSM / T) k_prune_rows(Shape sh, 
 void launch_prune_fused(const Shape& sh, const Workspace& ws, int32_t min_size, int32_t* labels, cudaStream_t st) {
   // 128-thread CTAs (16 per SM) for throughput; one-wave batches (single
   // scans) use 256 threads per row to cut the per-row latency
-  const bool wide = (int64_t)sh.F * sh.R < 148 * 8;
+  const bool wide = (int64_t)sh.F * sh.R < num_sms() * 8;
   const int nwr = (sh.S + 31) / 32;
   const size_t smem = sizeof(int) * ((size_t)nwr * 33 + 2 * (size_t)sh.Wk);
   if (smem > 48 * 1024)
@@ -2254,7 +2254,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
         sn, sh, ranges, ws.vbits, ws.wpre, cp, node_ids, neighbors, n32, nmask, ws.masks, bn4, ws.normals64, dbg_err,
         ws.fscal, n_labels);
     prof_mark("tile", st);
-    if (nt < 148 * 16)  // one-wave batches: 256 threads per tile for latency
+    if (nt < num_sms() * 16)  // one-wave batches: 256 threads per tile for latency
       launch_pdl(k_tile_cc<TILE_R, TILE_C, 256>, tgrid, 256, 0, st, sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
     else
       launch_pdl(k_tile_cc<TILE_R, TILE_C, LSEG_CC_TBIG>, tgrid, LSEG_CC_TBIG, 0, st, sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
@@ -2278,7 +2278,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
                                                                   thr[2], node_ids, neighbors, n32, nmask, ws.masks,
                                                                   ws.bnorm, ws.parent, ws.lroots, n_labels, n64, node_rc);
   prof_mark("tile", st);
-  if (nt < 148 * 16)  // one-wave batches: 256 threads per tile for latency
+  if (nt < num_sms() * 16)  // one-wave batches: 256 threads per tile for latency
     launch_pdl(k_tile_cc<TILE_R, TILE_C, 256>, tgrid, 256, 0, st, sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
   else
     launch_pdl(k_tile_cc<TILE_R, TILE_C, LSEG_CC_TBIG>, tgrid, LSEG_CC_TBIG, 0, st, sh, ws.masks, ws.parent, ws.lroots, ws.hist, ws.K);
@@ -2289,7 +2289,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   }
   const bool fold = !node_labels && LSEG_FOLD_FLATTEN;
   if (!fold) {
-    const int ft = (int64_t)sh.F * sh.R < 148 * 8 ? 256 : 128;  // one-wave batches: wider CTAs
+    const int ft = (int64_t)sh.F * sh.R < num_sms() * 8 ? 256 : 128;  // one-wave batches: wider CTAs
     const int thr = sh.Wk >= ft / 32 ? ft : 32 * sh.Wk;
     launch_pdl(k_root_flatten, sh.F * sh.R, thr, 0, st, sh, ws.parent, ws.lroots, ws.rbits, ws.hist, ws.K, ws.fscal,
                                                 ws.rcnt, n_labels);
@@ -2305,7 +2305,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   if (smem > 48 * 1024)
     for (auto fn : {k_labels_backfill<128>, k_labels_backfill<256>})
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if ((int64_t)sh.F * sh.R < 148 * 8)  // one-wave batches: 256 threads per row for latency
+  if ((int64_t)sh.F * sh.R < num_sms() * 8)  // one-wave batches: 256 threads per row for latency
     launch_pdl(k_labels_backfill<256>, sh.F * sh.R, 256, smem, st, sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits,
                                                            ws.rpre, node_labels, ws.lab_tmp, ws.hist, ws.K,
                                                            fold ? ws.rbits : nullptr, n_labels, ws.rcnt, ws.fscal + 3);

@@ -579,7 +579,7 @@ __global__ void k_selftest_math(int64_t n, uint64_t seed, unsigned long long* ba
 
 void launch_selftest_math(int64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t st) {
   cudaMemsetAsync(bad, 0, 16, st);
-  k_selftest_math<<<148 * 16, 256, 0, st>>>(n, seed, bad);
+  k_selftest_math<<<num_sms() * 16, 256, 0, st>>>(n, seed, bad);
 }
 
 // --------------------------------------------------------------------------
@@ -587,7 +587,7 @@ void launch_selftest_math(int64_t n, uint64_t seed, unsigned long long* bad, cud
 // --------------------------------------------------------------------------
 static inline int grid_for(int64_t n, int threads) {
   int64_t b = (n + threads - 1) / threads;
-  const int64_t cap = 148LL * 64;  // persistent-ish grid-stride cap
+  const int64_t cap = (int64_t)num_sms() * 64;  // persistent-ish grid-stride cap
   if (b > cap) b = cap;
   return (int)(b < 1 ? 1 : b);
 }

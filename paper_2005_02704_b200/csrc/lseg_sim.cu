@@ -342,7 +342,7 @@ __global__ void k_scene_normals(lseg_sensor sn, const double* __restrict__ prims
 
 static int sim_grid(int64_t n) {
   const int64_t b = (n + 127) / 128;
-  return (int)(b > 148 * 16 ? 148 * 16 : (b < 1 ? 1 : b));
+  return (int)(b > num_sms() * 16 ? num_sms() * 16 : (b < 1 ? 1 : b));
 }
 
 void launch_cast_grid(const lseg_sensor& sn, int F, const double* prims, int n_prims, const double* poses,

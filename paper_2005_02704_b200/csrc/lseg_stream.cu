@@ -108,7 +108,7 @@ void launch_mb_finish(int R, int Sk, const int32_t* runcnt, const int32_t* colra
   k_mb_wrap<<<1, R < 256 ? ((R + 31) / 32) * 32 : 256, 0, st>>>(R, Sk, runcnt, colrank, slots, rowoff, n_nodes);
   const int64_t n = (int64_t)R * Sk;
   int64_t blocks = (n + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks > num_sms() * 16) blocks = num_sms() * 16;
   k_mb_resolve<<<(int)blocks, 256, 0, st>>>(R, Sk, colrank, slots, rowoff, node_ids, neighbors);
 }
 
