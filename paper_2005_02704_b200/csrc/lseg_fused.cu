@@ -69,6 +69,9 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_POS_SMEM
 #define LSEG_POS_SMEM 0  // halo positions in shared memory (3 CTAs / SM) instead of rebuilt per use
 #endif
+#ifndef LSEG_GEN_SUBST
+#define LSEG_GEN_SUBST 1  // general-slot nodes: straight-line six-slot fan with absent slots substituted
+#endif
 #ifndef LSEG_BN_SEP
 #define LSEG_BN_SEP 1  // border fp64 normals written by a separate border-cell pass
 #endif
@@ -362,6 +365,17 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     const int y = e / TC, x = e - y * TC;
     const unsigned m = s_m[e];
     const Vec3 p = posyx(y + 1, x + 1);
+    double nv[3];
+#if LSEG_GEN_SUBST
+    // straight-line six-slot sequence with absent slots substituted
+    // (fan_subst): slot s -> (row, column) offsets from packed tables
+    // (dr + 1, dc + 1 in 2-bit fields)
+    auto pos = [&](int sl) -> Vec3 {
+      const int dr = (int)((0x41Au >> (2 * sl)) & 3u) - 1, dc = (int)((0x069u >> (2 * sl)) & 3u) - 1;
+      return posyx(y + 1 + dr, x + 1 + dc);
+    };
+    if (fan_subst<kFastMath>(p, m, pos, nv)) {
+#else
     FanT<kFastMath> fan;
 #pragma unroll
     for (int s = 0; s < 6; ++s) {
@@ -373,8 +387,8 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       const Vec3 q = posyx(yq, gq - yq * GC);
       fan.add(__dsub_rn(q.x, p.x), __dsub_rn(q.y, p.y), __dsub_rn(q.z, p.z));
     }
-    double nv[3];
     if (fan.finish(p, nv)) {
+#endif
       s_nx[e] = nv[0];
       s_ny[e] = nv[1];
       s_nz[e] = nv[2];
