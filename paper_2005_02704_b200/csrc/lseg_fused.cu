@@ -1612,6 +1612,40 @@ __device__ __forceinline__ int nearest_kept_donor(const uint32_t* s_kdm, int nwk
   return dl < dr ? cl : (dr < dl ? cr : (L < Rc ? cl : cr));
 }
 
+// nearest_donor with per-word tables: P[w] / N[w] = the nearest word at or
+// before / after word w (cyclic) holding a donor.  O(1) per target instead of
+// a word-by-word search (rows of fragmented frames have few, far donors).
+// Same result as nearest_donor (the row must hold at least one donor).
+__device__ __forceinline__ int nearest_donor_tab(const uint32_t* s_dm, const short* P, const short* N, int nw, int S,
+                                                 int s) {
+  const int w = s >> 5, b = s & 31;
+  int left;
+  {
+    const uint32_t m = s_dm[w] & ((1u << b) - 1u);
+    if (m) {
+      left = w * 32 + 31 - __clz(m);
+    } else {  // the nearest earlier donor word; if that wrapped back to w, its donors are all above s
+      const int pw = P[w == 0 ? nw - 1 : w - 1];
+      left = pw * 32 + 31 - __clz(s_dm[pw]);
+    }
+  }
+  int right;
+  {
+    const uint32_t m = (b == 31) ? 0u : (s_dm[w] & ~((2u << b) - 1u));
+    if (m) {
+      right = w * 32 + __ffs(m) - 1;
+    } else {
+      const int nx = N[w + 1 == nw ? 0 : w + 1];
+      right = nx * 32 + __ffs(s_dm[nx]) - 1;
+    }
+  }
+  int dl = s - left;
+  if (dl <= 0) dl += S;
+  int dr = right - s;
+  if (dr <= 0) dr += S;
+  return dl < dr ? left : (dr < dl ? right : min(left, right));
+}
+
 // Shared body of k_prune_rows' fill: s_val[s] holds a donor label (> 0),
 // 0 (passive: stays 0) or -2 (target: nearest donor's label, 0 if the row has
 // no donor); s_dm the donor bits.  Returns the filled label of cell s.
@@ -2088,6 +2122,8 @@ __global__ void __launch_bounds__(T, LSEG_PRUNE_TSM / T) k_prune_rows(Shape sh, 
   uint32_t* s_dm = reinterpret_cast<uint32_t*>(s_dynrow + nw * 32);
   int* s_wc = reinterpret_cast<int*>(s_dm + nw);  // per-word survivor counts -> row-local prefix
   uint32_t* s_sb = reinterpret_cast<uint32_t*>(s_wc + sh.Wk);  // survivor bits of the row
+  short* s_pw = reinterpret_cast<short*>(s_sb + sh.Wk);  // nearest donor word at / before each word (cyclic)
+  short* s_nx = s_pw + nw;                              // ... at / after
   __shared__ int s_any, s_row, s_base, s_part[NW];
   if (threadIdx.x == 0) {
     s_row = atomicAdd(ticket, 1);
@@ -2207,7 +2243,44 @@ __global__ void __launch_bounds__(T, LSEG_PRUNE_TSM / T) k_prune_rows(Shape sh, 
   if (any && lane == 0) s_any = 1;
   __syncthreads();
   const bool rany = s_any != 0;
-  for (int s = threadIdx.x; s < S; s += T) out[rb + s] = fill_one(s_val, s_dm, nw, S, s, rany);
+  if (rany) {
+    // donor-word tables (one warp): running max / min of donor word indices,
+    // entries before the first / after the last donor word wrap around
+    if (warp == 0) {
+      int carry = -1;
+      for (int c0 = 0; c0 < nw; c0 += 32) {
+        const int w = c0 + lane;
+        int x = (w < nw && s_dm[w]) ? w : -1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) x = max(x, __shfl_up_sync(0xffffffffu, x, o));
+        x = max(x, carry);
+        if (w < nw) s_pw[w] = (short)x;
+        carry = __shfl_sync(0xffffffffu, x, 31);
+      }
+      const int last = carry;
+      carry = 0x7fffffff;
+      for (int c0 = ((nw - 1) & ~31); c0 >= 0; c0 -= 32) {
+        const int w = c0 + 31 - lane;  // lane 0 holds the highest word of the chunk
+        int x = (w < nw && s_dm[w]) ? w : 0x7fffffff;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) x = min(x, __shfl_up_sync(0xffffffffu, x, o));
+        x = min(x, carry);
+        if (w < nw) s_nx[w] = (short)(x == 0x7fffffff ? -1 : x);
+        carry = __shfl_sync(0xffffffffu, x, 31);
+      }
+      const int first = carry;
+      __syncwarp();
+      for (int w = lane; w < nw; w += 32) {
+        if (s_pw[w] < 0) s_pw[w] = (short)last;
+        if (s_nx[w] < 0) s_nx[w] = (short)first;
+      }
+    }
+    __syncthreads();
+  }
+  for (int s = threadIdx.x; s < S; s += T) {
+    const int v = s_val[s];
+    out[rb + s] = v != -2 ? (v > 0 ? v : 0) : (rany ? s_val[nearest_donor_tab(s_dm, s_pw, s_nx, nw, S, s)] : 0);
+  }
 }
 
 void launch_prune_fused(const Shape& sh, const Workspace& ws, int32_t min_size, int32_t* labels, cudaStream_t st) {
@@ -2215,7 +2288,7 @@ void launch_prune_fused(const Shape& sh, const Workspace& ws, int32_t min_size, 
   // scans) use 256 threads per row to cut the per-row latency
   const bool wide = (int64_t)sh.F * sh.R < num_sms() * 8;
   const int nwr = (sh.S + 31) / 32;
-  const size_t smem = sizeof(int) * ((size_t)nwr * 33 + 2 * (size_t)sh.Wk);
+  const size_t smem = sizeof(int) * ((size_t)nwr * 33 + 2 * (size_t)sh.Wk) + sizeof(short) * 2 * (size_t)nwr;
   if (smem > 48 * 1024)
     for (auto fn : {k_prune_rows<128>, k_prune_rows<256>})
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
