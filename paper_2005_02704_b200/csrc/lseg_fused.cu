@@ -1217,9 +1217,13 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
     s_par[e] = y * TC + (Z ? 64 - __clzll((long long)Z) : 0);
   }
   __syncthreads();
-  // vertical / diagonal unions: edges whose parallel edge one column to the
-  // left already joins the same two runs are dropped with 64-bit mask
-  // arithmetic (one thread per row pair), the rest are unioned cell-parallel
+  // vertical / diagonal unions: an edge is dropped (64-bit mask arithmetic,
+  // one thread per row pair) when another kept edge joins the same two runs:
+  // the parallel edge one column to the left, or -- for a diagonal (y,x) ->
+  // (y+1,x+1) -- the vertical edge into (y+1,x) or out of (y,x+1) when the
+  // row edge between them passes (vertical edges are only ever dropped for
+  // vertical edges further left, so no drop depends on itself); the rest are
+  // unioned cell-parallel
   __shared__ unsigned long long s_U[TR * 2];
   for (int y = threadIdx.x; y < TR; y += T) {
     unsigned long long U0 = 0, U1 = 0;
@@ -1227,7 +1231,7 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
       const unsigned long long Hy = s_m[y * 5], V0 = s_m[y * 5 + 1], V1 = s_m[y * 5 + 2];
       const unsigned long long Hn = s_m[(y + 1) * 5];
       U0 = V0 & ~((Hy << 1) & (Hn << 1) & (V0 << 1));
-      U1 = V1 & ~((V0 & Hn) | ((Hy << 1) & Hn & (V1 << 1)));
+      U1 = V1 & ~((V0 & Hn) | ((Hy << 1) & Hn & (V1 << 1)) | (Hy & (V0 >> 1)));
     }
     s_U[2 * y] = U0;
     s_U[2 * y + 1] = U1;
