@@ -66,9 +66,6 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_PF_PRUNE
 #define LSEG_PF_PRUNE 8
 #endif
-#ifndef LSEG_POS_SMEM
-#define LSEG_POS_SMEM 0  // halo positions in shared memory (3 CTAs / SM) instead of rebuilt per use
-#endif
 #ifndef LSEG_GEN_SUBST
 #define LSEG_GEN_SUBST 1  // general-slot nodes: straight-line six-slot fan with absent slots substituted
 #endif
@@ -163,17 +160,6 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   extern __shared__ __align__(16) unsigned char s_dyn[];
   // ranges + separable direction tables; positions are rebuilt on use
   // (5 multiplies) -- 19 KB less shared memory buys a 4th CTA per SM
-#if LSEG_POS_SMEM
-  // halo positions computed once per halo cell (reference product order)
-  double* s_px = reinterpret_cast<double*>(s_dyn);
-  double* s_py = s_px + GR * GC;
-  double* s_pz = s_py + GR * GC;
-  double* s_nx = s_pz + GR * GC;
-  auto posyx = [&](int yy, int xx) -> Vec3 {
-    const int i = yy * GC + xx;
-    return Vec3{s_px[i], s_py[i], s_pz[i]};
-  };
-#else
   double* s_r = reinterpret_cast<double*>(s_dyn);
   double* s_ct = s_r + GR * GC;   // cos(elev) per halo row
   double* s_st = s_ct + GR;       // sin(elev) per halo row
@@ -190,7 +176,6 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     q.z = __dmul_rn(s_st[yy], r);
     return q;
   };
-#endif
   double* s_ny = s_nx + NT;
   double* s_nz = s_ny + NT;
   int* s_id = reinterpret_cast<int*>(s_nz + NT);
@@ -246,19 +231,9 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       const int cc = wrapc(c0 - 1 + x, sh.Sk);
       const uint32_t bit = 1u << (cc & 31);
       const int id = (wv[j] & bit) ? pv[j] + __popc(wv[j] & (bit - 1u)) : -1;
-#if LSEG_POS_SMEM
-      Vec3 q = {0.0, 0.0, 0.0};
-      if (id >= 0) q = cell_pos(sn, rr, cc * sh.k, rv[j]);
-      s_px[e] = q.x;
-      s_py[e] = q.y;
-      s_pz[e] = q.z;
-#else
-      (void)rr;
       s_r[e] = id >= 0 ? rv[j] : 0.0;
-#endif
       s_id[e] = id;
     }
-#if !LSEG_POS_SMEM
     for (int e = tid; e < GR + GC; e += T) {
       if (e < GR) {
         const int rr = min(max(r0 - 1 + e, 0), sh.R - 1);
@@ -270,7 +245,6 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
         s_sp[e - GR] = __ldg(sn.sin_az + cc);
       }
     }
-#endif
   }
   __syncthreads();
   PH_MARK(1);
@@ -2356,14 +2330,9 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
                                                                  ws.rank, ws.fscal);
     prof_mark("merge", st);
   } else {
-#if LSEG_POS_SMEM
-  const size_t tsmem = (size_t)(3 * (TILE_R + 2) * (TILE_C + 2) + 3 * TILE_R * TILE_C) * 8 +
-                       (size_t)(TILE_R + 2) * (TILE_C + 2) * 4 + (size_t)TILE_R * TILE_C * 4;
-#else
   const size_t tsmem =
       (size_t)((TILE_R + 2) * (TILE_C + 2) + 2 * (TILE_R + 2) + 2 * (TILE_C + 2) + 3 * TILE_R * TILE_C) * 8 +
       (size_t)(TILE_R + 2) * (TILE_C + 2) * 4 + (size_t)TILE_R * TILE_C * 4;
-#endif
   cudaFuncSetAttribute(k_tile<TILE_R, TILE_C, TILE_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
   launch_pdl(k_tile<TILE_R, TILE_C, TILE_T>, tgrid, TILE_T, tsmem, st, sn, sh, ranges, ws.vbits, ws.wpre, thr[0], thr[1],
                                                                   thr[2], node_ids, neighbors, n32, nmask, ws.masks,
