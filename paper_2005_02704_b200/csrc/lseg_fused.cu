@@ -227,7 +227,6 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       const int e = tid + j * T;
       if (e >= GR * GC) break;
       const int y = e / GC, x = e - y * GC;
-      const int rr = r0 - 1 + y;
       const int cc = wrapc(c0 - 1 + x, sh.Sk);
       const uint32_t bit = 1u << (cc & 31);
       const int id = (wv[j] & bit) ? pv[j] + __popc(wv[j] & (bit - 1u)) : -1;
