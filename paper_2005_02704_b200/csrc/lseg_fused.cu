@@ -1677,6 +1677,10 @@ __global__ void __launch_bounds__(T, LSEG_LAB_TSM / T) k_labels_backfill(lseg_se
   // itself, the row's final roots go to rbits_out and n_labels, and the
   // pruning's per-row counters are reset here
   const bool fold = rbits_out != nullptr;
+  // k = 1 without the segment() output: labelled / passive cells are written
+  // and counted while the columns are classified; the second pass only
+  // handles the backfill targets (valid cells without a normal: rare at k = 1)
+  const bool direct = (k == 1) && !node_labels;
   __shared__ int s_nroot;
   if (threadIdx.x == 0) {
     s_any = 0;
@@ -1725,6 +1729,10 @@ __global__ void __launch_bounds__(T, LSEG_LAB_TSM / T) k_labels_backfill(lseg_se
       const uint32_t dm = __ballot_sync(0xffffffffu, v > 0);
       if ((c & 31) == 0) s_kdm[c >> 5] = dm;
       any |= dm != 0;
+      if (direct) {  // k = 1: every cell but the backfill targets is final here
+        if (c < S && v != -2) out[(int64_t)row * S + c] = v > 0 ? v : 0;
+        hist_add(hist + (int64_t)f * K, v > 0 ? v : 0);
+      }
     }
   }
   if (any && (threadIdx.x & 31) == 0) s_any = 1;
@@ -1736,6 +1744,7 @@ __global__ void __launch_bounds__(T, LSEG_LAB_TSM / T) k_labels_backfill(lseg_se
   // s / k as a multiply-high: exact for s < 2^32 / k (S <= 16384 here)
   const unsigned kmag = 0xffffffffu / (unsigned)k + 1u;
   for (int s = threadIdx.x; s < nw * 32; s += T) {  // whole warps (hist_add)
+    if (direct && !__any_sync(0xffffffffu, s < S && s_kv[s] == -2)) continue;  // warp-uniform
     int r = 0;
     if (s < S) {
       const int c = (k == 1) ? s : (int)__umulhi((unsigned)s, kmag);
@@ -1762,7 +1771,8 @@ __global__ void __launch_bounds__(T, LSEG_LAB_TSM / T) k_labels_backfill(lseg_se
       }
       if (node_labels)  // reference segment() output: 1 + rank of the root
         node_labels[rb + s] = (j == 0 && v > 0) ? rank_label(rbf, rpf, sh.Wk, sh.Sk, v - 1, sh.inv_Sk) : 0;
-      out[rb + s] = r;
+      if (!direct || v == -2) out[rb + s] = r;
+      else r = 0;  // written and counted in the first pass
     }
     hist_add(hw, r);
   }
