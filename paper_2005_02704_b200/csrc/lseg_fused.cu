@@ -1645,7 +1645,7 @@ __device__ __forceinline__ void hist_add(int32_t* hw, int lab) {
 // (label / valid-without-label target / invalid) and every cell then takes
 // its value: a non-kept valid cell between two donor columns picks the nearer
 // one directly, the rest search the donor-column bits.
-template <int T>
+template <int T, bool DIRECT>
 __global__ void __launch_bounds__(T, LSEG_LAB_TSM / T) k_labels_backfill(lseg_sensor sn, Shape sh, const double* __restrict__ ranges,
                                                        const uint32_t* __restrict__ vbits,
                                                        const uint32_t* __restrict__ fbits,
@@ -1680,7 +1680,7 @@ __global__ void __launch_bounds__(T, LSEG_LAB_TSM / T) k_labels_backfill(lseg_se
   // k = 1 without the segment() output: labelled / passive cells are written
   // and counted while the columns are classified; the second pass only
   // handles the backfill targets (valid cells without a normal: rare at k = 1)
-  const bool direct = (k == 1) && !node_labels;
+  constexpr bool direct = DIRECT;  // the launcher's choice: k == 1 && !node_labels
   __shared__ int s_nroot;
   if (threadIdx.x == 0) {
     s_any = 0;
@@ -2371,17 +2371,13 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   // labels + backfill -> lab_tmp (+ histogram)
   const size_t smem = sizeof(int) * (size_t)sh.Wk * 33;
   const uint32_t* fb = (sh.k > 1 && fbits_valid) ? ws.fbits : nullptr;
-  if (smem > 48 * 1024)
-    for (auto fn : {k_labels_backfill<128>, k_labels_backfill<256>})
-      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if ((int64_t)sh.F * sh.R < num_sms() * 8)  // one-wave batches: 256 threads per row for latency
-    launch_pdl(k_labels_backfill<256>, sh.F * sh.R, 256, smem, st, sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits,
-                                                           ws.rpre, node_labels, ws.lab_tmp, ws.hist, ws.K,
-                                                           fold ? ws.rbits : nullptr, n_labels, ws.rcnt, ws.fscal + 3);
-  else
-    launch_pdl(k_labels_backfill<128>, sh.F * sh.R, 128, smem, st, sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits,
-                                                           ws.rpre, node_labels, ws.lab_tmp, ws.hist, ws.K,
-                                                           fold ? ws.rbits : nullptr, n_labels, ws.rcnt, ws.fscal + 3);
+  const bool wide = (int64_t)sh.F * sh.R < num_sms() * 8;  // one-wave batches: 256 threads per row for latency
+  const bool direct = sh.k == 1 && !node_labels;
+  auto kern = wide ? (direct ? k_labels_backfill<256, true> : k_labels_backfill<256, false>)
+                   : (direct ? k_labels_backfill<128, true> : k_labels_backfill<128, false>);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  launch_pdl(kern, sh.F * sh.R, wide ? 256 : 128, smem, st, sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits, ws.rpre,
+             node_labels, ws.lab_tmp, ws.hist, ws.K, fold ? ws.rbits : nullptr, n_labels, ws.rcnt, ws.fscal + 3);
   prof_mark("labels_backfill", st);
 }
 
