@@ -11,6 +11,7 @@
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -110,8 +111,9 @@ def run_pipeline(scan: ScanGrid, cfg: PipelineConfig, interval: int | None = Non
     dev = torch.device("cuda")
     _, sn = device_tables(conf, dev)
     seg = cfg.segmenter
-    key = (R, S, interval)
-    bufs = _SCAN_BUFS.get(key)
+    key = (torch.cuda.current_device(), R, S, interval)
+    cache = _SCAN_BUFS.__dict__.setdefault("bufs", {})  # per thread: concurrent callers never share buffers
+    bufs = cache.get(key)
     if bufs is None:
         wsb = _lib.workspace_bytes(1, R, S, interval)
         bufs = {"ws": torch.empty(wsb, dtype=torch.uint8, device=dev), "wsb": wsb,
@@ -123,8 +125,8 @@ def run_pipeline(scan: ScanGrid, cfg: PipelineConfig, interval: int | None = Non
                 "cells": torch.empty((1, cap, 2), dtype=torch.int32, device=dev),
                 "labels": torch.empty((1, R, S), dtype=torch.int32, device=dev),
                 "counts": torch.empty((1, 2), dtype=torch.int32, device=dev)}
-        _SCAN_BUFS.clear()  # keep one shape's buffers
-        _SCAN_BUFS[key] = bufs
+        cache.clear()  # keep one shape's buffers
+        cache[key] = bufs
     b = bufs
     b["ranges"].copy_(torch.from_numpy(np.array(scan.ranges, dtype=np.float64, copy=True)).view(1, R, S))
     _lib.profile_begin()
@@ -159,7 +161,7 @@ def run_pipeline(scan: ScanGrid, cfg: PipelineConfig, interval: int | None = Non
     return PipelineResult(labels=labels, normals=NormalMap(values=vals, mask=m), mesh=mesh, timings_ms=timings)
 
 
-_SCAN_BUFS: dict = {}
+_SCAN_BUFS = threading.local()
 
 
 class BatchPipeline:
