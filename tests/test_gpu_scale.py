@@ -210,3 +210,33 @@ def test_chunked_streamed_batches_match_single_batch(L, oracle, S):
         sp.run_host(hx, hr, ho, hl)
         torch.cuda.synchronize()
         assert torch.equal(hl, want.cpu())
+
+
+def test_single_scan_api_concurrent_threads(L):
+    """run_pipeline from two threads at once (the reference's functions are
+    pure and safe to call concurrently): each thread gets its
+    own device buffers, results equal the sequential ones."""
+    import threading
+    g1, g2 = load_golden("vlp16_k1"), load_golden("vlp16_k5")
+    cfg = L.SensorConfig(ring_elevations=g1["elev"], azimuth_steps=int(g1["steps"]), r_min=float(g1["r_min"]),
+                         r_max=float(g1["r_max"]))
+    grids = [L.ScanGrid(config=cfg, ranges=g1["ranges"]), L.ScanGrid(config=cfg, ranges=g2["ranges"] * 1.01)]
+    pc = L.PipelineConfig(sensor=cfg, interval=1)
+    want = [L.run_pipeline(g, pc).labels for g in grids]
+    errors = []
+
+    def work(i):
+        try:
+            for _ in range(10):
+                if not np.array_equal(L.run_pipeline(grids[i], pc).labels, want[i]):
+                    errors.append(i)
+        except Exception as exc:  # noqa: BLE001
+            errors.append(repr(exc))
+
+    th = [threading.Thread(target=work, args=(i,)) for i in (0, 1)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    np.testing.assert_array_equal(want[0], g1["labels"])
