@@ -69,6 +69,9 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_GEN_SUBST
 #define LSEG_GEN_SUBST 1  // general-slot nodes: straight-line six-slot fan with absent slots substituted
 #endif
+#ifndef LSEG_D_BF
+#define LSEG_D_BF 1  // branch-free homogeneity tests in k_tile's mask phase
+#endif
 #ifndef LSEG_BN_SEP
 #define LSEG_BN_SEP 1  // border fp64 normals written by a separate border-cell pass
 #endif
@@ -472,6 +475,27 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       const int e = y * TC + x;
       bool h = false, v0 = false, v1 = false;
       const bool has = (y < TRe) && s_has[e];
+#if LSEG_D_BF
+      // branch-free: every test runs (an absent partner reads the node's own
+      // normal, a test that is then masked off), no short-circuit
+      {
+        const bool ph = has && x + 1 < TCe && s_has[e + 1];
+        const bool pv0 = has && y + 1 < TRe && s_has[e + TC];
+        const bool pv1 = has && y + 1 < TRe && x + 1 < TCe && s_has[e + TC + 1];
+        const double ax = s_nx[e], ay = s_ny[e], az = s_nz[e];
+        auto pass = [&](int q) -> bool {
+          const bool c0 = fabs(__dsub_rn(s_nx[q], ax)) < t0;
+          const bool c1 = fabs(__dsub_rn(s_ny[q], ay)) < t1;
+          const bool c2 = fabs(__dsub_rn(s_nz[q], az)) < t2;
+          return c0 & c1 & c2;
+        };
+        h = ph & pass(ph ? e + 1 : e);
+        v0 = pv0 & pass(pv0 ? e + TC : e);
+        v1 = pv1 & pass(pv1 ? e + TC + 1 : e);
+      }
+      if (has && full_width && x == TCe - 1) {  // the column wrap of a full-width tile (rare)
+        const double a[3] = {s_nx[e], s_ny[e], s_nz[e]};
+#else
       if (has) {
         const double a[3] = {s_nx[e], s_ny[e], s_nz[e]};
         if (x + 1 < TCe && s_has[e + 1]) {
@@ -488,6 +512,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
             v1 = normals_pass(a, q, t0, t1, t2);
           }
         }
+#endif
         if (full_width && x == TCe - 1) {
           const int e0 = y * TC;  // (y, 0)
           if (TCe > 1 && s_has[e0]) {
