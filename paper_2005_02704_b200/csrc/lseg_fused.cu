@@ -63,6 +63,9 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_PF_LAB
 #define LSEG_PF_LAB 2
 #endif
+#ifndef LSEG_PRUNE_BATCH_A
+#define LSEG_PRUNE_BATCH_A 1  // pruning phase A: root bits + histogram reads batched per warp
+#endif
 #ifndef LSEG_PF_PRUNE
 #define LSEG_PF_PRUNE 8
 #endif
@@ -1687,6 +1690,7 @@ __global__ void __launch_bounds__(T, LSEG_LAB_TSM / T) k_labels_backfill(lseg_se
   const int S = sh.S, Sk = sh.Sk, k = sh.k, nwk = sh.Wk, nw = (S + 31) / 32;
   int* s_kv = s_dynrow;                                                 // per kept column
   uint32_t* s_kdm = reinterpret_cast<uint32_t*>(s_dynrow + nwk * 32);  // donor columns
+  uint32_t* s_ktw = s_kdm + nwk;                                        // k = 1: backfill-target columns
   __shared__ int s_any;
   const int row = blockIdx.x;
   const int f = row / sh.R, i = row - f * sh.R;
@@ -1755,6 +1759,8 @@ __global__ void __launch_bounds__(T, LSEG_LAB_TSM / T) k_labels_backfill(lseg_se
       if ((c & 31) == 0) s_kdm[c >> 5] = dm;
       any |= dm != 0;
       if (direct) {  // k = 1: every cell but the backfill targets is final here
+        const uint32_t tm = __ballot_sync(0xffffffffu, v == -2);
+        if ((c & 31) == 0) s_ktw[c >> 5] = tm;
         if (c < S && v != -2) out[(int64_t)row * S + c] = v > 0 ? v : 0;
         hist_add(hist + (int64_t)f * K, v > 0 ? v : 0);
       }
@@ -1768,8 +1774,9 @@ __global__ void __launch_bounds__(T, LSEG_LAB_TSM / T) k_labels_backfill(lseg_se
   int32_t* hw = hist + (int64_t)f * K;
   // s / k as a multiply-high: exact for s < 2^32 / k (S <= 16384 here)
   const unsigned kmag = 0xffffffffu / (unsigned)k + 1u;
+  // k = 1: only the words holding backfill targets (one shared load per word)
   for (int s = threadIdx.x; s < nw * 32; s += T) {  // whole warps (hist_add)
-    if (direct && !__any_sync(0xffffffffu, s < S && s_kv[s] == -2)) continue;  // warp-uniform
+    if (direct && s_ktw[s >> 5] == 0u) continue;  // warp-uniform
     int r = 0;
     if (s < S) {
       const int c = (k == 1) ? s : (int)__umulhi((unsigned)s, kmag);
@@ -2136,6 +2143,7 @@ __global__ void __launch_bounds__(T, LSEG_PRUNE_TSM / T) k_prune_rows(Shape sh, 
   uint32_t* s_sb = reinterpret_cast<uint32_t*>(s_wc + sh.Wk);  // survivor bits of the row
   short* s_pw = reinterpret_cast<short*>(s_sb + sh.Wk);  // nearest donor word at / before each word (cyclic)
   short* s_nx = s_pw + nw;                              // ... at / after
+  uint32_t* s_rbw = reinterpret_cast<uint32_t*>(s_nx + nw);  // the row's root bits (s_pw is 4-B aligned, 2 nw shorts)
   __shared__ int s_any, s_row, s_base, s_part[NW];
   if (threadIdx.x == 0) {
     s_row = atomicAdd(ticket, 1);
@@ -2151,8 +2159,39 @@ __global__ void __launch_bounds__(T, LSEG_PRUNE_TSM / T) k_prune_rows(Shape sh, 
   // histogram reads of a word are one coalesced load)
   {
     const int32_t* hf = hist + (int64_t)f * K + (int64_t)i * sh.Sk + 1;
+#if LSEG_PRUNE_BATCH_A
+    // the warp's words are w = warp + NW q: lane q loads word q's root bits,
+    // then the histogram reads go out PA words at a time (3 dependent loads
+    // per 32 words instead of 2 per word)
+    constexpr int PA = 4;
+    for (int wb = warp; wb < sh.Wk; wb += NW * 32) {
+      const int wl = wb + lane * NW;
+      const uint32_t rbl = wl < sh.Wk ? __ldg(rbits + (int64_t)row * sh.Wk + wl) : 0u;
+      if (wl < sh.Wk) s_rbw[wl] = rbl;
+      for (int q0 = 0; q0 < 32 && wb + q0 * NW < sh.Wk; q0 += PA) {
+        uint32_t rq[PA];
+        int hv[PA];
+#pragma unroll
+        for (int j = 0; j < PA; ++j) {
+          rq[j] = __shfl_sync(0xffffffffu, rbl, q0 + j);
+          hv[j] = ((rq[j] >> lane) & 1u) ? __ldcg(hf + (wb + (q0 + j) * NW) * 32 + lane) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < PA; ++j) {
+          const int w = wb + (q0 + j) * NW;
+          const bool surv = ((rq[j] >> lane) & 1u) && !((min_size > 0) && (hv[j] < min_size));
+          const uint32_t b = __ballot_sync(0xffffffffu, surv);
+          if (lane == 0 && w < sh.Wk) {
+            s_sb[w] = b;
+            s_wc[w] = __popc(b);
+          }
+        }
+      }
+    }
+#else
     for (int w = warp; w < sh.Wk; w += NW) {
       const uint32_t rb = __ldg(rbits + (int64_t)row * sh.Wk + w);
+      s_rbw[w] = rb;
       bool surv = false;
       if ((rb >> lane) & 1u) surv = !((min_size > 0) && (__ldcg(hf + w * 32 + lane) < min_size));
       const uint32_t b = __ballot_sync(0xffffffffu, surv);
@@ -2161,6 +2200,7 @@ __global__ void __launch_bounds__(T, LSEG_PRUNE_TSM / T) k_prune_rows(Shape sh, 
         s_wc[w] = __popc(b);
       }
     }
+#endif
     __syncthreads();
     // row-local exclusive prefix over the words: each warp scans a
     // contiguous block of words, then the block totals are offset
@@ -2208,7 +2248,7 @@ __global__ void __launch_bounds__(T, LSEG_PRUNE_TSM / T) k_prune_rows(Shape sh, 
   {
     const int base = s_base;
     for (int w = warp; w < sh.Wk; w += NW) {
-      const uint32_t rb = __ldg(rbits + (int64_t)row * sh.Wk + w);
+      const uint32_t rb = s_rbw[w];
       if ((rb >> lane) & 1u) {
         const uint32_t sb = s_sb[w], bit = 1u << lane;
         rmf[i * sh.Sk + w * 32 + lane] = (sb & bit) ? 1 + base + s_wc[w] + __popc(sb & (bit - 1u)) : -2;
@@ -2300,7 +2340,7 @@ void launch_prune_fused(const Shape& sh, const Workspace& ws, int32_t min_size, 
   // scans) use 256 threads per row to cut the per-row latency
   const bool wide = (int64_t)sh.F * sh.R < num_sms() * 8;
   const int nwr = (sh.S + 31) / 32;
-  const size_t smem = sizeof(int) * ((size_t)nwr * 33 + 2 * (size_t)sh.Wk) + sizeof(short) * 2 * (size_t)nwr;
+  const size_t smem = sizeof(int) * ((size_t)nwr * 33 + 3 * (size_t)sh.Wk) + sizeof(short) * 2 * ((size_t)nwr + 1);
   if (smem > 48 * 1024)
     for (auto fn : {k_prune_rows<128>, k_prune_rows<256>})
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -2394,7 +2434,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
     }
   }
   // labels + backfill -> lab_tmp (+ histogram)
-  const size_t smem = sizeof(int) * (size_t)sh.Wk * 33;
+  const size_t smem = sizeof(int) * (size_t)sh.Wk * 34;
   const uint32_t* fb = (sh.k > 1 && fbits_valid) ? ws.fbits : nullptr;
   const bool wide = (int64_t)sh.F * sh.R < num_sms() * 8;  // one-wave batches: 256 threads per row for latency
   const bool direct = sh.k == 1 && !node_labels;
