@@ -72,6 +72,12 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_GEN_SUBST
 #define LSEG_GEN_SUBST 1  // general-slot nodes: straight-line six-slot fan with absent slots substituted
 #endif
+#ifndef LSEG_HALO_ROWS
+#define LSEG_HALO_ROWS 1  // k_tile halo staged by (column, row group) with per-row pointers
+#endif
+#ifndef LSEG_CC_OUT2
+#define LSEG_CC_OUT2 1  // k_tile_cc: per-tile base pointers for the parent / histogram / root-bit writes
+#endif
 #ifndef LSEG_D_BF
 #define LSEG_D_BF 1  // branch-free homogeneity tests in k_tile's mask phase
 #endif
@@ -208,6 +214,78 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   // A. halo positions dir*r (reference product order) and node ids (-1 absent).
   // All of a thread's loads are issued before any is used (one memory round
   // trip for the whole halo instead of one per cell).
+#if LSEG_HALO_ROWS
+  // row-structured: thread (column xi, row group g) loads rows g, g + NG, ...
+  // of tile column xi (per-thread column offsets, one row pointer per row),
+  // then threads 0 .. 2 GR - 1 load the two halo columns
+  {
+    static_assert(T % TC == 0, "whole row groups");
+    constexpr int NG = T / TC, NRA = (GR + NG - 1) / NG;
+    const int xi = tid % TC, g = tid / TC;
+    const bool colok = xi < TCe;
+    const int cc = c0 + (colok ? xi : 0);
+    const int64_t coff = (int64_t)cc * sh.k;
+    const int wo = cc >> 5;
+    const uint32_t bit = 1u << (cc & 31);
+    double rv[NRA];
+    uint32_t wv[NRA];
+    int32_t pv[NRA];
+#pragma unroll
+    for (int j = 0; j < NRA; ++j) {
+      const int y = g + NG * j, rr = r0 - 1 + y;
+      rv[j] = 0.0;
+      wv[j] = 0u;
+      pv[j] = 0;
+      if (y < GR && colok && rr >= 0 && rr < sh.R) {
+        rv[j] = __ldg(rf + (int64_t)rr * sh.S + coff);
+        wv[j] = __ldg(vbf + (int64_t)rr * sh.Wk + wo);
+        pv[j] = __ldg(wpf + (int64_t)rr * sh.Wk + wo);
+      }
+    }
+    // halo columns: halo index 0 = column c0 - 1, index TCe + 1 = column
+    // c0 + TCe (both cyclic)
+    const bool hthr = tid < 2 * GR;
+    const int hy = tid >> 1, hside = tid & 1, hrr = r0 - 1 + hy;
+    const int hcol = hside ? (c0 + TCe == sh.Sk ? 0 : c0 + TCe) : (c0 == 0 ? sh.Sk - 1 : c0 - 1);
+    double hr = 0.0;
+    uint32_t hw = 0u;
+    int32_t hp = 0;
+    if (hthr && hrr >= 0 && hrr < sh.R) {
+      hr = __ldg(rf + (int64_t)hrr * sh.S + (int64_t)hcol * sh.k);
+      hw = __ldg(vbf + (int64_t)hrr * sh.Wk + (hcol >> 5));
+      hp = __ldg(wpf + (int64_t)hrr * sh.Wk + (hcol >> 5));
+    }
+#pragma unroll
+    for (int j = 0; j < NRA; ++j) {
+      const int y = g + NG * j;
+      if (y < GR && colok) {
+        const int id = (wv[j] & bit) ? pv[j] + __popc(wv[j] & (bit - 1u)) : -1;
+        const int e = y * GC + xi + 1;
+        s_r[e] = id >= 0 ? rv[j] : 0.0;
+        s_id[e] = id;
+      }
+    }
+    if (hthr) {
+      const uint32_t hb = 1u << (hcol & 31);
+      const int id = (hw & hb) ? hp + __popc(hw & (hb - 1u)) : -1;
+      const int e = hy * GC + (hside ? TCe + 1 : 0);
+      s_r[e] = id >= 0 ? hr : 0.0;
+      s_id[e] = id;
+    }
+    for (int e = tid; e < GR + GC; e += T) {
+      if (e < GR) {
+        const int rr = min(max(r0 - 1 + e, 0), sh.R - 1);
+        s_ct[e] = __ldg(sn.cos_el + rr);
+        s_st[e] = __ldg(sn.sin_el + rr);
+      } else {
+        int c = (c0 - 1 + (e - GR)) % sh.Sk;
+        if (c < 0) c += sh.Sk;
+        s_cp[e - GR] = __ldg(sn.cos_az + (int64_t)c * sh.k);
+        s_sp[e - GR] = __ldg(sn.sin_az + (int64_t)c * sh.k);
+      }
+    }
+  }
+#else
   {
     constexpr int NA = (GR * GC + T - 1) / T;
     double rv[NA];
@@ -251,6 +329,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       }
     }
   }
+#endif
   __syncthreads();
   PH_MARK(1);
 
@@ -1338,6 +1417,30 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
   // (cells that are their own root) also get a bit in `lroots`, so the global
   // flatten only has to chase those
   const int64_t nbase = (int64_t)f * sh.cap;
+#if LSEG_CC_OUT2
+  // frame-local cell of the tile's first cell; per-tile base pointers
+  const int tbase = r0 * sh.Sk + c0;
+  int32_t* pbase = parent + nbase + tbase;
+  int32_t* hbase = hist ? hist + (int64_t)f * K + 1 + tbase : nullptr;
+  uint32_t* lbase = lroots + ((int64_t)f * sh.R + r0) * sh.Wk + (c0 >> 5);
+  const int wrem = sh.Wk - (c0 >> 5);  // words of the row from the tile's first
+  for (int e = threadIdx.x; e < NT; e += T) {  // NT is a multiple of T: whole warps
+    const int y = e / TC, x = e - y * TC;
+    const bool in = (y < TRe && x < TCe);
+    const int loc = y * sh.Sk + x;
+    int pc = -1;
+    if (in && ((s_m[y * 5 + 3] >> x) & 1ull)) {
+      const int lr = s_par[s_par[e]];  // run start -> its label
+      pc = tbase + (lr / TC) * sh.Sk + lr % TC;
+    }
+    const bool isroot = in && pc == tbase + loc;
+    if (in) pbase[loc] = pc;
+    if (hbase && isroot) hbase[loc] = 0;
+    const uint32_t b = __ballot_sync(0xffffffffu, isroot);
+    if ((threadIdx.x & 31) == 0 && y < TRe && (x >> 5) < wrem) lbase[y * sh.Wk + (x >> 5)] = b;
+  }
+  if (false)
+#endif
   for (int e = threadIdx.x; e < NT; e += T) {  // NT is a multiple of T: whole warps
     const int y = e / TC, x = e - y * TC;
     const bool in = (y < TRe && x < TCe);
