@@ -78,6 +78,9 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_CC_OUT2
 #define LSEG_CC_OUT2 1  // k_tile_cc: per-tile base pointers for the parent / histogram / root-bit writes
 #endif
+#ifndef LSEG_W_UNIFORM
+#define LSEG_W_UNIFORM 1  // k_tile mask phase: wrap-bit ballots only in full-width tiles
+#endif
 #ifndef LSEG_D_BF
 #define LSEG_D_BF 1  // branch-free homogeneity tests in k_tile's mask phase
 #endif
@@ -613,7 +616,13 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       V1 |= (unsigned long long)__ballot_sync(0xffffffffu, v1) << sh_;
       HS |= (unsigned long long)__ballot_sync(0xffffffffu, has) << sh_;
     }
+#if LSEG_W_UNIFORM
+    unsigned W = 0u;
+    if (full_width)  // block-uniform: the wrap bits exist only in a full-width tile
+      W = (__ballot_sync(0xffffffffu, w0) ? 1u : 0u) | (__ballot_sync(0xffffffffu, w1) ? 2u : 0u);
+#else
     const unsigned W = (__ballot_sync(0xffffffffu, w0) ? 1u : 0u) | (__ballot_sync(0xffffffffu, w1) ? 2u : 0u);
+#endif
     if (lane == 0) {
       mrow[y * 5 + 0] = H;
       mrow[y * 5 + 1] = V0;
@@ -1796,7 +1805,7 @@ __global__ void __launch_bounds__(T, LSEG_LAB_TSM / T) k_labels_backfill(lseg_se
   uint32_t* s_ktw = s_kdm + nwk;                                        // k = 1: backfill-target columns
   __shared__ int s_any;
   const int row = blockIdx.x;
-  const int f = row / sh.R, i = row - f * sh.R;
+  const int f = fdiv(row, sh.R, sh.inv_R), i = row - f * sh.R;
   const uint32_t* vbr = vbits + (int64_t)row * sh.Wk;
   const uint32_t* fbr = fbits ? fbits + (int64_t)row * nw : nullptr;
   const int32_t* parf = parent + (int64_t)f * sh.cap;
@@ -2254,7 +2263,7 @@ __global__ void __launch_bounds__(T, LSEG_PRUNE_TSM / T) k_prune_rows(Shape sh, 
   }
   __syncthreads();
   const int row = s_row;
-  const int f = row / sh.R, i = row - f * sh.R;
+  const int f = fdiv(row, sh.R, sh.inv_R), i = row - f * sh.R;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const volatile int32_t* rs = rstat + (int64_t)f * sh.R;
   int32_t* rmf = remap + (int64_t)f * K;
