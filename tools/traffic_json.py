@@ -43,6 +43,14 @@ def main(path, frames, interval, source, full_raw=None):
                                     "dram_read": rd, "dram_write": wr, "dram_bytes_per_launch": rd + wr,
                                     "ncu_ms_per_launch": sum(m["gpu__time_duration.sum"]) / n / 1e6,
                                     "launches": n, "source": source}
+    if full_raw:  # the dominant kernel's limiter from its full capture (bench.py: roofline.limiter)
+        rows = list(csv.reader(open(full_raw)))
+        d = dict(zip(rows[0], rows[2]))
+        key = f"tile@k{interval}"
+        if key in out:
+            out[key]["fp64_pipe_active"] = float(d["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]) / 100
+            out[key]["issue_active"] = float(d["smsp__issue_active.avg.pct_of_peak_sustained_active"]) / 100
+            out[key]["limiter_source"] = full_raw
     json.dump(out, open(out_path, "w"), indent=1)
     print("wrote", out_path, sorted(k for k in out if not k.startswith("_")))
 
