@@ -57,35 +57,11 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #define LSEG_FOLD_FLATTEN 1
 #endif
 // loads in flight per thread in the row kernels (measured: labels 2, pruning 8)
-#ifndef LSEG_GEN_WARP_ROT
-#define LSEG_GEN_WARP_ROT 1
-#endif
 #ifndef LSEG_PF_LAB
 #define LSEG_PF_LAB 2
 #endif
-#ifndef LSEG_PRUNE_BATCH_A
-#define LSEG_PRUNE_BATCH_A 1  // pruning phase A: root bits + histogram reads batched per warp
-#endif
 #ifndef LSEG_PF_PRUNE
 #define LSEG_PF_PRUNE 8
-#endif
-#ifndef LSEG_GEN_SUBST
-#define LSEG_GEN_SUBST 1  // general-slot nodes: straight-line six-slot fan with absent slots substituted
-#endif
-#ifndef LSEG_HALO_ROWS
-#define LSEG_HALO_ROWS 1  // k_tile halo staged by (column, row group) with per-row pointers
-#endif
-#ifndef LSEG_CC_OUT2
-#define LSEG_CC_OUT2 1  // k_tile_cc: per-tile base pointers for the parent / histogram / root-bit writes
-#endif
-#ifndef LSEG_W_UNIFORM
-#define LSEG_W_UNIFORM 1  // k_tile mask phase: wrap-bit ballots only in full-width tiles
-#endif
-#ifndef LSEG_D_BF
-#define LSEG_D_BF 1  // branch-free homogeneity tests in k_tile's mask phase
-#endif
-#ifndef LSEG_BN_SEP
-#define LSEG_BN_SEP 1  // border fp64 normals written by a separate border-cell pass
 #endif
 // resident threads per SM the row kernels are compiled for (2048: 32 registers)
 #ifndef LSEG_CC_TSM
@@ -217,7 +193,6 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   // A. halo positions dir*r (reference product order) and node ids (-1 absent).
   // All of a thread's loads are issued before any is used (one memory round
   // trip for the whole halo instead of one per cell).
-#if LSEG_HALO_ROWS
   // row-structured: thread (column xi, row group g) loads rows g, g + NG, ...
   // of tile column xi (per-thread column offsets, one row pointer per row),
   // then threads 0 .. 2 GR - 1 load the two halo columns
@@ -288,51 +263,6 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       }
     }
   }
-#else
-  {
-    constexpr int NA = (GR * GC + T - 1) / T;
-    double rv[NA];
-    uint32_t wv[NA];
-    int32_t pv[NA];
-#pragma unroll
-    for (int j = 0; j < NA; ++j) {
-      const int e = tid + j * T;
-      const int y = e / GC, x = e - y * GC;
-      const int rr = r0 - 1 + y;
-      rv[j] = 0.0;
-      wv[j] = 0u;
-      pv[j] = 0;
-      if (e < GR * GC && rr >= 0 && rr < sh.R) {
-        const int cc = wrapc(c0 - 1 + x, sh.Sk);
-        rv[j] = __ldg(rf + (int64_t)rr * sh.S + (int64_t)cc * sh.k);
-        wv[j] = __ldg(vbf + (int64_t)rr * sh.Wk + (cc >> 5));
-        pv[j] = __ldg(wpf + (int64_t)rr * sh.Wk + (cc >> 5));
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < NA; ++j) {
-      const int e = tid + j * T;
-      if (e >= GR * GC) break;
-      const int y = e / GC, x = e - y * GC;
-      const int cc = wrapc(c0 - 1 + x, sh.Sk);
-      const uint32_t bit = 1u << (cc & 31);
-      const int id = (wv[j] & bit) ? pv[j] + __popc(wv[j] & (bit - 1u)) : -1;
-      s_r[e] = id >= 0 ? rv[j] : 0.0;
-      s_id[e] = id;
-    }
-    for (int e = tid; e < GR + GC; e += T) {
-      if (e < GR) {
-        const int rr = min(max(r0 - 1 + e, 0), sh.R - 1);
-        s_ct[e] = __ldg(sn.cos_el + rr);
-        s_st[e] = __ldg(sn.sin_el + rr);
-      } else {
-        const int cc = wrapc(c0 - 1 + (e - GR), sh.Sk) * sh.k;
-        s_cp[e - GR] = __ldg(sn.cos_az + cc);
-        s_sp[e - GR] = __ldg(sn.sin_az + cc);
-      }
-    }
-  }
-#endif
   __syncthreads();
   PH_MARK(1);
 
@@ -416,18 +346,13 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   }
   // the general nodes start at the first warp after the last fan6 node's
   // warp, i.e. on the warps with one fan6 node fewer per lane
-#if LSEG_GEN_WARP_ROT
   const int gstart = (((nfan6 % T) + 31) & ~31) % T;
   for (int i = (tid - gstart + T) % T; i < ngen; i += T) {
-#else
-  for (int i = tid; i < ngen; i += T) {
-#endif
     const int e = s_list[NT - 1 - i];
     const int y = e / TC, x = e - y * TC;
     const unsigned m = s_m[e];
     const Vec3 p = posyx(y + 1, x + 1);
     double nv[3];
-#if LSEG_GEN_SUBST
     // straight-line six-slot sequence with absent slots substituted
     // (fan_subst): slot s -> (row, column) offsets from packed tables
     // (dr + 1, dc + 1 in 2-bit fields)
@@ -436,20 +361,6 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       return posyx(y + 1 + dr, x + 1 + dc);
     };
     if (fan_subst<kFastMath>(p, m, pos, nv)) {
-#else
-    FanT<kFastMath> fan;
-#pragma unroll
-    for (int s = 0; s < 6; ++s) {
-      if (!((m >> s) & 1u)) continue;
-      // (row, column) through the flat index on purpose: the direct
-      // posyx(y + 1 + dr, x + 1 + dc) measured 1.3 % slower (register allocation)
-      const int gq = (y + 1 + slot_dr(s)) * GC + x + 1 + slot_dc(s);
-      const int yq = gq / GC;
-      const Vec3 q = posyx(yq, gq - yq * GC);
-      fan.add(__dsub_rn(q.x, p.x), __dsub_rn(q.y, p.y), __dsub_rn(q.z, p.z));
-    }
-    if (fan.finish(p, nv)) {
-#endif
       s_nx[e] = nv[0];
       s_ny[e] = nv[1];
       s_nz[e] = nv[2];
@@ -497,18 +408,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       o[2] = has ? s_nz[e] : qn;
     }
     nmask[nbase + id] = has ? 1 : 0;
-#if !LSEG_BN_SEP
-    if (has) {  // fp64 normals of the tile's border rows / columns for k_merge (coalesced)
-      double* bf = bnorm + (int64_t)f * bn_frame(sh, TR, TC);
-      const int tr = r0 / TR, tc = c0 / TC;
-      if (y == 0) bn_put(bf + bn_row(sh, 2 * tr, cc), s_nx[e], s_ny[e], s_nz[e]);
-      if (y == TRe - 1) bn_put(bf + bn_row(sh, 2 * tr + 1, cc), s_nx[e], s_ny[e], s_nz[e]);
-      if (x == 0) bn_put(bf + bn_col(sh, TR, 2 * tc, rr), s_nx[e], s_ny[e], s_nz[e]);
-      if (x == TCe - 1) bn_put(bf + bn_col(sh, TR, 2 * tc + 1, rr), s_nx[e], s_ny[e], s_nz[e]);
-    }
-#endif
   }
-#if LSEG_BN_SEP
   // fp64 normals of the tile's border rows / columns for k_merge: only the
   // 2 TC + 2 TR border cells, one thread each (row stores coalesced)
   {
@@ -535,7 +435,6 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       bn_put(o, s_nx[e], s_ny[e], s_nz[e]);
     }
   }
-#endif
 
 #if LSEG_PHASES
   __syncthreads();
@@ -560,7 +459,6 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       const int e = y * TC + x;
       bool h = false, v0 = false, v1 = false;
       const bool has = (y < TRe) && s_has[e];
-#if LSEG_D_BF
       // branch-free: every test runs (an absent partner reads the node's own
       // normal, a test that is then masked off), no short-circuit
       {
@@ -580,24 +478,6 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       }
       if (has && full_width && x == TCe - 1) {  // the column wrap of a full-width tile (rare)
         const double a[3] = {s_nx[e], s_ny[e], s_nz[e]};
-#else
-      if (has) {
-        const double a[3] = {s_nx[e], s_ny[e], s_nz[e]};
-        if (x + 1 < TCe && s_has[e + 1]) {
-          const double q[3] = {s_nx[e + 1], s_ny[e + 1], s_nz[e + 1]};
-          h = normals_pass(a, q, t0, t1, t2);
-        }
-        if (y + 1 < TRe) {
-          if (s_has[e + TC]) {
-            const double q[3] = {s_nx[e + TC], s_ny[e + TC], s_nz[e + TC]};
-            v0 = normals_pass(a, q, t0, t1, t2);
-          }
-          if (x + 1 < TCe && s_has[e + TC + 1]) {
-            const double q[3] = {s_nx[e + TC + 1], s_ny[e + TC + 1], s_nz[e + TC + 1]};
-            v1 = normals_pass(a, q, t0, t1, t2);
-          }
-        }
-#endif
         if (full_width && x == TCe - 1) {
           const int e0 = y * TC;  // (y, 0)
           if (TCe > 1 && s_has[e0]) {
@@ -616,13 +496,9 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       V1 |= (unsigned long long)__ballot_sync(0xffffffffu, v1) << sh_;
       HS |= (unsigned long long)__ballot_sync(0xffffffffu, has) << sh_;
     }
-#if LSEG_W_UNIFORM
     unsigned W = 0u;
     if (full_width)  // block-uniform: the wrap bits exist only in a full-width tile
       W = (__ballot_sync(0xffffffffu, w0) ? 1u : 0u) | (__ballot_sync(0xffffffffu, w1) ? 2u : 0u);
-#else
-    const unsigned W = (__ballot_sync(0xffffffffu, w0) ? 1u : 0u) | (__ballot_sync(0xffffffffu, w1) ? 2u : 0u);
-#endif
     if (lane == 0) {
       mrow[y * 5 + 0] = H;
       mrow[y * 5 + 1] = V0;
@@ -966,12 +842,8 @@ __global__ void __launch_bounds__(T, LSEG_CERT_MINB) k_tile_cert(
   for (int i = tid; i < nfan6; i += T) node_normal(s_list[i], 0x3fu);  // straight-line: all six slots
   // the rest from the first warp after the six-slot list's last partial warp
   // (as in k_tile)
-#if LSEG_GEN_WARP_ROT
   const int gstart = (((nfan6 % T) + 31) & ~31) % T;
   for (int i = (tid - gstart + T) % T; i < ngen; i += T) {
-#else
-  for (int i = tid; i < ngen; i += T) {
-#endif
     const int e = s_list[NT - 1 - i];
     node_normal(e, s_m[e]);
   }
@@ -1426,7 +1298,6 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
   // (cells that are their own root) also get a bit in `lroots`, so the global
   // flatten only has to chase those
   const int64_t nbase = (int64_t)f * sh.cap;
-#if LSEG_CC_OUT2
   // frame-local cell of the tile's first cell; per-tile base pointers
   const int tbase = r0 * sh.Sk + c0;
   int32_t* pbase = parent + nbase + tbase;
@@ -1444,28 +1315,11 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
     }
     const bool isroot = in && pc == tbase + loc;
     if (in) pbase[loc] = pc;
+    // histogram slot of every tile-local root zeroed here (a superset of the
+    // final roots k_labels_backfill counts into)
     if (hbase && isroot) hbase[loc] = 0;
     const uint32_t b = __ballot_sync(0xffffffffu, isroot);
     if ((threadIdx.x & 31) == 0 && y < TRe && (x >> 5) < wrem) lbase[y * sh.Wk + (x >> 5)] = b;
-  }
-  if (false)
-#endif
-  for (int e = threadIdx.x; e < NT; e += T) {  // NT is a multiple of T: whole warps
-    const int y = e / TC, x = e - y * TC;
-    const bool in = (y < TRe && x < TCe);
-    int pc = -1;
-    if (in && ((s_m[y * 5 + 3] >> x) & 1ull)) {
-      const int lr = s_par[s_par[e]];  // run start -> its label
-      pc = (r0 + lr / TC) * sh.Sk + c0 + lr % TC;
-    }
-    const int cell = (r0 + y) * sh.Sk + c0 + x;
-    if (in) parent[nbase + cell] = pc;
-    // histogram slot of every tile-local root zeroed here (a superset of the
-    // final roots k_labels_backfill counts into)
-    if (hist && in && pc == cell) hist[(int64_t)f * K + cell + 1] = 0;
-    const uint32_t b = __ballot_sync(0xffffffffu, in && pc == cell);
-    const int word = (c0 + x) >> 5;
-    if ((threadIdx.x & 31) == 0 && y < TRe && word < sh.Wk) lroots[((int64_t)f * sh.R + r0 + y) * sh.Wk + word] = b;
   }
 }
 
@@ -2271,7 +2125,6 @@ __global__ void __launch_bounds__(T, LSEG_PRUNE_TSM / T) k_prune_rows(Shape sh, 
   // histogram reads of a word are one coalesced load)
   {
     const int32_t* hf = hist + (int64_t)f * K + (int64_t)i * sh.Sk + 1;
-#if LSEG_PRUNE_BATCH_A
     // the warp's words are w = warp + NW q: lane q loads word q's root bits,
     // then the histogram reads go out PA words at a time (3 dependent loads
     // per 32 words instead of 2 per word)
@@ -2300,19 +2153,6 @@ __global__ void __launch_bounds__(T, LSEG_PRUNE_TSM / T) k_prune_rows(Shape sh, 
         }
       }
     }
-#else
-    for (int w = warp; w < sh.Wk; w += NW) {
-      const uint32_t rb = __ldg(rbits + (int64_t)row * sh.Wk + w);
-      s_rbw[w] = rb;
-      bool surv = false;
-      if ((rb >> lane) & 1u) surv = !((min_size > 0) && (__ldcg(hf + w * 32 + lane) < min_size));
-      const uint32_t b = __ballot_sync(0xffffffffu, surv);
-      if (lane == 0) {
-        s_sb[w] = b;
-        s_wc[w] = __popc(b);
-      }
-    }
-#endif
     __syncthreads();
     // row-local exclusive prefix over the words: each warp scans a
     // contiguous block of words, then the block totals are offset
