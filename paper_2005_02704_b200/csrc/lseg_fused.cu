@@ -1171,11 +1171,28 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
                                              const unsigned long long* s_m, int* s_par, int32_t* __restrict__ parent,
                                              uint32_t* __restrict__ lroots, int32_t* __restrict__ hist, int64_t K) {
   constexpr int NT = TR * TC;
-  // run starts: parent of every cell = first cell of its horizontal run
-  for (int e = threadIdx.x; e < NT; e += T) {
+  // run starts: parent of every cell = first cell of its horizontal run (the
+  // cell after the highest failing row edge below it), on 32-bit halves of
+  // the row mask: a warp's 32 cells lie in one half (warp-uniform branch)
+  static_assert(NT % T == 0 && TC == 64 && T % 32 == 0, "each warp step covers a 32-cell chunk of one row");
+  constexpr int NJ = NT / T;
+  unsigned starts = 0;  // which of this thread's cells (tid + j T) are run starts
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int e = threadIdx.x + j * T;
     const int y = e / TC, x = e - y * TC;
-    const unsigned long long Z = ~s_m[y * 5] & ((1ull << x) - 1ull);
-    s_par[e] = y * TC + (Z ? 64 - __clzll((long long)Z) : 0);
+    const unsigned long long Hm = s_m[y * 5];
+    const uint32_t hl = (uint32_t)Hm, hh = (uint32_t)(Hm >> 32);
+    int st;
+    if (x < 32) {
+      const uint32_t Z = ~hl & ((1u << x) - 1u);
+      st = Z ? 32 - __clz(Z) : 0;
+    } else {
+      const uint32_t Zh = ~hh & ((1u << (x - 32)) - 1u);
+      st = Zh ? 64 - __clz(Zh) : (~hl ? 32 - __clz(~hl) : 0);
+    }
+    s_par[e] = y * TC + st;
+    if (st == x) starts |= 1u << j;
   }
   __syncthreads();
   // vertical / diagonal unions: an edge is dropped (64-bit mask arithmetic,
@@ -1206,8 +1223,7 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
   // under the smaller, so each root is its component's minimum run start)
   // and compress the run starts -- two barriers, no rounds.
   static_assert(NT <= 1024, "10-bit cell indices");
-  constexpr int NJ = (NT + T - 1) / T;
-  static_assert(NT % T == 0 && TC % 32 == 0, "each warp step covers a 32-cell chunk of one row");
+
   // each warp's edges as a dense list (a | b << 10) in its own shared-memory
   // segment (appended without atomics), then unioned by the same warp:
   // no block barrier between gathering and union.  At step j the warp's
@@ -1219,13 +1235,11 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
   const unsigned lt = (1u << lane) - 1u;
   unsigned* el = s_el + (threadIdx.x >> 5) * SEG;
   int ne = 0;
-  unsigned starts = 0;  // which of this thread's cells are run starts
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
     const int e0 = (threadIdx.x & ~31) + j * T;
     const int y = e0 / TC, x0 = e0 - y * TC;
     const int e = e0 + lane;
-    if (((~(s_m[y * 5] << 1) >> x0) >> lane) & 1ull) starts |= 1u << j;  // x = 0 or no run edge from x - 1
     const unsigned c0 = (unsigned)(s_U[2 * y] >> x0), c1 = (unsigned)(s_U[2 * y + 1] >> x0);
     if (c0 | c1) {  // warp-uniform
       const unsigned a = (unsigned)s_par[e];
