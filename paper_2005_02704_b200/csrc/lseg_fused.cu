@@ -1240,7 +1240,8 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
     const int e0 = (threadIdx.x & ~31) + j * T;
     const int y = e0 / TC, x0 = e0 - y * TC;
     const int e = e0 + lane;
-    const unsigned c0 = (unsigned)(s_U[2 * y] >> x0), c1 = (unsigned)(s_U[2 * y + 1] >> x0);
+    const uint32_t* sU32 = reinterpret_cast<const uint32_t*>(s_U);  // 32-bit halves (little-endian)
+    const unsigned c0 = sU32[4 * y + (x0 >> 5)], c1 = sU32[4 * y + 2 + (x0 >> 5)];
     if (c0 | c1) {  // warp-uniform
       const unsigned a = (unsigned)s_par[e];
       if ((c0 >> lane) & 1u) el[ne + __popc(c0 & lt)] = a | (unsigned)s_par[e + TC] << 10;
@@ -1323,7 +1324,7 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
     const bool in = (y < TRe && x < TCe);
     const int loc = y * sh.Sk + x;
     int pc = -1;
-    if (in && ((s_m[y * 5 + 3] >> x) & 1ull)) {
+    if (in && ((reinterpret_cast<const uint32_t*>(s_m)[(y * 5 + 3) * 2 + (x >> 5)] >> (x & 31)) & 1u)) {
       const int lr = s_par[s_par[e]];  // run start -> its label
       pc = tbase + (lr / TC) * sh.Sk + lr % TC;
     }
