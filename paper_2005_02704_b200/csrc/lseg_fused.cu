@@ -105,9 +105,10 @@ __device__ __forceinline__ bool edge_internal(int r, int c, int s, int Sk) {
 __device__ __forceinline__ int64_t bn_frame(const Shape& sh, int TR, int TC) {
   return ((int64_t)2 * ((sh.R + TR - 1) / TR) * sh.Sk + (int64_t)2 * ((sh.Sk + TC - 1) / TC) * sh.R) * 3;
 }
-__device__ __forceinline__ int64_t bn_row(const Shape& sh, int slot, int c) { return ((int64_t)slot * sh.Sk + c) * 3; }
-__device__ __forceinline__ int64_t bn_col(const Shape& sh, int TR, int slot, int r) {
-  return ((int64_t)2 * ((sh.R + TR - 1) / TR) * sh.Sk + (int64_t)slot * sh.R + r) * 3;
+// (offsets within one frame's store fit 32 bits: 6 (R/TR + S'/TC) doubles per cell row / column)
+__device__ __forceinline__ int bn_row(const Shape& sh, int slot, int c) { return (slot * sh.Sk + c) * 3; }
+__device__ __forceinline__ int bn_col(const Shape& sh, int TR, int slot, int r) {
+  return (2 * ((sh.R + TR - 1) / TR) * sh.Sk + slot * sh.R + r) * 3;
 }
 __device__ __forceinline__ void bn_put(double* o, double a, double b, double c) { o[0] = a; o[1] = b; o[2] = c; }
 
@@ -1405,12 +1406,12 @@ __global__ void k_merge(Shape sh, const double* __restrict__ bnorm, double t0, d
     int r = 0, c = 0, pp = -1;
     if (u < per) {
       if (u < nbr * sh.Sk) {
-        const int br = u / sh.Sk;
+        const int br = fdiv(u, sh.Sk, sh.inv_Sk);
         r = min(br * TR + TR - 1, sh.R - 1);
         c = u - br * sh.Sk;
       } else {
         const int v = u - nbr * sh.Sk;
-        const int bc = v / sh.R;
+        const int bc = fdiv(v, sh.R, sh.inv_R);
         c = min(bc * TC + TC - 1, sh.Sk - 1);
         r = v - bc * sh.R;
       }
