@@ -1679,6 +1679,9 @@ __global__ void __launch_bounds__(T, LSEG_LAB_TSM / T) k_labels_backfill(lseg_se
   const uint32_t* vbr = vbits + (int64_t)row * sh.Wk;
   const uint32_t* fbr = fbits ? fbits + (int64_t)row * nw : nullptr;
   const int32_t* parf = parent + (int64_t)f * sh.cap;
+  // opaque to the optimiser: frame-local indices then cost one wide multiply-add
+  // per load instead of a re-associated 64-bit index computation
+  asm volatile("" : "+l"(parf));
   const int32_t* par = parf + (int64_t)i * sh.Sk;
   const uint32_t* rbf = rbits + (int64_t)f * sh.R * sh.Wk;
   const int32_t* rpf = rpre + (int64_t)f * sh.R * sh.Wk;
@@ -1687,7 +1690,7 @@ __global__ void __launch_bounds__(T, LSEG_LAB_TSM / T) k_labels_backfill(lseg_se
   // output): each column chases its tile-local root to the final root
   // itself, the row's final roots go to rbits_out and n_labels, and the
   // pruning's per-row counters are reset here
-  const bool fold = rbits_out != nullptr;
+  const bool fold = DIRECT || rbits_out != nullptr;  // the direct (k = 1) variant is only launched folded
   // k = 1 without the segment() output: labelled / passive cells are written
   // and counted while the columns are classified; the second pass only
   // handles the backfill targets (valid cells without a normal: rare at k = 1)
@@ -2405,7 +2408,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   const size_t smem = sizeof(int) * (size_t)sh.Wk * 34;
   const uint32_t* fb = (sh.k > 1 && fbits_valid) ? ws.fbits : nullptr;
   const bool wide = (int64_t)sh.F * sh.R < num_sms() * 8;  // one-wave batches: 256 threads per row for latency
-  const bool direct = sh.k == 1 && !node_labels;
+  const bool direct = sh.k == 1 && fold;  // (fold implies no segment() output)
   auto kern = wide ? (direct ? k_labels_backfill<256, true> : k_labels_backfill<256, false>)
                    : (direct ? k_labels_backfill<128, true> : k_labels_backfill<128, false>);
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
