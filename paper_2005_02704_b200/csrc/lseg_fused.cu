@@ -1399,6 +1399,7 @@ __global__ void k_merge(Shape sh, const double* __restrict__ bnorm, double t0, d
   const int per = nbr * sh.Sk + nbc * sh.R;
   int32_t* par = parent + (int64_t)f * sh.cap;
   const double* bn = bnorm + (int64_t)f * bn_frame(sh, TR, TC);
+  asm volatile("" : "+l"(par), "+l"(bn));  // frame bases opaque: one wide multiply-add per access
   const int lane = threadIdx.x & 31;
   // warp-uniform trip count (the dedup below needs whole warps)
   for (int u0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); u0 < per; u0 += gridDim.x * blockDim.x) {
@@ -1681,7 +1682,8 @@ __global__ void __launch_bounds__(T, LSEG_LAB_TSM / T) k_labels_backfill(lseg_se
   const int32_t* parf = parent + (int64_t)f * sh.cap;
   // opaque to the optimiser: frame-local indices then cost one wide multiply-add
   // per load instead of a re-associated 64-bit index computation
-  asm volatile("" : "+l"(parf));
+  int32_t* hw = hist + (int64_t)f * K;
+  asm volatile("" : "+l"(parf), "+l"(hw));
   const int32_t* par = parf + (int64_t)i * sh.Sk;
   const uint32_t* rbf = rbits + (int64_t)f * sh.R * sh.Wk;
   const int32_t* rpf = rpre + (int64_t)f * sh.R * sh.Wk;
@@ -1747,7 +1749,7 @@ __global__ void __launch_bounds__(T, LSEG_LAB_TSM / T) k_labels_backfill(lseg_se
         const uint32_t tm = __ballot_sync(0xffffffffu, v == -2);
         if ((c & 31) == 0) s_ktw[c >> 5] = tm;
         if (c < S && v != -2) out[(int64_t)row * S + c] = v > 0 ? v : 0;
-        hist_add(hist + (int64_t)f * K, v > 0 ? v : 0);
+        hist_add(hw, v > 0 ? v : 0);
       }
     }
   }
@@ -1756,7 +1758,6 @@ __global__ void __launch_bounds__(T, LSEG_LAB_TSM / T) k_labels_backfill(lseg_se
   __syncthreads();
   if (fold && threadIdx.x == 0 && s_nroot) atomicAdd(n_labels + f, s_nroot);
   const bool rany = s_any != 0;
-  int32_t* hw = hist + (int64_t)f * K;
   // s / k as a multiply-high: exact for s < 2^32 / k (S <= 16384 here)
   const unsigned kmag = 0xffffffffu / (unsigned)k + 1u;
   // k = 1: only the words holding backfill targets (one shared load per word)
@@ -2140,6 +2141,7 @@ __global__ void __launch_bounds__(T, LSEG_PRUNE_TSM / T) k_prune_rows(Shape sh, 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const volatile int32_t* rs = rstat + (int64_t)f * sh.R;
   int32_t* rmf = remap + (int64_t)f * K;
+  asm volatile("" : "+l"(rmf));  // frame base opaque: one wide multiply-add per lookup
   // A. survivors of this row's roots, one warp per 32-cell word (the
   // histogram reads of a word are one coalesced load)
   {
