@@ -1314,20 +1314,26 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
   // (cells that are their own root) also get a bit in `lroots`, so the global
   // flatten only has to chase those
   const int64_t nbase = (int64_t)f * sh.cap;
-  // frame-local cell of the tile's first cell; per-tile base pointers
-  const int tbase = r0 * sh.Sk + c0;
+  // frame-local cell of the tile's first cell; per-tile base pointers, opaque
+  // to the optimiser (32-bit tile-local offsets: one wide multiply-add per store)
+  const int Sk = sh.Sk, Wk = sh.Wk;
+  const int tbase = r0 * Sk + c0;
   int32_t* pbase = parent + nbase + tbase;
   int32_t* hbase = hist ? hist + (int64_t)f * K + 1 + tbase : nullptr;
-  uint32_t* lbase = lroots + ((int64_t)f * sh.R + r0) * sh.Wk + (c0 >> 5);
-  const int wrem = sh.Wk - (c0 >> 5);  // words of the row from the tile's first
-  for (int e = threadIdx.x; e < NT; e += T) {  // NT is a multiple of T: whole warps
+  uint32_t* lbase = lroots + ((int64_t)f * sh.R + r0) * Wk + (c0 >> 5);
+  asm volatile("" : "+l"(pbase), "+l"(hbase), "+l"(lbase));
+  const int wrem = Wk - (c0 >> 5);  // words of the row from the tile's first
+  const uint32_t* sm32 = reinterpret_cast<const uint32_t*>(s_m);
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {  // whole warps: cell e = tid + j T, one 32-cell half-row per warp
+    const int e = threadIdx.x + j * T;
     const int y = e / TC, x = e - y * TC;
     const bool in = (y < TRe && x < TCe);
-    const int loc = y * sh.Sk + x;
+    const int loc = y * Sk + x;
     int pc = -1;
-    if (in && ((reinterpret_cast<const uint32_t*>(s_m)[(y * 5 + 3) * 2 + (x >> 5)] >> (x & 31)) & 1u)) {
+    if (in && ((sm32[(y * 5 + 3) * 2 + (x >> 5)] >> (x & 31)) & 1u)) {
       const int lr = s_par[s_par[e]];  // run start -> its label
-      pc = tbase + (lr / TC) * sh.Sk + lr % TC;
+      pc = tbase + (lr / TC) * Sk + lr % TC;
     }
     const bool isroot = in && pc == tbase + loc;
     if (in) pbase[loc] = pc;
@@ -1335,7 +1341,7 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
     // final roots k_labels_backfill counts into)
     if (hbase && isroot) hbase[loc] = 0;
     const uint32_t b = __ballot_sync(0xffffffffu, isroot);
-    if ((threadIdx.x & 31) == 0 && y < TRe && (x >> 5) < wrem) lbase[y * sh.Wk + (x >> 5)] = b;
+    if ((threadIdx.x & 31) == 0 && y < TRe && (x >> 5) < wrem) lbase[y * Wk + (x >> 5)] = b;
   }
 }
 
