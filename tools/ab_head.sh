@@ -3,6 +3,7 @@
 # the parity tests and tools/variants2.sh base old.   bash tools/ab_head.sh [TIMEOUT]
 set -e
 cd "$(dirname "$0")/.."
+if git diff --quiet; then echo "no working-tree changes to compare"; exit 1; fi
 git stash -q
 python -c "from paper_2005_02704_b200 import _build; _build.build(force=True, out='paper_2005_02704_b200/liblidarseg_b200_old.so')"
 git stash pop -q
