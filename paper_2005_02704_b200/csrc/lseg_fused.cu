@@ -1184,14 +1184,11 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
     const int y = e / TC, x = e - y * TC;
     const unsigned long long Hm = s_m[y * 5];
     const uint32_t hl = (uint32_t)Hm, hh = (uint32_t)(Hm >> 32);
-    int st;
-    if (x < 32) {
-      const uint32_t Z = ~hl & ((1u << x) - 1u);
-      st = Z ? 32 - __clz(Z) : 0;
-    } else {
-      const uint32_t Zh = ~hh & ((1u << (x - 32)) - 1u);
-      st = Zh ? 64 - __clz(Zh) : (~hl ? 32 - __clz(~hl) : 0);
-    }
+    // branch-free: the cell's own half first, then (upper half) the lower one
+    const bool up = x >= 32;
+    const uint32_t Z = ~(up ? hh : hl) & ((1u << (x & 31)) - 1u);
+    const int lowst = (up && ~hl) ? 32 - __clz(~hl) : 0;
+    const int st = Z ? (up ? 64 : 32) - __clz(Z) : lowst;
     s_par[e] = y * TC + st;
     if (st == x) starts |= 1u << j;
   }
