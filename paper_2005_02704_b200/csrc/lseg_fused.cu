@@ -1240,13 +1240,12 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
     const int e = e0 + lane;
     const uint32_t* sU32 = reinterpret_cast<const uint32_t*>(s_U);  // 32-bit halves (little-endian)
     const unsigned c0 = sU32[4 * y + (x0 >> 5)], c1 = sU32[4 * y + 2 + (x0 >> 5)];
-    if (c0 | c1) {  // warp-uniform
-      const unsigned a = (unsigned)s_par[e];
-      if ((c0 >> lane) & 1u) el[ne + __popc(c0 & lt)] = a | (unsigned)s_par[e + TC] << 10;
-      ne += __popc(c0);
-      if ((c1 >> lane) & 1u) el[ne + __popc(c1 & lt)] = a | (unsigned)s_par[e + TC + 1] << 10;
-      ne += __popc(c1);
-    }
+    // unconditional (chunks without edges are rare; no branch / reconvergence)
+    const unsigned a = (unsigned)s_par[e];
+    if ((c0 >> lane) & 1u) el[ne + __popc(c0 & lt)] = a | (unsigned)s_par[min(e + TC, NT - 1)] << 10;
+    ne += __popc(c0);
+    if ((c1 >> lane) & 1u) el[ne + __popc(c1 & lt)] = a | (unsigned)s_par[min(e + TC + 1, NT - 1)] << 10;
+    ne += __popc(c1);
   }
   // full-width column wrap (x = S'-1 -> 0), added by the last warp (fewest
   // edges: it holds row TR-1)
