@@ -1242,9 +1242,10 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
     const unsigned c0 = sU32[4 * y + (x0 >> 5)], c1 = sU32[4 * y + 2 + (x0 >> 5)];
     // unconditional (chunks without edges are rare; no branch / reconvergence)
     const unsigned a = (unsigned)s_par[e];
-    if ((c0 >> lane) & 1u) el[ne + __popc(c0 & lt)] = a | (unsigned)s_par[min(e + TC, NT - 1)] << 10;
+    // (the last row's reads past the tile land in s_par's padding: unused)
+    if ((c0 >> lane) & 1u) el[ne + __popc(c0 & lt)] = a | (unsigned)s_par[e + TC] << 10;
     ne += __popc(c0);
-    if ((c1 >> lane) & 1u) el[ne + __popc(c1 & lt)] = a | (unsigned)s_par[min(e + TC + 1, NT - 1)] << 10;
+    if ((c1 >> lane) & 1u) el[ne + __popc(c1 & lt)] = a | (unsigned)s_par[e + TC + 1] << 10;
     ne += __popc(c1);
   }
   // full-width column wrap (x = S'-1 -> 0), added by the last warp (fewest
@@ -1347,7 +1348,7 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
 template <int TR, int TC, int T>
 __global__ void k_tile_cc_dbg(Shape sh, const unsigned long long* __restrict__ masks, int32_t* parent,
                               uint32_t* lroots) {
-  __shared__ int s_par[TR * TC];
+  __shared__ int s_par[TR * TC + TC + 1];  // + padding: the edge gathering's reads below the last row
   __shared__ unsigned long long s_m[TR * 5];
   const int f = blockIdx.x;
   for (int j = threadIdx.x; j < TR * 5; j += T) s_m[j] = masks[(int64_t)f * TR * 5 + j];
@@ -1365,7 +1366,7 @@ __global__ void __launch_bounds__(T, LSEG_CC_TSM / T) k_tile_cc(Shape sh, const 
                                                int32_t* __restrict__ hist, int64_t K) {
   pdl_trigger();
   pdl_wait();
-  __shared__ int s_par[TR * TC];
+  __shared__ int s_par[TR * TC + TC + 1];  // + padding: the edge gathering's reads below the last row
   __shared__ unsigned long long s_m[TR * 5];
   const int tilesC = (sh.Sk + TC - 1) / TC;
   const int tilesR = (sh.R + TR - 1) / TR;
