@@ -2149,13 +2149,15 @@ __global__ void __launch_bounds__(T, LSEG_PRUNE_TSM / T) k_prune_rows(Shape sh, 
   // histogram reads of a word are one coalesced load)
   {
     const int32_t* hf = hist + (int64_t)f * K + (int64_t)i * sh.Sk + 1;
+    const uint32_t* rbr = rbits + (int64_t)row * sh.Wk;
+    asm volatile("" : "+l"(hf), "+l"(rbr));  // row bases opaque: 32-bit offsets, one wide multiply-add each
     // the warp's words are w = warp + NW q: lane q loads word q's root bits,
     // then the histogram reads go out PA words at a time (3 dependent loads
     // per 32 words instead of 2 per word)
     constexpr int PA = 4;
     for (int wb = warp; wb < sh.Wk; wb += NW * 32) {
       const int wl = wb + lane * NW;
-      const uint32_t rbl = wl < sh.Wk ? __ldg(rbits + (int64_t)row * sh.Wk + wl) : 0u;
+      const uint32_t rbl = wl < sh.Wk ? __ldg(rbr + wl) : 0u;
       if (wl < sh.Wk) s_rbw[wl] = rbl;
       for (int q0 = 0; q0 < 32 && wb + q0 * NW < sh.Wk; q0 += PA) {
         uint32_t rq[PA];
@@ -2247,6 +2249,8 @@ __global__ void __launch_bounds__(T, LSEG_PRUNE_TSM / T) k_prune_rows(Shape sh, 
   }
   __syncthreads();
   const int64_t rb = (int64_t)row * S;
+  const int32_t* lin = lab_in + rb;
+  asm volatile("" : "+l"(lin));
   bool any = false;
   constexpr int PF = LSEG_PF_PRUNE;
   for (int s0 = 0; s0 < nw * 32; s0 += T * PF) {
@@ -2254,7 +2258,7 @@ __global__ void __launch_bounds__(T, LSEG_PRUNE_TSM / T) k_prune_rows(Shape sh, 
 #pragma unroll
     for (int j = 0; j < PF; ++j) {
       const int s = s0 + threadIdx.x + j * T;
-      lv[j] = (s < S) ? __ldcg(lab_in + rb + s) : 0;
+      lv[j] = (s < S) ? __ldcg(lin + s) : 0;
     }
 #pragma unroll
     for (int j = 0; j < PF; ++j) lv[j] = lv[j] > 0 ? __ldcg(rmf + lv[j] - 1) : 0;
