@@ -68,7 +68,7 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #define LSEG_CC_TSM 2048
 #endif
 #ifndef LSEG_LAB_TSM
-#define LSEG_LAB_TSM 2048
+#define LSEG_LAB_TSM 1280  // measured: 0.356 ms vs 0.367 at 2048, 0.405 at 1024
 #endif
 #ifndef LSEG_PRUNE_TSM
 #define LSEG_PRUNE_TSM 2048
@@ -1691,6 +1691,7 @@ __global__ void __launch_bounds__(T, LSEG_LAB_TSM / T) k_labels_backfill(lseg_se
   const uint32_t* rbf = rbits + (int64_t)f * sh.R * sh.Wk;
   const int32_t* rpf = rpre + (int64_t)f * sh.R * sh.Wk;
   const int64_t rb = (int64_t)row * S;
+  int32_t* outr = out + rb;
   // rbits_out != nullptr: k_root_flatten's work folded in (no node_labels
   // output): each column chases its tile-local root to the final root
   // itself, the row's final roots go to rbits_out and n_labels, and the
@@ -1751,7 +1752,7 @@ __global__ void __launch_bounds__(T, LSEG_LAB_TSM / T) k_labels_backfill(lseg_se
       if (direct) {  // k = 1: every cell but the backfill targets is final here
         const uint32_t tm = __ballot_sync(0xffffffffu, v == -2);
         if ((c & 31) == 0) s_ktw[c >> 5] = tm;
-        if (c < S && v != -2) out[(int64_t)row * S + c] = v > 0 ? v : 0;
+        if (c < S && v != -2) outr[c] = v > 0 ? v : 0;
         hist_add(hw, v > 0 ? v : 0);
       }
     }
@@ -1792,7 +1793,7 @@ __global__ void __launch_bounds__(T, LSEG_LAB_TSM / T) k_labels_backfill(lseg_se
       }
       if (node_labels)  // reference segment() output: 1 + rank of the root
         node_labels[rb + s] = (j == 0 && v > 0) ? rank_label(rbf, rpf, sh.Wk, sh.Sk, v - 1, sh.inv_Sk) : 0;
-      if (!direct || v == -2) out[rb + s] = r;
+      if (!direct || v == -2) outr[s] = r;
       else r = 0;  // written and counted in the first pass
     }
     hist_add(hw, r);
