@@ -67,6 +67,9 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_CC_TSM
 #define LSEG_CC_TSM 2048
 #endif
+#ifndef LSEG_MERGE_T
+#define LSEG_MERGE_T 128
+#endif
 #ifndef LSEG_LAB_TSM
 #define LSEG_LAB_TSM 1280  // measured: 0.356 ms vs 0.367 at 2048, 0.405 at 1024
 #endif
@@ -2354,7 +2357,7 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   const int64_t nt = (int64_t)sh.F * tilesR * tilesC;
   const dim3 tgrid(tilesC, tilesR, sh.F);  // frames <= 65535 (check_shape)
   const int per = tilesR * sh.Sk + tilesC * sh.R;
-  const int mt = sh.F < 8 ? 64 : 128;  // border-merge threads per CTA (more CTAs for single scans)
+  const int mt = sh.F < 8 ? 64 : LSEG_MERGE_T;  // border-merge threads per CTA (more CTAs for single scans)
   if (!exact_normals) {
     CertParams cp;
     for (int c = 0; c < 3; ++c) {
