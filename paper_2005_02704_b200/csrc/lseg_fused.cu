@@ -287,11 +287,28 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       const int g = (y + 1) * GC + (x + 1);
       unsigned m = 0;
       kind[j] = 0;
-      if (e < NT && y < TRe && x < TCe && s_id[g] >= 0) {
+      if (e < NT && y < TRe && x < TCe) {
+        // the mesh outputs (node ids, neighbours, node cells) need no
+        // normal: written here, while the neighbour ids are at hand
+        const int id = s_id[g];
+        if (node_ids) node_ids[nbase + (int64_t)(r0 + y) * sh.Sk + c0 + x] = id;
+        if (id >= 0) {
+          int nb[6];
 #pragma unroll
-        for (int s = 0; s < 6; ++s)
-          if (s_id[g + slot_dr(s) * GC + slot_dc(s)] >= 0 && !(s == 5 && sh.Sk == 2)) m |= 1u << s;  // mesh.py:96-101
-        kind[j] = (m == 0x3fu) ? 1 : 2;
+          for (int s = 0; s < 6; ++s) {
+            nb[s] = (s == 5 && sh.Sk == 2) ? -1 : s_id[g + slot_dr(s) * GC + slot_dc(s)];  // mesh.py:96-101
+            if (nb[s] >= 0) m |= 1u << s;
+          }
+          kind[j] = (m == 0x3fu) ? 1 : 2;
+          int2* o2 = reinterpret_cast<int2*>(neighbors + (nbase + id) * 6);  // 24 B rows, 8-B aligned
+          o2[0] = make_int2(nb[0], nb[1]);
+          o2[1] = make_int2(nb[2], nb[3]);
+          o2[2] = make_int2(nb[4], nb[5]);
+          if (node_rc) {  // the single-scan Mesh's node_rings / node_steps (mesh.py:115-117)
+            node_rc[(nbase + id) * 2] = r0 + y;
+            node_rc[(nbase + id) * 2 + 1] = (c0 + x) * sh.k;
+          }
+        }
       }
       ml[j] = (unsigned char)m;
       na += kind[j] == 1;
@@ -381,21 +398,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     const int rr = r0 + y, cc = c0 + x;
     const int g = (y + 1) * GC + (x + 1);
     const int id = s_id[g];
-    const int64_t cell = (int64_t)rr * sh.Sk + cc;
-    if (node_ids) node_ids[nbase + cell] = id;
-    if (id < 0) continue;
-    if (node_rc) {  // the single-scan Mesh's node_rings / node_steps (mesh.py:115-117)
-      node_rc[(nbase + id) * 2] = rr;
-      node_rc[(nbase + id) * 2 + 1] = cc * sh.k;
-    }
-    int nb[6];
-#pragma unroll
-    for (int s = 0; s < 6; ++s) nb[s] = s_id[g + slot_dr(s) * GC + slot_dc(s)];
-    if (sh.Sk == 2 && nb[5] == nb[2]) nb[5] = -1;
-    int2* o2 = reinterpret_cast<int2*>(neighbors + (nbase + id) * 6);  // 24 B rows, 8-B aligned
-    o2[0] = make_int2(nb[0], nb[1]);
-    o2[1] = make_int2(nb[2], nb[3]);
-    o2[2] = make_int2(nb[4], nb[5]);
+    if (id < 0) continue;  // (mesh outputs: written by the classification)
     const bool has = s_has[e];
     if (n32) {
       float* o = n32 + (nbase + id) * 3;
