@@ -457,8 +457,11 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   const int lane = tid & 31;
   const bool full_width = (c0 == 0 && TCe == sh.Sk);
   unsigned long long* mrow = masks + (((int64_t)f * tilesR + r0 / TR) * tilesC + c0 / TC) * (TR * 5);
-  for (int y = tid >> 5; y < TR; y += T / 32) {
-    unsigned long long H = 0, V0 = 0, V1 = 0, HS = 0;
+  static_assert(TR % (T / 32) == 0, "whole rows per warp");
+#pragma unroll
+  for (int yy = 0; yy < TR / (T / 32); ++yy) {
+    const int y = (tid >> 5) + yy * (T / 32);
+    uint32_t H[2], V0[2], V1[2], HS[2];  // 32-bit halves of the row masks
     bool w0 = false, w1 = false;
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
@@ -497,21 +500,21 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
           }
         }
       }
-      const unsigned long long sh_ = half ? 32 : 0;
-      H |= (unsigned long long)__ballot_sync(0xffffffffu, h) << sh_;
-      V0 |= (unsigned long long)__ballot_sync(0xffffffffu, v0) << sh_;
-      V1 |= (unsigned long long)__ballot_sync(0xffffffffu, v1) << sh_;
-      HS |= (unsigned long long)__ballot_sync(0xffffffffu, has) << sh_;
+      H[half] = __ballot_sync(0xffffffffu, h);
+      V0[half] = __ballot_sync(0xffffffffu, v0);
+      V1[half] = __ballot_sync(0xffffffffu, v1);
+      HS[half] = __ballot_sync(0xffffffffu, has);
     }
     unsigned W = 0u;
     if (full_width)  // block-uniform: the wrap bits exist only in a full-width tile
       W = (__ballot_sync(0xffffffffu, w0) ? 1u : 0u) | (__ballot_sync(0xffffffffu, w1) ? 2u : 0u);
-    if (lane == 0) {
-      mrow[y * 5 + 0] = H;
-      mrow[y * 5 + 1] = V0;
-      mrow[y * 5 + 2] = V1;
-      mrow[y * 5 + 3] = HS;
-      mrow[y * 5 + 4] = W;
+    if (lane == 0) {  // little-endian: the low half first
+      uint2* m2 = reinterpret_cast<uint2*>(mrow + y * 5);
+      m2[0] = make_uint2(H[0], H[1]);
+      m2[1] = make_uint2(V0[0], V0[1]);
+      m2[2] = make_uint2(V1[0], V1[1]);
+      m2[3] = make_uint2(HS[0], HS[1]);
+      m2[4] = make_uint2(W, 0u);
     }
   }
 #if LSEG_PHASES
