@@ -212,6 +212,12 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     double rv[NRA];
     uint32_t wv[NRA];
     int32_t pv[NRA];
+    // frame bases opaque to the optimiser (phase-local copies): 32-bit
+    // frame-local offsets, one wide multiply-add per load
+    const double* rfa = rf;
+    const uint32_t* vba = vbf;
+    const int32_t* wpa = wpf;
+    asm volatile("" : "+l"(rfa), "+l"(vba), "+l"(wpa));
 #pragma unroll
     for (int j = 0; j < NRA; ++j) {
       const int y = g + NG * j, rr = r0 - 1 + y;
@@ -219,9 +225,9 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       wv[j] = 0u;
       pv[j] = 0;
       if (y < GR && colok && rr >= 0 && rr < sh.R) {
-        rv[j] = __ldg(rf + (int64_t)rr * sh.S + coff);
-        wv[j] = __ldg(vbf + (int64_t)rr * sh.Wk + wo);
-        pv[j] = __ldg(wpf + (int64_t)rr * sh.Wk + wo);
+        rv[j] = __ldg(rfa + (rr * sh.S + (int)coff));
+        wv[j] = __ldg(vba + (rr * sh.Wk + wo));
+        pv[j] = __ldg(wpa + (rr * sh.Wk + wo));
       }
     }
     // halo columns: halo index 0 = column c0 - 1, index TCe + 1 = column
