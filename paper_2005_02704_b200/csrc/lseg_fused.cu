@@ -397,30 +397,36 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   __syncthreads();
   PH_MARK(3);
 
-  // C. per-node outputs
-  for (int e = tid; e < NT; e += T) {
-    const int y = e / TC, x = e - y * TC;
-    if (y >= TRe || x >= TCe) continue;
-    const int rr = r0 + y, cc = c0 + x;
-    const int g = (y + 1) * GC + (x + 1);
-    const int id = s_id[g];
-    if (id < 0) continue;  // (mesh outputs: written by the classification)
-    const bool has = s_has[e];
-    if (n32) {
-      float* o = n32 + (nbase + id) * 3;
-      const float qn = __int_as_float(0x7fc00000);
-      o[0] = has ? (float)s_nx[e] : qn;
-      o[1] = has ? (float)s_ny[e] : qn;
-      o[2] = has ? (float)s_nz[e] : qn;
+  // C. per-node normal outputs (phase-local opaque frame bases: 32-bit node
+  // ids, one wide multiply-add per store)
+  {
+    float* n32f = n32 ? n32 + nbase * 3 : nullptr;
+    uint8_t* nmf = nmask + nbase;
+    asm volatile("" : "+l"(n32f), "+l"(nmf));
+#pragma unroll
+    for (int j = 0; j < (NT + T - 1) / T; ++j) {
+      const int e = tid + j * T;
+      const int y = e / TC, x = e - y * TC;
+      if (e >= NT || y >= TRe || x >= TCe) continue;
+      const int id = s_id[(y + 1) * GC + (x + 1)];
+      if (id < 0) continue;  // (mesh outputs: written by the classification)
+      const bool has = s_has[e];
+      if (n32f) {
+        float* o = n32f + id * 3;
+        const float qn = __int_as_float(0x7fc00000);
+        o[0] = has ? (float)s_nx[e] : qn;
+        o[1] = has ? (float)s_ny[e] : qn;
+        o[2] = has ? (float)s_nz[e] : qn;
+      }
+      if (n64) {  // fp64 normals (the single-scan drop-in: reference NormalMap values)
+        double* o = n64 + (nbase + id) * 3;
+        const double qn = __longlong_as_double(0x7ff8000000000000LL);
+        o[0] = has ? s_nx[e] : qn;
+        o[1] = has ? s_ny[e] : qn;
+        o[2] = has ? s_nz[e] : qn;
+      }
+      nmf[id] = has ? 1 : 0;
     }
-    if (n64) {  // fp64 normals (the single-scan drop-in: reference NormalMap values)
-      double* o = n64 + (nbase + id) * 3;
-      const double qn = __longlong_as_double(0x7ff8000000000000LL);
-      o[0] = has ? s_nx[e] : qn;
-      o[1] = has ? s_ny[e] : qn;
-      o[2] = has ? s_nz[e] : qn;
-    }
-    nmask[nbase + id] = has ? 1 : 0;
   }
   // fp64 normals of the tile's border rows / columns for k_merge: only the
   // 2 TC + 2 TR border cells, one thread each (row stores coalesced)
