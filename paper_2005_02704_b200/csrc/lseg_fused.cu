@@ -1961,6 +1961,8 @@ __global__ void __launch_bounds__(T, LSEG_BIN_MINB) k_bin_rows(lseg_sensor sn, S
     return;
   }
   double* out = ranges + row * S;
+  uint32_t* vbr = vbits + row * sh.Wk;
+  asm volatile("" : "+l"(out), "+l"(vbr));  // row bases opaque: 32-bit offsets
   const int lane = threadIdx.x & 31;
   // every binned range passed the window test in bin_xyz: a cell is valid
   // iff it received a point (the empty pattern ~0 is a NaN)
@@ -1970,7 +1972,7 @@ __global__ void __launch_bounds__(T, LSEG_BIN_MINB) k_bin_rows(lseg_sensor sn, S
       const unsigned long long v = c < S ? s_cell[c] : ~0ull;
       if (c < S) out[c] = __longlong_as_double((long long)v);
       const uint32_t b = __ballot_sync(0xffffffffu, v != ~0ull);
-      if (lane == 0) vbits[row * sh.Wk + w] = b;
+      if (lane == 0) vbr[w] = b;
     }
     return;
   }
