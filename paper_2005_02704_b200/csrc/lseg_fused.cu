@@ -61,7 +61,7 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #define LSEG_PF_LAB 2
 #endif
 #ifndef LSEG_PF_PRUNE
-#define LSEG_PF_PRUNE 8
+#define LSEG_PF_PRUNE 16
 #endif
 // resident threads per SM the row kernels are compiled for (2048: 32 registers)
 #ifndef LSEG_CC_TSM
