@@ -56,7 +56,7 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_FOLD_FLATTEN
 #define LSEG_FOLD_FLATTEN 1
 #endif
-// loads in flight per thread in the row kernels (measured: labels 2, pruning 8)
+// loads in flight per thread in the row kernels (measured: labels 2, pruning 16)
 #ifndef LSEG_PF_LAB
 #define LSEG_PF_LAB 2
 #endif
@@ -1194,8 +1194,8 @@ __device__ __forceinline__ void tile_cc_body(const Shape& sh, int f, int r0, int
                                              uint32_t* __restrict__ lroots, int32_t* __restrict__ hist, int64_t K) {
   constexpr int NT = TR * TC;
   // run starts: parent of every cell = first cell of its horizontal run (the
-  // cell after the highest failing row edge below it), on 32-bit halves of
-  // the row mask: a warp's 32 cells lie in one half (warp-uniform branch)
+  // cell after the highest failing row edge below it), branch-free on the
+  // 32-bit halves of the row mask
   static_assert(NT % T == 0 && TC == 64 && T % 32 == 0, "each warp step covers a 32-cell chunk of one row");
   constexpr int NJ = NT / T;
   unsigned starts = 0;  // which of this thread's cells (tid + j T) are run starts
