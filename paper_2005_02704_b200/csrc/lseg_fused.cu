@@ -73,6 +73,9 @@ static constexpr bool kFastMath = LSEG_FAST_MATH;
 #ifndef LSEG_MERGE_T
 #define LSEG_MERGE_T 128
 #endif
+#ifndef LSEG_LAB_T
+#define LSEG_LAB_T 128  // labels threads per row in large batches
+#endif
 #ifndef LSEG_LAB_TSM
 #define LSEG_LAB_TSM 1280  // measured: 0.356 ms vs 0.367 at 2048, 0.405 at 1024
 #endif
@@ -2447,9 +2450,9 @@ void launch_fused_graph(const lseg_sensor& sn, const Shape& sh, const Workspace&
   const bool wide = (int64_t)sh.F * sh.R < num_sms() * 8;  // one-wave batches: 256 threads per row for latency
   const bool direct = sh.k == 1 && fold;  // (fold implies no segment() output)
   auto kern = wide ? (direct ? k_labels_backfill<256, true> : k_labels_backfill<256, false>)
-                   : (direct ? k_labels_backfill<128, true> : k_labels_backfill<128, false>);
+                   : (direct ? k_labels_backfill<LSEG_LAB_T, true> : k_labels_backfill<LSEG_LAB_T, false>);
   if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  launch_pdl(kern, sh.F * sh.R, wide ? 256 : 128, smem, st, sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits, ws.rpre,
+  launch_pdl(kern, sh.F * sh.R, wide ? 256 : LSEG_LAB_T, smem, st, sn, sh, ranges, ws.vbits, fb, ws.parent, ws.rbits, ws.rpre,
              node_labels, ws.lab_tmp, ws.hist, ws.K, fold ? ws.rbits : nullptr, n_labels, ws.rcnt, ws.fscal + 3);
   prof_mark("labels_backfill", st);
 }
