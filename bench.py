@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-e2e-full", action="store_true", help="skip the e2e line that returns the whole result")
     ap.add_argument("--no-latency", action="store_true", help="skip the single-scan latency lines")
     ap.add_argument("--no-accuracy", action="store_true", help="skip the suite accuracy (F1) line")
     ap.add_argument("--no-parity", action="store_true", help="skip the sampled-frame oracle check / E_near")
@@ -530,6 +531,7 @@ def main():
     # (f32 xyz + int32 ring ids, the config's input) in, pinned label grid out
     e2e = None
     e2e_alt = None
+    e2e_full = None
     if not a.no_e2e:
         hx = xyz.cpu().pin_memory()
         ho = off.cpu()
@@ -541,15 +543,16 @@ def main():
         bp = None
         torch.cuda.empty_cache()
 
-        def e2e_run(ring_h, rdt):
+        def e2e_run(ring_h, rdt, extra=None):
             sp = L.StreamingPipeline(cfg, a.interval, chunk_frames=cf, max_chunk_points=max(maxp, 1), device=dev,
                                      ring_dtype=rdt, normals=a.normals)
+            extra = extra or {}
             if F > 0:
                 for _ in range(2):
-                    sp.run_host(hx, ring_h, ho, hl)
+                    sp.run_host(hx, ring_h, ho, hl, **extra)
             torch.cuda.synchronize()
             barrier()
-            el = timed(lambda: sp.run_host(hx, ring_h, ho, hl), a.steps, st) if F > 0 else 0.0
+            el = timed(lambda: sp.run_host(hx, ring_h, ho, hl, **extra), a.steps, st) if F > 0 else 0.0
             te = torch.tensor([el], dtype=torch.float64, device=dev)
             if ws > 1:
                 torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
@@ -571,6 +574,22 @@ def main():
                    "d2h_bytes_per_step": int(d2h), "ms_per_step": t_seg / a.steps,
                    "ring_input": "int32 ring ids -> per-frame ring segment table on the host (timed), "
                                  "12 B per point on the wire"}
+        # the whole PipelineResult back on the host (reference pipeline.py:39-44):
+        # labels + Mesh.neighbors + node counts + NormalMap values (fp32) / mask
+        if F > 0 and not a.no_e2e_full:
+            cap = cfg.rings * _lib.kept_count(cfg.azimuth_steps, a.interval)
+            full = {"n_nodes_h": torch.empty(F, dtype=torch.int32).pin_memory(),
+                    "neighbors_h": torch.empty((F, cap, 6), dtype=torch.int32).pin_memory(),
+                    "normals_h": torch.empty((F, cap, 3), dtype=torch.float32).pin_memory(),
+                    "mask_h": torch.empty((F, cap), dtype=torch.uint8).pin_memory()}
+            t_full = e2e_run(hr, torch.int32, full)
+            d2h_full = d2h + sum(t.numel() * t.element_size() for t in full.values())
+            e2e_full = {"value": run["points"] / (t_full / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                        "d2h_bytes_per_step": int(d2h_full), "ms_per_step": t_full / a.steps,
+                        "returns": "labels (F,R,S) i32 + per frame: n_nodes, Mesh.neighbors (R*S',6) i32, "
+                                   "NormalMap values (R*S',3) f32 + mask (R*S') u8 (node-capacity rows)",
+                        "api": "StreamingPipeline.run_host(..., n_nodes_h, neighbors_h, normals_h, mask_h)"}
+            del full
         # the PCIe ceiling of the headline traffic: copy-only time of the same
         # bytes up and the label bytes down, concurrently on two streams
         if F > 0:
@@ -625,6 +644,7 @@ def main():
                 "roofline": roof, "pipeline_roofline": pipe_roof, "stages": per_stage,
                 "other_intervals": others, "near_threshold": near,
                 "cpu_baseline": main_cpu, "cpu_baselines": cpu, "e2e": e2e, "e2e_ring_segments": e2e_alt,
+                "e2e_full_result": e2e_full,
                 "gpu_launches": int(launches), "clocks": clk}
         if not a.no_latency:
             line["single_scan_latency"] = single_scan_latency(dev, a.normals)

@@ -162,23 +162,24 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
   // ranges + separable direction tables; positions are rebuilt on use
   // (5 multiplies) -- 19 KB less shared memory buys a 4th CTA per SM
   double* s_r = reinterpret_cast<double*>(s_dyn);
-  double* s_ct = s_r + GR * GC;   // cos(elev) per halo row
-  double* s_st = s_ct + GR;       // sin(elev) per halo row
-  double* s_cp = s_st + GR;       // cos(az) per halo column
-  double* s_sp = s_cp + GC;       // sin(az) per halo column
-  double* s_nx = s_sp + GC;
-  // position of halo cell (row yy, column xx): the row / column tables are
-  // indexed directly (no division), so a node's 7 lookups share their loads
+  double2* s_el = reinterpret_cast<double2*>(s_r + GR * GC);  // (cos, sin)(elev) per halo row
+  double2* s_az = s_el + GR;                                  // (cos, sin)(az) per halo column
+  double* s_nend = reinterpret_cast<double*>(s_az + GC);
+  // position of halo cell (row yy, column xx): one 16-B load per table
   auto posyx = [&](int yy, int xx) -> Vec3 {
-    const double ct = s_ct[yy], r = s_r[yy * GC + xx];
+    const double2 el = s_el[yy], az = s_az[xx];
+    const double r = s_r[yy * GC + xx];
     Vec3 q;
-    q.x = __dmul_rn(__dmul_rn(ct, s_cp[xx]), r);
-    q.y = __dmul_rn(__dmul_rn(ct, s_sp[xx]), r);
-    q.z = __dmul_rn(s_st[yy], r);
+    q.x = __dmul_rn(__dmul_rn(el.x, az.x), r);
+    q.y = __dmul_rn(__dmul_rn(el.x, az.y), r);
+    q.z = __dmul_rn(el.y, r);
     return q;
   };
-  double* s_ny = s_nx + NT;
-  double* s_nz = s_ny + NT;
+  // tile normals: (x, y) as one 16-B element, z apart
+  double2* s_nxy = reinterpret_cast<double2*>(s_nend);
+  double* s_nz = reinterpret_cast<double*>(s_nxy + NT);
+  auto nput = [&](int e, double x, double y, double z) { s_nxy[e] = make_double2(x, y); s_nz[e] = z; };
+  auto nget = [&](int e) -> Vec3 { const double2 v = s_nxy[e]; Vec3 q; q.x = v.x; q.y = v.y; q.z = s_nz[e]; return q; };
   int* s_id = reinterpret_cast<int*>(s_nz + NT);
   unsigned short* s_list = reinterpret_cast<unsigned short*>(s_id + GR * GC);  // fan6 list from the front, rest from the back
   uint8_t* s_has = reinterpret_cast<uint8_t*>(s_list + NT);
@@ -269,13 +270,11 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     for (int e = tid; e < GR + GC; e += T) {
       if (e < GR) {
         const int rr = min(max(r0 - 1 + e, 0), sh.R - 1);
-        s_ct[e] = __ldg(sn.cos_el + rr);
-        s_st[e] = __ldg(sn.sin_el + rr);
+        s_el[e] = make_double2(__ldg(sn.cos_el + rr), __ldg(sn.sin_el + rr));
       } else {
         int c = (c0 - 1 + (e - GR)) % sh.Sk;
         if (c < 0) c += sh.Sk;
-        s_cp[e - GR] = __ldg(sn.cos_az + (int64_t)c * sh.k);
-        s_sp[e - GR] = __ldg(sn.sin_az + (int64_t)c * sh.k);
+        s_az[e - GR] = make_double2(__ldg(sn.cos_az + (int64_t)c * sh.k), __ldg(sn.sin_az + (int64_t)c * sh.k));
       }
     }
   }
@@ -325,7 +324,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       ml[j] = (unsigned char)m;
       na += kind[j] == 1;
       nb += kind[j] == 2;
-      if (e < NT) { s_has[e] = 0; s_nx[e] = s_ny[e] = s_nz[e] = 0.0; }
+      if (e < NT) { s_has[e] = 0; nput(e, 0.0, 0.0, 0.0); }
     }
     // block-wide exclusive offsets of (na, nb): warp scan + per-warp totals
     int ia = na, ib = nb;
@@ -371,9 +370,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
     }
     const bool okn = fan.finish(p, nv);
     if (okn) {
-      s_nx[e] = nv[0];
-      s_ny[e] = nv[1];
-      s_nz[e] = nv[2];
+      nput(e, nv[0], nv[1], nv[2]);
       s_has[e] = 1;
     }
   }
@@ -394,9 +391,7 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       return posyx(y + 1 + dr, x + 1 + dc);
     };
     if (fan_subst<kFastMath>(p, m, pos, nv)) {
-      s_nx[e] = nv[0];
-      s_ny[e] = nv[1];
-      s_nz[e] = nv[2];
+      nput(e, nv[0], nv[1], nv[2]);
       s_has[e] = 1;
     }
   }
@@ -417,19 +412,20 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       const int id = s_id[(y + 1) * GC + (x + 1)];
       if (id < 0) continue;  // (mesh outputs: written by the classification)
       const bool has = s_has[e];
+      const Vec3 nv = nget(e);
       if (n32f) {
         float* o = n32f + id * 3;
         const float qn = __int_as_float(0x7fc00000);
-        o[0] = has ? (float)s_nx[e] : qn;
-        o[1] = has ? (float)s_ny[e] : qn;
-        o[2] = has ? (float)s_nz[e] : qn;
+        o[0] = has ? (float)nv.x : qn;
+        o[1] = has ? (float)nv.y : qn;
+        o[2] = has ? (float)nv.z : qn;
       }
       if (n64) {  // fp64 normals (the single-scan drop-in: reference NormalMap values)
         double* o = n64 + (nbase + id) * 3;
         const double qn = __longlong_as_double(0x7ff8000000000000LL);
-        o[0] = has ? s_nx[e] : qn;
-        o[1] = has ? s_ny[e] : qn;
-        o[2] = has ? s_nz[e] : qn;
+        o[0] = has ? nv.x : qn;
+        o[1] = has ? nv.y : qn;
+        o[2] = has ? nv.z : qn;
       }
       nmf[id] = has ? 1 : 0;
     }
@@ -457,7 +453,8 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
       const int e = y * TC + x;
       if (!s_has[e]) continue;
       double* o = rowside ? bf + bn_row(sh, 2 * tr + slot, c0 + x) : bf + bn_col(sh, TR, 2 * tc + slot, r0 + y);
-      bn_put(o, s_nx[e], s_ny[e], s_nz[e]);
+      const Vec3 nv = nget(e);
+      bn_put(o, nv.x, nv.y, nv.z);
     }
   }
 
@@ -493,11 +490,12 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
         const bool ph = has && x + 1 < TCe && s_has[e + 1];
         const bool pv0 = has && y + 1 < TRe && s_has[e + TC];
         const bool pv1 = has && y + 1 < TRe && x + 1 < TCe && s_has[e + TC + 1];
-        const double ax = s_nx[e], ay = s_ny[e], az = s_nz[e];
+        const Vec3 a = nget(e);
         auto pass = [&](int q) -> bool {
-          const bool c0 = fabs(__dsub_rn(s_nx[q], ax)) < t0;
-          const bool c1 = fabs(__dsub_rn(s_ny[q], ay)) < t1;
-          const bool c2 = fabs(__dsub_rn(s_nz[q], az)) < t2;
+          const Vec3 b = nget(q);
+          const bool c0 = fabs(__dsub_rn(b.x, a.x)) < t0;
+          const bool c1 = fabs(__dsub_rn(b.y, a.y)) < t1;
+          const bool c2 = fabs(__dsub_rn(b.z, a.z)) < t2;
           return c0 & c1 & c2;
         };
         h = ph & pass(ph ? e + 1 : e);
@@ -505,15 +503,18 @@ __global__ void __launch_bounds__(T, LSEG_TILE_MINB) k_tile(lseg_sensor sn, Shap
         v1 = pv1 & pass(pv1 ? e + TC + 1 : e);
       }
       if (has && full_width && x == TCe - 1) {  // the column wrap of a full-width tile (rare)
-        const double a[3] = {s_nx[e], s_ny[e], s_nz[e]};
+        const Vec3 av = nget(e);
+        const double a[3] = {av.x, av.y, av.z};
         if (full_width && x == TCe - 1) {
           const int e0 = y * TC;  // (y, 0)
           if (TCe > 1 && s_has[e0]) {
-            const double q[3] = {s_nx[e0], s_ny[e0], s_nz[e0]};
+            const Vec3 qv = nget(e0);
+            const double q[3] = {qv.x, qv.y, qv.z};
             w0 = normals_pass(a, q, t0, t1, t2);
           }
           if (y + 1 < TRe && s_has[e0 + TC]) {
-            const double q[3] = {s_nx[e0 + TC], s_ny[e0 + TC], s_nz[e0 + TC]};
+            const Vec3 qv = nget(e0 + TC);
+            const double q[3] = {qv.x, qv.y, qv.z};
             w1 = normals_pass(a, q, t0, t1, t2);
           }
         }

@@ -367,13 +367,23 @@ class StreamingPipeline:
         self.loaded = [torch.cuda.Event() for _ in range(2)]
         self.computed = [torch.cuda.Event() for _ in range(2)]
 
-    def run_host(self, xyz_h, ring_h, offsets_h, labels_h):
+    def run_host(self, xyz_h, ring_h, offsets_h, labels_h, n_nodes_h=None, neighbors_h=None, normals_h=None,
+                 mask_h=None):
         """xyz_h (P,3) f32, ring_h (P,) i32 / u8 (with ring_dtype="segments",
         the (F, R+1) i64 table of ``ring_segments``; with "segments_from_ids",
         (P,) i32 ring ids converted per chunk on the host), offsets_h (F+1,) i64 host
         tensors (pinned); labels_h (F,R,S) i32 pinned output.  Enqueues everything and
-        returns; synchronise on the current stream to wait."""
+        returns; synchronise on the current stream to wait.
+
+        The rest of the reference's PipelineResult (pipeline.py:39-44) per
+        frame, when the optional pinned outputs are given: n_nodes_h (F,) i32,
+        neighbors_h (F, R*S', 6) i32 (Mesh.neighbors, rows [0, n_nodes) valid),
+        normals_h (F, R*S', 3) f32 and mask_h (F, R*S') u8 (NormalMap values /
+        mask; NaN where absent).  Whole node-capacity rows are copied so the
+        stream never waits on a node count."""
         F = offsets_h.numel() - 1
+        extra = [(h, name) for h, name in ((n_nodes_h, "n_nodes"), (neighbors_h, "neighbors"),
+                                           (normals_h, "normals"), (mask_h, "nmask")) if h is not None]
         offs = offsets_h.tolist()
         cur = torch.cuda.current_stream(self.device)
         start = torch.cuda.Event()
@@ -422,6 +432,8 @@ class StreamingPipeline:
             with torch.cuda.stream(self.s_out):
                 self.s_out.wait_event(self.computed[b])
                 labels_h[f0:f1].copy_(bp.labels[:nf], non_blocking=True)
+                for h, name in extra:
+                    h[f0:f1].copy_(getattr(bp, name)[:nf], non_blocking=True)
                 self.freed[b].record(self.s_out)
         cur.wait_stream(self.s_out)
         cur.wait_stream(self.s_run)

@@ -296,6 +296,24 @@ def test_streaming_pipeline_host_to_host(L):
     sp2.run_host(hx, hs, ho, hl2)
     torch.cuda.synchronize()
     assert torch.equal(hl2, want)
+    # the whole result on the host (labels + mesh + normals), int32 rings,
+    # 3 chunks of unequal size (2, 2, 1 frames)
+    cap = ref.cap
+    full = {"n_nodes_h": torch.zeros(5, dtype=torch.int32).pin_memory(),
+            "neighbors_h": torch.zeros((5, cap, 6), dtype=torch.int32).pin_memory(),
+            "normals_h": torch.zeros((5, cap, 3), dtype=torch.float32).pin_memory(),
+            "mask_h": torch.zeros((5, cap), dtype=torch.uint8).pin_memory()}
+    hl3 = torch.zeros_like(hl).pin_memory()
+    sp3 = L.StreamingPipeline(cfg, 1, chunk_frames=2, device="cuda", ring_dtype=torch.int32)
+    sp3.run_host(hx, ring.cpu().pin_memory(), ho, hl3, **full)
+    torch.cuda.synchronize()
+    assert torch.equal(hl3, want)
+    assert torch.equal(full["n_nodes_h"], ref.n_nodes.cpu())
+    for f in range(5):
+        n = int(ref.n_nodes[f])
+        assert torch.equal(full["neighbors_h"][f, :n], ref.neighbors[f, :n].cpu())
+        assert torch.equal(full["mask_h"][f, :n], ref.nmask[f, :n].cpu())
+        assert torch.equal(full["normals_h"][f, :n].view(torch.int32), ref.normals[f, :n].cpu().view(torch.int32))
 
 
 @pytest.mark.parametrize("shape_name,frames,seed", [("hdl64", 4, 21), ("stress", 1, 22), ("vlp16", 8, 23)])
