@@ -400,7 +400,10 @@ def main():
 
     from paper_2005_02704_b200 import dist as D
     ws, rank, local = D.env()
-    if ws > 1:
+    # under torchrun the NCCL path runs at any world size (a 1-rank launch
+    # exercises the communicator, the barriers and the final all-reduces too)
+    use_dist = ws > 1 or "TORCHELASTIC_RUN_ID" in os.environ
+    if use_dist:
         # NCCL's init report (communicator rank count, transport) on stderr:
         # the only NCCL traffic is the barriers and the final all-reduces
         os.environ.setdefault("NCCL_DEBUG", "INFO")
@@ -421,7 +424,7 @@ def main():
     st = torch.cuda.current_stream()
 
     def barrier():
-        if ws > 1:
+        if use_dist:
             torch.distributed.barrier()
 
     bp = None
@@ -554,7 +557,7 @@ def main():
             barrier()
             el = timed(lambda: sp.run_host(hx, ring_h, ho, hl, **extra), a.steps, st) if F > 0 else 0.0
             te = torch.tensor([el], dtype=torch.float64, device=dev)
-            if ws > 1:
+            if use_dist:
                 torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
             del sp
             return float(te.item())
@@ -651,7 +654,7 @@ def main():
         if not a.no_accuracy:
             line["accuracy_vs_truth"] = suite_accuracy(dev, a.normals)
         print(json.dumps(line), flush=True)
-    if ws > 1:
+    if use_dist:
         torch.distributed.destroy_process_group()
 
 

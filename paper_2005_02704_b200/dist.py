@@ -63,7 +63,7 @@ def reduce_run(points: int, frames: int, segments: int, elapsed_ms: float, devic
     dev = torch.device(device) if device is not None else torch.device("cpu")
     sums = torch.tensor([float(points), float(frames), float(segments)], dtype=torch.float64, device=dev)
     mx = torch.tensor([float(elapsed_ms)], dtype=torch.float64, device=dev)
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+    if dist.is_available() and dist.is_initialized():
         # pack max into the same collective: max(t) = -min(-t) is not a sum,
         # so two calls on 4 scalars -- still latency-only (~10 us on NVLink)
         dist.all_reduce(sums, op=dist.ReduceOp.SUM)
