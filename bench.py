@@ -408,7 +408,10 @@ def main():
         # the only NCCL traffic is the barriers and the final all-reduces
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        # to a per-process file (NCCL's default is stdout, which carries the
+        # JSON line; /dev/stderr is truncated when redirected): the init
+        # lines are copied to stderr at the end of the run
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/lseg_nccl.%p.log")
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
@@ -656,6 +659,12 @@ def main():
         print(json.dumps(line), flush=True)
     if use_dist:
         torch.distributed.destroy_process_group()
+        log = os.environ["NCCL_DEBUG_FILE"].replace("%p", str(os.getpid()))
+        if os.path.exists(log):
+            for ln in open(log, errors="replace"):
+                if "nranks" in ln or "Init COMPLETE" in ln or "NCCL version" in ln:
+                    sys.stderr.write(f"[rank {rank}] {ln}")
+            sys.stderr.flush()
 
 
 if __name__ == "__main__":
