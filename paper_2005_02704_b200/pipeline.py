@@ -118,6 +118,7 @@ def run_pipeline(scan: ScanGrid, cfg: PipelineConfig, interval: int | None = Non
         wsb = _lib.workspace_bytes(1, R, S, interval)
         bufs = {"ws": torch.empty(wsb, dtype=torch.uint8, device=dev), "wsb": wsb,
                 "ranges": torch.empty((1, R, S), dtype=torch.float64, device=dev),
+                "ranges_h": torch.empty((1, R, S), dtype=torch.float64, pin_memory=True),
                 "node_ids": torch.empty((1, R, Sk), dtype=torch.int32, device=dev),
                 "neighbors": torch.empty((1, cap, 6), dtype=torch.int32, device=dev),
                 "n64": torch.empty((1, cap, 3), dtype=torch.float64, device=dev),
@@ -128,7 +129,9 @@ def run_pipeline(scan: ScanGrid, cfg: PipelineConfig, interval: int | None = Non
         cache.clear()  # keep one shape's buffers
         cache[key] = bufs
     b = bufs
-    b["ranges"].copy_(torch.from_numpy(np.array(scan.ranges, dtype=np.float64, copy=True)).view(1, R, S))
+    # staged through a cached pinned buffer: one host memcpy, one async H2D
+    np.copyto(b["ranges_h"].numpy()[0], scan.ranges, casting="same_kind")
+    b["ranges"].copy_(b["ranges_h"], non_blocking=True)
     _lib.profile_begin()
     _lib.check(L.lseg_run_scans(sn, 1, interval, _lib.thresholds_arg(seg.thresholds), int(seg.min_segment_size),
                                 _lib.ptr(b["ranges"]), _lib.ptr(b["node_ids"]), _lib.ptr(b["neighbors"]),
@@ -148,8 +151,7 @@ def run_pipeline(scan: ScanGrid, cfg: PipelineConfig, interval: int | None = Non
     labels = h["labels"].numpy()
     nb = h["neighbors"].numpy()[:n]
     m = h["nmask"].numpy()[:n].view(np.bool_)
-    vals = h["n64"].numpy()[:n]
-    vals[~m] = np.nan
+    vals = h["n64"].numpy()[:n]  # NaN rows where the mask is False: written by the tile kernel
     cells = h["cells"].numpy()[:n]
     mesh = Mesh(rings=R, full_steps=S, interval=interval, kept_steps=kept, node_rings=cells[:, 0],
                 node_steps=cells[:, 1].astype(np.int64), node_ids=node_ids, neighbors=nb)
