@@ -87,6 +87,10 @@ def test_single_scan_api_matches_reference_fixture(L, name):
         assert res.mesh.n_nodes == int(g[f"k{k}_n_nodes"])
         assert digest(res.mesh.neighbors.astype(np.int32)) == str(g[f"k{k}_neighbors"])
         assert normals_digest(res.normals.values, res.normals.mask, np.float64) == str(g[f"k{k}_n64"])
+        # reference NormalMap contract (normals.py:94-145): rows without a normal are NaN
+        # (written by the tile kernel, not patched on the host)
+        assert np.isnan(res.normals.values[~res.normals.mask]).all()
+        assert not np.isnan(res.normals.values[res.normals.mask]).any()
         near = near_threshold_edges(res.mesh.neighbors, res.normals.values, res.normals.mask, g["thr"])
         assert near == (int(g[f"k{k}_e_near"]), int(g[f"k{k}_e_fwd"]))
 
