@@ -406,7 +406,9 @@ def main():
     if use_dist:
         # NCCL's init report (communicator rank count, transport) on stderr:
         # the only NCCL traffic is the barriers and the final all-reduces
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        # (forced up to INFO: the GPU boxes export a lower NCCL_DEBUG level)
+        if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+            os.environ["NCCL_DEBUG"] = "INFO"
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         # to a per-process file (NCCL's default is stdout, which carries the
         # JSON line; /dev/stderr is truncated when redirected): the init
