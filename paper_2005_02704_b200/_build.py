@@ -41,7 +41,8 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
 
     def compile_one(src):
         obj = os.path.join(objdir, src.rsplit(".", 1)[0] + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, *["-D" + d for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
+        extra = os.environ.get("LSEG_NVCC_FLAGS", "").split()  # experiments only (tools/variants2.sh)
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, *["-D" + d for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
