@@ -470,6 +470,7 @@ def main():
     peak, peak_kind = measured_peak_hbm()
     alg = alg_stage_bytes(P, C, Ck, N)
     des = design_stage_bytes(P, C, Ck, N, a.interval)
+    streams_used = bp.nstreams if bp is not None else 0
     timed_stages = stages  # launch counts of the timed region
     stage_step_ms = ms_step  # the step the stage shares refer to
     stages_from = "timed region"
@@ -669,8 +670,10 @@ def main():
                            "interval": a.interval, "frames_total": run["frames"] // a.steps,
                            "frames_rank0": F, "points_rank0": P, "nodes_rank0": N,
                            "parallelism": f"frame-shard x{ws} ({a.scaling})", "normals": a.normals,
-                           "streams_per_rank": (bp.nstreams if bp is not None else 0),
-                           "l2": "inputs (~1 GB per step) exceed the 126 MB L2; no flush needed"},
+                           "streams_per_rank": streams_used,
+                           "l2": f"a step reads {16 * P / 1e6:.0f} MB of points and moves {pb / 1e6:.0f} MB of "
+                                 "SURVEY 8(d) bytes (grid, mesh, normals, labels), several times the 126 MB L2, "
+                                 "so every step re-reads its inputs from HBM; no flush needed"},
                 "frames_per_s": run["frames"] / (ms / 1e3),
                 "final_segments_per_frame": run["segments"] / max(run["frames"], 1),
                 "roofline": roof, "pipeline_roofline": pipe_roof, "stages": per_stage,
